@@ -1,0 +1,157 @@
+/*
+ * cyclicot.h — C ABI of the B200-native (sm_100a) hot path of
+ *   "Optimal Transport with Cyclic Symmetry" (arXiv 2311.13147; /root/reference/PAPER.md = P).
+ *
+ * Problem (Assumption 1): d = n*m; the marginals are n stacked copies of alpha, beta in
+ * R^m_{>0}; the d x d cost is block-circulant, block (r, s) = C_{(s - r) mod n}
+ * (P:161-168). Everything here works on the REDUCED data: the n cost blocks C_0..C_{n-1}.
+ *
+ * Conventions shared by every entry point
+ *   - Pointers are caller-owned DEVICE memory unless a comment says HOST. Arrays are dense, row-major,
+ *     contiguous; the library never allocates persistent device memory and never frees caller memory.
+ *     Scratch lives in a caller-provided workspace of cot_workspace_bytes(...) bytes.
+ *   - Layouts (B = number of independent problems in the batch, B >= 1):
+ *       C       [B][n][m][m]  cost blocks, block k row-major (C[b][k][i][j] = C_ijk of problem b)
+ *       G       [B][m][m]     aggregated cost (same dtype as C);  argmin [B][m][m] int32
+ *       alpha   [B][m], beta [B][m]   float64, every entry > 0, sum(alpha_b) == sum(beta_b)
+ *                                      (the library checks this to 1e-6 relative; convention 1/n)
+ *       eps     [B]           float64 > 0 (the paper's lambda)
+ *       w_hat, z_hat [B][m]   float64 SCALED dual potentials w/eps, z/eps
+ *       T_full  [B][d][d]     dense plan, same dtype as C
+ *   - dtype: COT_F32 (float) or COT_F64 (double) for C, G, S, T.
+ *   - stream: a cudaStream_t passed as void*. All work is enqueued on it; calls are asynchronous
+ *     unless the comment says "synchronises".
+ *   - Every function returns a cot_status. Negative = error (nothing useful was written; the
+ *     message is in cot_last_error(), which is thread-local). COT_NOT_CONVERGED (> 0) is a warning:
+ *     outputs are valid.
+ *   - Reported objective values are FULL-problem scale (x n).
+ *   - No CPU fallback: every compute step runs in the sm_100a kernels of this library.
+ */
+#ifndef CYCLICOT_H
+#define CYCLICOT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COT_ABI_VERSION 1
+
+typedef enum { COT_F32 = 0, COT_F64 = 1 } cot_dtype;
+
+typedef enum {
+  COT_OK = 0,
+  COT_NOT_CONVERGED = 1,   /* warning: max_iter reached before tol; outputs valid                     */
+  COT_E_ARG = -1,          /* n < 1, m < 1, B < 1, NULL required pointer, bad dtype, eps <= 0, ...     */
+  COT_E_NONFINITE = -2,    /* a cost entry is NaN or +-Inf                                 */
+  COT_E_MARGINAL = -3,     /* alpha_i <= 0, beta_j <= 0, or |sum alpha - sum beta| > 1e-6 relative    */
+  COT_E_CUDA = -4,         /* a CUDA runtime error (message in cot_last_error)                         */
+  COT_E_NCCL = -5,         /* an NCCL error in the sharded path                                        */
+  COT_E_WORKSPACE = -6,    /* ws_bytes < cot_workspace_bytes(...) or misaligned workspace              */
+  COT_E_UNDERFLOW = -7     /* a column sum fell below 1e-28 in the fp32 path (eps too small)*/
+} cot_status;
+
+/* Flags for cerot_* */
+#define COT_COLD_START 0x1u   /* start from q = 1_m, i.e. z_hat = 0 (Alg. 2 line 2); otherwise
+                                 z_hat is a warm start                                                  */
+#define COT_FORCE_LDG  0x2u   /* use the generic LDG row kernel even where the TMA kernel applies     */
+
+/* Layout of one problem's report (HOST struct; the device report is the same 8 doubles + 2 ints). */
+typedef struct {
+  double objective;   /* transport cost n * sum_k <C_k, T_k>       (Table 1 'Obj. value')      */
+  double reg_primal;  /* objective + n*eps*sum T (log T - 1)       (eq. problem_CROT)      */
+  double dual;        /* n * (<w,alpha> + <z,beta> - eps sum T)    (eq. dual_problem_cyclic_ROT)      */
+  double row_l1;      /* || T 1_d - a ||_1 of the full plan                                            */
+  double col_l1;      /* || T^T 1_d - b ||_1                                                           */
+  double col_l2;      /* || T^T 1_d - b ||_2   (the marginal error of Sec. 6.1)                */
+  double mass;        /* sum of the full plan                                                          */
+  double residual;    /* last convergence monitor n*sum_j|c_j - beta_j| after a p-update */
+  int64_t iters;      /* iterations performed                                                          */
+  int32_t converged;  /* 1 if the monitor reached tol                                                  */
+  int32_t status;     /* per-problem cot_status                                                        */
+} cot_report;
+
+int cot_abi_version(void);
+const char* cot_last_error(void);
+
+/* Bytes of scratch needed by cerot_* for this shape on the current device (includes G and argmin for
+ * cerot_solve, the fp64 column partials, the per-problem solver state and the plan reductions). */
+size_t cot_workspace_bytes(int64_t B, int64_t n, int64_t m, int dtype);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* A2  C-LOT aggregation (Alg. 1 line 1).                                                   */
+/*   G[b][i][j] = min_k C[b][k][i][j]            (eq. definition_G)                       */
+/*   argmin[b][i][j] = the SMALLEST k attaining it (tie remark P:291); G is the value stored   */
+/*   at that k, so the sign of zero is deterministic. Comparisons only: bit-exact.                    */
+/*   d_nonfinite (DEVICE int32, may be NULL): receives the number of NaN/Inf entries of C (it is     */
+/*   overwritten, not accumulated). Asynchronous; use cot_check_nonfinite to turn it into a status.   */
+int clot_aggregate(const void* C, int64_t B, int64_t n, int64_t m, int dtype,
+                   void* G, int32_t* argmin, int32_t* d_nonfinite, void* stream);
+
+/* Synchronises `stream`, reads *d_nonfinite and returns COT_E_NONFINITE if it is > 0, else COT_OK. */
+int cot_check_nonfinite(const int32_t* d_nonfinite, void* stream);
+
+/* A6  Dense d x d block-circulant expansion (Lemma 1, eq. blkstr_optimal_solution).      */
+/*   argmin != NULL  (C-LOT, Alg. 1 lines 3-6): S is [B][m][m];                           */
+/*       T_full[b][r*m+i][s*m+j] = S[b][i][j] if argmin[b][i][j] == (s - r) mod n, else 0            */
+/*       (the lift of eq. optimal_solution_problem_CLOT, placed by Lemma 1).               */
+/*   argmin == NULL  (C-EROT blocks, Alg. 2 line 10): S is T_blocks [B][n][m][m];              */
+/*       T_full[b][r*m+i][s*m+j] = T_blocks[b][(s - r) mod n][i][j].                                   */
+/*   Pure placement: bit-exact copies. T_full must hold B*d*d elements.                               */
+int clot_expand(const void* S, const int32_t* argmin, int64_t B, int64_t n, int64_t m, int dtype,
+                void* T_full, void* stream);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* A3+A4  Cyclic Sinkhorn iterations (Alg. 2 lines 3-6) in the log domain of             */
+/* eq. optimal_f_sinkhorn_logdomain. One iteration = p-update then q-update:            */
+/*   for each row i:  s_ij = sum_k exp((G_ij - C_ijk)/eps)            (streamed, never cached)      */
+/*                    x_ij = z_hat_j - G_ij/eps,  M_i = max_j x_ij                                  */
+/*                    r_i = sum_j s_ij exp(x_ij - M_i)                                              */
+/*                    w_hat_i = log alpha_i - M_i - log r_i                                         */
+/*   for each column: c_j = sum_i (alpha_i/r_i) s_ij exp(x_ij - M_i)   (plan column sum after p)    */
+/*                    z_hat_j += log beta_j - log c_j                  (q-update)            */
+/*                    monitor  n * sum_j |c_j - beta_j|                   */
+/* G must be clot_aggregate's output for the same C (it is the exact per-(i,j) maximum of -C/eps).  */
+/* cerot_init: resets the solver state in `workspace` (iteration counters, convergence flags) and,  */
+/*   with COT_COLD_START, sets z_hat = 0 (q = 1_m). It validates alpha, beta on the device;   */
+/*   a violation is reported by cerot_state / cerot_solve as COT_E_MARGINAL.                          */
+/* cerot_iter: enqueues exactly `iters` iterations (asynchronous). With tol > 0, a problem whose      */
+/*   monitor is <= tol at an iteration t with t % check_every == 0 is frozen after that iteration's  */
+/*   q-update (its potentials stop changing), exactly as the oracle's stopping rule.                 */
+int cerot_init(const double* alpha, const double* beta, int64_t B, int64_t m, uint32_t flags,
+               double* z_hat, void* workspace, size_t ws_bytes, void* stream);
+int cerot_iter(const double* alpha, const double* beta, const void* C, const void* G,
+               int64_t B, int64_t n, int64_t m, int dtype, const double* eps,
+               int64_t iters, double tol, int64_t check_every, uint32_t flags,
+               double* w_hat, double* z_hat, void* workspace, size_t ws_bytes, void* stream);
+/* Synchronises `stream` and copies the per-problem state to HOST arrays (any may be NULL):         */
+/*   iters_done[B] (int64), converged[B] (int32), residual[B] (double). Returns COT_E_MARGINAL,     */
+/*   COT_E_UNDERFLOW if the device flagged one, else COT_OK.                                          */
+int cerot_state(const void* workspace, int64_t B, int64_t m, int64_t n, int dtype,
+                int64_t* iters_done, int32_t* converged, double* residual, void* stream);
+
+/* A5  Plan reconstruction (Alg. 2 lines 7-9; eq. optimality_condition):     */
+/*   T[b][k][i][j] = exp(w_hat_i + z_hat_j - C_ijk/eps)  written if T_blocks != NULL, and the       */
+/*   fp64 reductions of cot_report (objective, reg_primal, dual, row/col residuals, mass) written    */
+/*   to d_report (DEVICE, [B][8] doubles in cot_report field order; may be NULL). Asynchronous.       */
+int cerot_plan(const double* alpha, const double* beta, const void* C, const void* G,
+               int64_t B, int64_t n, int64_t m, int dtype, const double* eps,
+               const double* w_hat, const double* z_hat, void* T_blocks, double* d_report,
+               void* workspace, size_t ws_bytes, void* stream);
+
+/* Whole C-EROT solve (A2..A5): clot_aggregate into the workspace, cerot_init, iterations in chunks  */
+/* of check_every until every problem converged (tol > 0) or max_iter, then cerot_plan. Synchronises.*/
+/* report: HOST array of B cot_report. T_blocks may be NULL. Returns COT_OK, COT_NOT_CONVERGED if    */
+/* some problem did not reach tol (tol > 0), or an error.                                             */
+int cerot_solve(const double* alpha, const double* beta, const void* C,
+                int64_t B, int64_t n, int64_t m, int dtype, const double* eps,
+                double tol, int64_t max_iter, int64_t check_every, uint32_t flags,
+                double* w_hat, double* z_hat, void* T_blocks,
+                void* workspace, size_t ws_bytes, cot_report* report, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CYCLICOT_H */

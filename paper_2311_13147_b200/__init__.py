@@ -1,0 +1,237 @@
+"""paper_2311_13147_b200 — B200-native (sm_100a) hot path of "Optimal Transport with Cyclic Symmetry"
+(arXiv 2311.13147): C-LOT aggregation, cyclic Sinkhorn (C-EROT) iterations, plan reconstruction and the
+d x d block-circulant expansion, behind the C ABI of include/cyclicot.h (libcyclicot.so).
+
+This module is a thin ctypes binding: it marshals torch tensors (device memory, streams) into the C ABI
+and raises on error codes. Every step of the path runs in the library's CUDA kernels; there is no CPU
+fallback — if libcyclicot.so is missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcyclicot.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "cyclicot.h")
+
+COT_F32, COT_F64 = 0, 1
+COT_COLD_START, COT_FORCE_LDG = 0x1, 0x2
+STATUS = {0: "COT_OK", 1: "COT_NOT_CONVERGED", -1: "COT_E_ARG", -2: "COT_E_NONFINITE", -3: "COT_E_MARGINAL",
+          -4: "COT_E_CUDA", -5: "COT_E_NCCL", -6: "COT_E_WORKSPACE", -7: "COT_E_UNDERFLOW"}
+REPORT_FIELDS = ("objective", "reg_primal", "dual", "row_l1", "col_l1", "col_l2", "mass", "residual")
+
+
+class CotError(RuntimeError):
+    def __init__(self, code: int, fn: str, msg: str):
+        super().__init__(f"{fn}: {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class cot_report(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_double) for f in REPORT_FIELDS] + [
+        ("iters", ctypes.c_int64), ("converged", ctypes.c_int32), ("status", ctypes.c_int32)]
+
+
+_lib = None
+_vp, _i64, _i32, _u32, _dbl, _sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32,
+                                    ctypes.c_double, ctypes.c_size_t)
+
+_SIGS = {
+    "cot_abi_version": (ctypes.c_int, []),
+    "cot_last_error": (ctypes.c_char_p, []),
+    "cot_workspace_bytes": (_sz, [_i64, _i64, _i64, ctypes.c_int]),
+    "clot_aggregate": (ctypes.c_int, [_vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "cot_check_nonfinite": (ctypes.c_int, [_vp, _vp]),
+    "clot_expand": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp]),
+    "cerot_init": (ctypes.c_int, [_vp, _vp, _i64, _i64, _u32, _vp, _vp, _sz, _vp]),
+    "cerot_iter": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl, _i64, _u32,
+                                  _vp, _vp, _vp, _sz, _vp]),
+    "cerot_state": (ctypes.c_int, [_vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "cerot_plan": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
+                                  _sz, _vp]),
+    "cerot_solve": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _dbl, _i64, _i64, _u32, _vp,
+                                   _vp, _vp, _vp, _sz, ctypes.POINTER(cot_report), _vp]),
+}
+
+
+def lib():
+    """Load libcyclicot.so (built in-tree by __graft_entry__.build()). Raises if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(code: int, fn: str, ok=(0,)):
+    if code not in ok:
+        raise CotError(code, fn, lib().cot_last_error().decode())
+    return code
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype == torch.float32:
+        return COT_F32
+    if t.dtype == torch.float64:
+        return COT_F64
+    raise TypeError(f"cost dtype must be float32 or float64, got {t.dtype}")
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("tensor must live in CUDA device memory")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _shape(C):
+    """(B, n, m, batched) from C [n][m][m] or [B][n][m][m]."""
+    if C.dim() == 3:
+        return 1, C.shape[0], C.shape[1], False
+    if C.dim() == 4:
+        return C.shape[0], C.shape[1], C.shape[2], True
+    raise ValueError("C must be [n][m][m] or [B][n][m][m]")
+
+
+# ------------------------------------------------------------------------------------ C-LOT
+def clot_aggregate(C, G=None, argmin=None, nonfinite=None, stream=None, check=True):
+    """G = min_k C_k and the smallest argmin. Returns (G, argmin)."""
+    import torch
+    B, n, m, batched = _shape(C)
+    shp = (B, m, m) if batched else (m, m)
+    G = torch.empty(shp, dtype=C.dtype, device=C.device) if G is None else G
+    argmin = torch.empty(shp, dtype=torch.int32, device=C.device) if argmin is None else argmin
+    if check and nonfinite is None:
+        nonfinite = torch.zeros(1, dtype=torch.int32, device=C.device)
+    s = _stream(stream)
+    _check(lib().clot_aggregate(_ptr(C), B, n, m, _dtype_code(C), _ptr(G), _ptr(argmin), _ptr(nonfinite), s),
+           "clot_aggregate")
+    if check:
+        _check(lib().cot_check_nonfinite(_ptr(nonfinite), s), "clot_aggregate")
+    return G, argmin
+
+
+def clot_expand(S, n: int, argmin=None, out=None, stream=None):
+    """Dense d x d block-circulant plan (Lemma 1). With argmin: S is the small LOT solution
+    [.., m, m] lifted by eq. optimal_solution_problem_CLOT; without: S is the n blocks [.., n, m, m]."""
+    import torch
+    if argmin is not None:
+        batched = S.dim() == 3
+        B = S.shape[0] if batched else 1
+        m = S.shape[-1]
+    else:
+        batched = S.dim() == 4
+        B = S.shape[0] if batched else 1
+        m = S.shape[-1]
+        assert S.shape[-3] == n
+    d = n * m
+    shp = (B, d, d) if batched else (d, d)
+    out = torch.empty(shp, dtype=S.dtype, device=S.device) if out is None else out
+    _check(lib().clot_expand(_ptr(S), _ptr(argmin), B, n, m, _dtype_code(S), _ptr(out), _stream(stream)),
+           "clot_expand")
+    return out
+
+
+# ------------------------------------------------------------------------------------ C-EROT
+def workspace(B: int, n: int, m: int, dtype_code: int, device="cuda"):
+    import torch
+    nbytes = int(lib().cot_workspace_bytes(B, n, m, dtype_code))
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+class CerotProblem:
+    """Device-resident problem + state for step-by-step use of cerot_init / cerot_iter / cerot_plan.
+    Tensors: C [n,m,m] or [B,n,m,m] (fp32/fp64), alpha/beta [.., m] fp64, eps [B] fp64."""
+
+    def __init__(self, C, alpha, beta, eps, stream=None):
+        import torch
+        self.C = C
+        self.B, self.n, self.m, self.batched = _shape(C)
+        self.dt = _dtype_code(C)
+        self.alpha = alpha.to(torch.float64).contiguous()
+        self.beta = beta.to(torch.float64).contiguous()
+        self.eps = torch.as_tensor(eps, dtype=torch.float64, device=C.device).reshape(self.B).contiguous()
+        self.w_hat = torch.zeros_like(self.alpha)
+        self.z_hat = torch.zeros_like(self.beta)
+        self.ws = workspace(self.B, self.n, self.m, self.dt, C.device)
+        self.stream = stream
+        self.G, self.argmin = clot_aggregate(C, stream=stream)
+
+    def init(self, cold: bool = True):
+        _check(lib().cerot_init(_ptr(self.alpha), _ptr(self.beta), self.B, self.m, COT_COLD_START if cold else 0,
+                                _ptr(self.z_hat), _ptr(self.ws), self.ws.numel(), _stream(self.stream)), "cerot_init")
+        return self
+
+    def iterate(self, iters: int, tol: float = 0.0, check_every: int = 1, flags: int = 0):
+        _check(lib().cerot_iter(_ptr(self.alpha), _ptr(self.beta), _ptr(self.C), _ptr(self.G), self.B, self.n,
+                                self.m, self.dt, _ptr(self.eps), iters, tol, check_every, flags, _ptr(self.w_hat),
+                                _ptr(self.z_hat), _ptr(self.ws), self.ws.numel(), _stream(self.stream)), "cerot_iter")
+        return self
+
+    def state(self):
+        it = (ctypes.c_int64 * self.B)()
+        cv = (ctypes.c_int32 * self.B)()
+        rs = (ctypes.c_double * self.B)()
+        _check(lib().cerot_state(_ptr(self.ws), self.B, self.m, self.n, self.dt, it, cv, rs, _stream(self.stream)),
+               "cerot_state")
+        return np.array(it[:]), np.array(cv[:]), np.array(rs[:])
+
+    def plan(self, T_blocks: bool = False, report=None):
+        import torch
+        T = torch.empty_like(self.C) if T_blocks else None
+        rep = torch.empty((self.B, 8), dtype=torch.float64, device=self.C.device) if report is None else report
+        _check(lib().cerot_plan(_ptr(self.alpha), _ptr(self.beta), _ptr(self.C), _ptr(self.G), self.B, self.n,
+                                self.m, self.dt, _ptr(self.eps), _ptr(self.w_hat), _ptr(self.z_hat), _ptr(T),
+                                _ptr(rep), _ptr(self.ws), self.ws.numel(), _stream(self.stream)), "cerot_plan")
+        return T, rep
+
+
+def report_dict(rep_row) -> dict:
+    v = [float(x) for x in rep_row]
+    return dict(zip(REPORT_FIELDS, v))
+
+
+def cerot_solve(C, alpha, beta, eps, tol=0.0, max_iter=1000, check_every=1, T_blocks=False, cold=True,
+                w_hat=None, z_hat=None, ws=None, stream=None):
+    """Whole C-EROT solve on the device (A2..A5). Returns (w_hat, z_hat, T_blocks or None, [report dict])."""
+    import torch
+    B, n, m, batched = _shape(C)
+    dt = _dtype_code(C)
+    alpha = alpha.to(torch.float64).contiguous()
+    beta = beta.to(torch.float64).contiguous()
+    eps_t = torch.as_tensor(eps, dtype=torch.float64, device=C.device).reshape(B).contiguous()
+    w_hat = torch.zeros_like(alpha) if w_hat is None else w_hat
+    z_hat = torch.zeros_like(beta) if z_hat is None else z_hat
+    ws = workspace(B, n, m, dt, C.device) if ws is None else ws
+    T = torch.empty_like(C) if T_blocks else None
+    reps = (cot_report * B)()
+    code = lib().cerot_solve(_ptr(alpha), _ptr(beta), _ptr(C), B, n, m, dt, _ptr(eps_t), tol, max_iter, check_every,
+                             COT_COLD_START if cold else 0, _ptr(w_hat), _ptr(z_hat), _ptr(T), _ptr(ws), ws.numel(),
+                             reps, _stream(stream))
+    _check(code, "cerot_solve", ok=(0, 1))
+    out = []
+    for r in reps:
+        d = {f: getattr(r, f) for f in REPORT_FIELDS}
+        d.update(iters=r.iters, converged=bool(r.converged), status=STATUS[r.status])
+        out.append(d)
+    return w_hat, z_hat, T, out

@@ -1,0 +1,120 @@
+// Device helpers shared by the sm_100a kernels of libcyclicot (no torch, no host logic).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/cyclicot.h"
+
+#define COT_LOG2E 1.4426950408889634
+#define COT_LN2 0.6931471805599453
+
+namespace cot {
+
+// ------------------------------------------------------------------------------------- math
+// MUFU.EX2 with flush-to-zero: 2^x, max rel. error ~2 ulp; x <= 0 in every use here.
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ bool finite_f(float x) { return fabsf(x) <= 3.402823466e38f; }
+__device__ __forceinline__ bool finite_f(double x) { return fabs(x) <= 1.7976931348623157e308; }
+
+// --------------------------------------------------------------------------------- reductions
+template <typename V>
+__device__ __forceinline__ V warp_sum(V v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename V>
+__device__ __forceinline__ V warp_max(V v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide reductions over the first NW warps (NW = blockDim/32), fixed order => deterministic.
+// `scratch` must hold NW doubles; it is reused, so consecutive calls are separated by a barrier.
+template <int NW>
+__device__ __forceinline__ double block_sum(double v, double* scratch, int bar_id, int nthreads) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) scratch[wid] = v;
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads));
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) t += scratch[w];
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads));
+  return t;
+}
+template <int NW>
+__device__ __forceinline__ double block_max(double v, double* scratch, int bar_id, int nthreads) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_max(v);
+  if (lane == 0) scratch[wid] = v;
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads));
+  double t = scratch[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) t = fmax(t, scratch[w]);
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads));
+  return t;
+}
+
+// ---------------------------------------------------------------------- mbarrier + bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk async copy global -> shared (TMA engine; SASS UBLKCP), completion on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// streaming stores (evict-first) for write-once outputs
+__device__ __forceinline__ void st_cs(float4* p, float4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_cs(float* p, float v) { __stcs(p, v); }
+__device__ __forceinline__ void st_cs(double* p, double v) { __stcs(p, v); }
+__device__ __forceinline__ void st_cs(double2* p, double2 v) { __stcs(p, v); }
+
+}  // namespace cot

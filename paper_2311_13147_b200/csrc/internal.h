@@ -1,0 +1,83 @@
+// Internal host/device interface of libcyclicot: workspace layout, row-unit plan, kernel launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/cyclicot.h"
+
+namespace cot {
+
+// Per-problem solver state kept in the workspace (32 bytes).
+struct SolverState {
+  long long iters;   // iterations performed on this problem
+  int active;        // 1 while iterating; 0 once converged (frozen)
+  int converged;     // 1 if the monitor reached tol
+  double residual;   // last monitor n*sum_j |c_j - beta_j| (after the p-update of the last iteration)
+  int flags;         // bit 0: marginal validation failed; bit 1: column underflow
+  int pad;
+};
+enum { STATE_BAD_MARGINAL = 1, STATE_UNDERFLOW = 2 };
+
+// Rows of each problem are cut into units of `rpu` consecutive rows; units are the work items of the
+// row kernels (K-ITER, K-PLAN) and each unit writes one fp64 column-partial row. `upp` units per
+// problem, U = B * upp in total, processed by `grid` persistent CTAs (unit u -> CTA u % grid).
+struct UnitPlan {
+  int64_t rpu, upp, U;
+  int grid;
+};
+UnitPlan unit_plan(int64_t B, int64_t R, int sm_count);
+
+constexpr int kReportDoubles = 8;   // cot_report field order: objective .. residual
+constexpr int kPlanScalars = 4;     // per unit: transport, entropy sum, row |r - alpha| sum, mass
+
+struct Workspace {
+  void* G;                 // [B][m][m] dtype
+  int32_t* A;              // [B][m][m]
+  double* partials[2];     // [U][m] x 2 (ping-pong by iteration parity)
+  double* plan_scal;       // [U][kPlanScalars]
+  double* resid_part;      // [B][ceil(m/32)]
+  SolverState* state;      // [B]
+  unsigned* counters;      // [B] last-block-done tickets (self-resetting)
+  int32_t* nonfinite;      // [1]
+  double* report;          // [B][kReportDoubles]
+};
+// Lays the workspace out from `base` (may be NULL to only size it). Returns the byte count.
+size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int dtype, int sm_count, Workspace* ws);
+
+int device_sm_count();
+void set_error(const std::string& msg);
+
+// ------------------------------------------------------------------------------- launchers
+cudaError_t launch_aggregate(const void* C, int64_t B, int64_t n, int64_t m, int dtype, void* G, int32_t* A,
+                             int32_t* nonfinite, cudaStream_t s);
+cudaError_t launch_expand(const void* S, const int32_t* A, int64_t B, int64_t n, int64_t m, int dtype, void* out,
+                          cudaStream_t s);
+
+struct IterArgs {
+  const double* alpha;
+  const double* beta;
+  const void* C;
+  const void* G;
+  const double* eps;
+  double* w_hat;
+  double* z_hat;
+  int64_t B, n, m;
+  int64_t R;          // rows of each problem held by this call (== m unless row-sharded)
+  int64_t row_begin;  // global index of the first held row
+  int dtype;
+  double tol;
+  int64_t check_every;
+  uint32_t flags;
+};
+cudaError_t launch_init(const double* alpha, const double* beta, int64_t B, int64_t m, uint32_t flags, double* z_hat,
+                        const Workspace& ws, cudaStream_t s);
+// Row pass (p-update + column partials) of one iteration into ws.partials[parity].
+cudaError_t launch_rows(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int parity, cudaStream_t s);
+// Column pass (deterministic reduction + q-update + monitor) reading ws.partials[parity].
+cudaError_t launch_cols(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int parity, cudaStream_t s);
+cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& up, void* T_blocks, double* d_report,
+                        cudaStream_t s);
+
+}  // namespace cot

@@ -1,0 +1,256 @@
+// K-PLAN: plan reconstruction T_ijk = exp(w_hat_i + z_hat_j - C_ijk/eps) (Alg. 2 lines 7-9, P:434-436;
+// eq. optimality_condition) fused with the fp64 reductions of the report:
+//   transport sum C T, entropy sum T (log T - 1), row sums r_i (-> row residual, mass), column sums c_j.
+// Numerics: y_ij = w_hat_i + z_hat_j - G_ij/eps and E_ij = exp(y_ij) in fp64 once per (i,j);
+// a_ijk = (G_ij - C_ijk)/eps <= 0 in fp64, exp(a) in fp32 (accurate exp2f, not ex2.approx),
+// T = E * exp(a) and log T = y + a in fp64. All sums fp64 in a fixed order (deterministic).
+#include "common.cuh"
+#include "internal.h"
+
+namespace cot {
+
+template <typename T, int V>
+struct VecP;
+template <>
+struct VecP<float, 4> {
+  using type = float4;
+  __device__ static void unpack(const type& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+  __device__ static type pack(const float* o) { return make_float4(o[0], o[1], o[2], o[3]); }
+};
+template <>
+struct VecP<float, 1> {
+  using type = float;
+  __device__ static void unpack(const type& v, float* o) { o[0] = v; }
+  __device__ static type pack(const float* o) { return o[0]; }
+};
+template <>
+struct VecP<double, 2> {
+  using type = double2;
+  __device__ static void unpack(const type& v, double* o) { o[0] = v.x; o[1] = v.y; }
+  __device__ static type pack(const double* o) { return make_double2(o[0], o[1]); }
+};
+template <>
+struct VecP<double, 1> {
+  using type = double;
+  __device__ static void unpack(const type& v, double* o) { o[0] = v; }
+  __device__ static type pack(const double* o) { return o[0]; }
+};
+
+struct PlanParams {
+  const void* C;
+  const void* G;
+  const double* alpha;
+  const double* w_hat;
+  const double* z_hat;
+  const double* eps;
+  void* T;               // [B][n][R][m] or nullptr
+  int64_t n, m, R, row_begin, rpu, upp, U;
+  double* partials;      // [U][m] column partials
+  double* scal;          // [U][kPlanScalars]
+  const SolverState* state;
+};
+
+__device__ __forceinline__ double pblk_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < nw; ++w) t += sh[w];
+  __syncthreads();
+  return t;
+}
+
+template <typename T, int V, int CPT>
+__global__ void __launch_bounds__(256) k_plan(PlanParams p) {
+  using VT = typename VecP<T, V>::type;
+  __shared__ double sh[32];
+  const int NT = blockDim.x;
+  const int64_t m = p.m, mv = m / V;
+  const T* C = static_cast<const T*>(p.C);
+  const T* G = static_cast<const T*>(p.G);
+  T* Tout = static_cast<T*>(p.T);
+  for (int64_t u = blockIdx.x; u < p.U; u += gridDim.x) {
+    const int64_t b = u / p.upp, cu = u - b * p.upp;
+    const int64_t i0 = cu * p.rpu;
+    const int64_t i1 = min(p.R, i0 + p.rpu);
+    const double eps = p.eps[b];
+    const double inv_eps = 1.0 / eps;
+    double z[CPT][V], P[CPT][V];
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int64_t jv = (int64_t)q * NT + threadIdx.x;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        P[q][v] = 0.0;
+        z[q][v] = jv < mv ? p.z_hat[b * m + jv * V + v] : 0.0;
+      }
+    }
+    double transport = 0.0, ent = 0.0, rl1 = 0.0, mass = 0.0;
+    for (int64_t i = i0; i < i1; ++i) {
+      const int64_t gi = p.row_begin + i;
+      const double wi = p.w_hat[b * m + gi];
+      const VT* Grow = reinterpret_cast<const VT*>(G + (b * p.R + i) * m);
+      const VT* Crow = reinterpret_cast<const VT*>(C + (b * p.n * p.R + i) * m);
+      VT* Trow = Tout ? reinterpret_cast<VT*>(Tout + (b * p.n * p.R + i) * m) : nullptr;
+      const int64_t kstride = p.R * mv;
+      T g[CPT][V];
+      double y[CPT][V], E[CPT][V];
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const int64_t jv = (int64_t)q * NT + threadIdx.x;
+        VT gv = jv < mv ? Grow[jv] : VT{};
+        VecP<T, V>::unpack(gv, g[q]);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          y[q][v] = wi + z[q][v] - (double)g[q][v] * inv_eps;
+          E[q][v] = exp(y[q][v]);
+        }
+      }
+      double row = 0.0;
+      for (int64_t k = 0; k < p.n; ++k) {
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          const int64_t jv = (int64_t)q * NT + threadIdx.x;
+          if (jv >= mv) continue;
+          T c[V], tout[V];
+          VecP<T, V>::unpack(__ldcs(Crow + k * kstride + jv), c);
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const double a = ((double)g[q][v] - (double)c[v]) * inv_eps;   // <= 0
+            double e;
+            if constexpr (sizeof(T) == 4)
+              e = (double)exp2f((float)(a * COT_LOG2E));
+            else
+              e = exp(a);
+            const double Tv = E[q][v] * e;
+            transport = fma((double)c[v], Tv, transport);
+            ent = fma(Tv, (y[q][v] + a) - 1.0, ent);
+            row += Tv;
+            P[q][v] += Tv;
+            tout[v] = (T)Tv;
+          }
+          if (Trow) __stcs(Trow + k * kstride + jv, VecP<T, V>::pack(tout));
+        }
+      }
+      const double r = pblk_sum(row, sh);
+      rl1 += fabs(r - p.alpha[b * m + gi]);
+      mass += r;
+    }
+    transport = pblk_sum(transport, sh);
+    ent = pblk_sum(ent, sh);
+    if (threadIdx.x == 0) {
+      double* sc = p.scal + u * kPlanScalars;
+      sc[0] = transport;
+      sc[1] = ent;
+      sc[2] = rl1;
+      sc[3] = mass;
+    }
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int64_t jv = (int64_t)q * NT + threadIdx.x;
+      if (jv < mv) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) p.partials[u * m + jv * V + v] = P[q][v];
+      }
+    }
+  }
+}
+
+// One block per problem: fixed-order sums of the unit partials -> the report (cot_report field order).
+__global__ void __launch_bounds__(256) k_plan_finalize(const double* __restrict__ partials,
+                                                       const double* __restrict__ scal, int64_t upp, int64_t m,
+                                                       int64_t n, const double* __restrict__ alpha,
+                                                       const double* __restrict__ beta,
+                                                       const double* __restrict__ w_hat,
+                                                       const double* __restrict__ z_hat,
+                                                       const double* __restrict__ eps,
+                                                       const SolverState* __restrict__ state,
+                                                       double* __restrict__ report) {
+  __shared__ double sh[32];
+  const int64_t b = blockIdx.x;
+  double cl1 = 0.0, cl2 = 0.0, dot = 0.0;
+  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+    double c = 0.0;
+    for (int64_t u = 0; u < upp; ++u) c += partials[(b * upp + u) * m + j];
+    const double dv = c - beta[b * m + j];
+    cl1 += fabs(dv);
+    cl2 += dv * dv;
+    dot += w_hat[b * m + j] * alpha[b * m + j] + z_hat[b * m + j] * beta[b * m + j];
+  }
+  cl1 = pblk_sum(cl1, sh);
+  cl2 = pblk_sum(cl2, sh);
+  dot = pblk_sum(dot, sh);
+  if (threadIdx.x == 0) {
+    double tr = 0.0, en = 0.0, rl1 = 0.0, mass = 0.0;
+    for (int64_t u = 0; u < upp; ++u) {
+      const double* sc = scal + (b * upp + u) * kPlanScalars;
+      tr += sc[0];
+      en += sc[1];
+      rl1 += sc[2];
+      mass += sc[3];
+    }
+    const double nn = (double)n, e = eps[b];
+    double* rep = report + b * kReportDoubles;
+    rep[0] = nn * tr;                       // objective: transport cost of the full plan
+    rep[1] = nn * (tr + e * en);            // regularised primal
+    rep[2] = nn * e * (dot - mass);         // dual (phi*(y) = eps e^{y/eps})
+    rep[3] = nn * rl1;                      // ||T 1 - a||_1
+    rep[4] = nn * cl1;                      // ||T^T 1 - b||_1
+    rep[5] = sqrt(nn * cl2);                // ||T^T 1 - b||_2
+    rep[6] = nn * mass;                     // full plan mass
+    rep[7] = state ? state[b].residual : 0.0;
+  }
+}
+
+template <typename T, int V>
+static cudaError_t plan_dispatch(const PlanParams& pp, int grid, int64_t m, cudaStream_t s) {
+  const int64_t mv = m / V;
+  int nt = (int)((mv + 31) / 32 * 32);
+  if (nt > 256) nt = 256;
+  const int64_t cpt = (mv + nt - 1) / nt;
+  if (cpt <= 1)
+    k_plan<T, V, 1><<<grid, nt, 0, s>>>(pp);
+  else if (cpt <= 2)
+    k_plan<T, V, 2><<<grid, nt, 0, s>>>(pp);
+  else if (cpt <= 4)
+    k_plan<T, V, 4><<<grid, nt, 0, s>>>(pp);
+  else if (cpt <= 8)
+    k_plan<T, V, 8><<<grid, nt, 0, s>>>(pp);
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& up, void* T_blocks, double* d_report,
+                        cudaStream_t s) {
+  PlanParams pp;
+  pp.C = a.C;
+  pp.G = a.G;
+  pp.alpha = a.alpha;
+  pp.w_hat = a.w_hat;
+  pp.z_hat = a.z_hat;
+  pp.eps = a.eps;
+  pp.T = T_blocks;
+  pp.n = a.n;
+  pp.m = a.m;
+  pp.R = a.R;
+  pp.row_begin = a.row_begin;
+  pp.rpu = up.rpu;
+  pp.upp = up.upp;
+  pp.U = up.U;
+  pp.partials = ws.partials[0];
+  pp.scal = ws.plan_scal;
+  pp.state = ws.state;
+  cudaError_t e;
+  if (a.dtype == COT_F32)
+    e = (a.m % 4 == 0) ? plan_dispatch<float, 4>(pp, up.grid, a.m, s) : plan_dispatch<float, 1>(pp, up.grid, a.m, s);
+  else
+    e = (a.m % 2 == 0) ? plan_dispatch<double, 2>(pp, up.grid, a.m, s) : plan_dispatch<double, 1>(pp, up.grid, a.m, s);
+  if (e != cudaSuccess) return e;
+  k_plan_finalize<<<(unsigned)a.B, 256, 0, s>>>(ws.partials[0], ws.plan_scal, up.upp, a.m, a.n, a.alpha, a.beta,
+                                                a.w_hat, a.z_hat, a.eps, ws.state, d_report ? d_report : ws.report);
+  return cudaGetLastError();
+}
+
+}  // namespace cot

@@ -1,0 +1,273 @@
+"""GPU parity: the C-ABI path (libcyclicot.so on an sm_100a B200) against the fp64 oracle.
+
+Bars (BASELINE.json north_star):
+  * G, argmin and the d x d expansion: bit-exact.
+  * C-EROT: objective (transport cost), dual and regularised primal within 1e-6 relative; marginal
+    residuals and the plan within 1e-5 in L1 (full scale); the fp64 template (C1) within 1e-10.
+Iteration parity is iterate-for-iterate: same start (z = 0), same order (p then q), same count.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic
+
+pytestmark = pytest.mark.gpu
+
+cot = pytest.importorskip("paper_2311_13147_b200")
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2311_13147_b200 import build
+    build.build()
+    cot.lib()
+
+
+def _dev(x):
+    return torch.as_tensor(np.ascontiguousarray(x), device=DEV)
+
+
+# ------------------------------------------------------------------------------- A2: aggregation
+def _agg_cases():
+    rng = np.random.default_rng(0)
+    ties = rng.integers(0, 3, size=(5, 37, 37)).astype(np.float32)
+    signed = np.zeros((3, 4, 4), np.float32)
+    signed[1] = -0.0
+    signed[2, 0, 0] = -1.0
+    return [
+        ("C1", synthetic.c1_tiny().C),
+        ("C2", synthetic.c2_ring().C),
+        ("C3", synthetic.c3_image().C),
+        ("C5x8", synthetic.c5_batched(B=8).C),
+        ("ties_odd_m", ties),
+        ("ties_fp64_odd", ties.astype(np.float64)[:, :7, :7].copy()),
+        ("signed_zero", signed),
+        ("n1", rng.random((1, 9, 9)).astype(np.float32)),
+        ("m1", rng.random((6, 1, 1)).astype(np.float32)),
+    ]
+
+
+@pytest.mark.parametrize("name,C", _agg_cases(), ids=[c[0] for c in _agg_cases()])
+def test_aggregate_bitexact(name, C):
+    G, A = cot.clot_aggregate(_dev(C))
+    Go, Ao = oracle.aggregate(C)
+    Gg = G.cpu().numpy()
+    assert Gg.dtype == Go.dtype
+    assert np.array_equal(Gg.view(np.uint32 if Gg.dtype == np.float32 else np.uint64),
+                          Go.view(np.uint32 if Go.dtype == np.float32 else np.uint64))   # sign of zero too
+    assert np.array_equal(A.cpu().numpy(), Ao)
+
+
+def test_aggregate_nonfinite_rejected():
+    C = np.random.default_rng(1).random((4, 8, 8)).astype(np.float32)
+    for bad in (np.nan, np.inf, -np.inf):
+        C2 = C.copy()
+        C2[2, 3, 5] = bad
+        with pytest.raises(cot.CotError) as e:
+            cot.clot_aggregate(_dev(C2))
+        assert e.value.code == -2
+
+
+# ------------------------------------------------------------------------------- A6: expansion
+def test_expand_clot_c1_bitexact():
+    p = synthetic.c1_tiny()
+    r = oracle.clot(p.alpha, p.beta, p.C)
+    _, A = cot.clot_aggregate(_dev(p.C))
+    T = cot.clot_expand(_dev(r["S"]), p.n, argmin=A).cpu().numpy()
+    ref = oracle.expand_plan(oracle.lift(r["S"], r["A"], p.n))
+    assert np.array_equal(T, ref)
+    # Theorem 1: the expanded plan is feasible and optimal for the explicit problem
+    Cf = oracle.expand_cost(p.C)
+    assert abs((Cf * T).sum() - r["value"]) < 1e-12
+
+
+@pytest.mark.parametrize("B,n,m,dt", [(1, 8, 128, np.float32), (3, 4, 37, np.float32), (1, 5, 16, np.float64),
+                                      (2, 1, 24, np.float32), (1, 3, 1, np.float64), (2, 6, 130, np.float32)])
+def test_expand_blocks_and_lift_bitexact(B, n, m, dt):
+    rng = np.random.default_rng(B * 100 + n * 10 + m)
+    blocks = rng.random((B, n, m, m)).astype(dt)
+    T = cot.clot_expand(_dev(blocks), n).cpu().numpy()
+    for b in range(B):
+        assert np.array_equal(T[b], oracle.expand_plan(blocks[b]))
+    S = rng.random((B, m, m)).astype(dt)
+    A = rng.integers(0, n, size=(B, m, m)).astype(np.int32)
+    T2 = cot.clot_expand(_dev(S), n, argmin=_dev(A)).cpu().numpy()
+    for b in range(B):
+        assert np.array_equal(T2[b], oracle.expand_plan(oracle.lift(S[b], A[b], n)))
+
+
+def test_clot_pipeline_c5_sample():
+    """C5 sample: clot_aggregate -> host LP -> clot_expand per problem; value n<G,S> equals the oracle's
+    Alg. 1 value and the expanded plan equals the oracle's expansion of the same S (bit-exact)."""
+    from paper_2311_13147_b200 import host_lp
+    p = synthetic.c5_batched(B=4)
+    for b in range(p.B):
+        q = p.single(b)
+        res = host_lp.clot_solve(_dev(q.C), q.alpha, q.beta)
+        ro = oracle.clot(q.alpha, q.beta, q.C)
+        assert abs(res["value"] - ro["value"]) <= 1e-9 * max(1.0, abs(ro["value"]))
+        S32 = res["S"].cpu().numpy()
+        assert np.array_equal(res["argmin"].cpu().numpy(), ro["A"])
+        ref = oracle.expand_plan(oracle.lift(S32, ro["A"], q.n))
+        assert np.array_equal(res["T_full"].cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------------------- A3-A5: C-EROT
+def _gpu_run(p, iters, tol=0.0, check_every=1, T_blocks=True):
+    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps))
+    prob.init().iterate(iters, tol=tol, check_every=check_every)
+    T, rep = prob.plan(T_blocks=T_blocks)
+    torch.cuda.synchronize()
+    it, conv, res = prob.state()
+    return prob, (T.cpu().numpy() if T is not None else None), rep.cpu().numpy(), it, conv
+
+
+def _compare(p, rep_gpu, T_gpu, w, z, obj_rtol=1e-6, l1_tol=1e-5):
+    eps = float(p.eps[0])
+    ro = oracle.report(w, z, p.alpha, p.beta, p.C, eps)
+    g = cot.report_dict(rep_gpu)
+    for key in ("objective", "dual", "reg_primal"):
+        assert math.isclose(g[key], ro[key], rel_tol=obj_rtol, abs_tol=1e-300), (key, g[key], ro[key])
+    for key in ("row_l1", "col_l1"):
+        assert abs(g[key] - ro[key]) <= l1_tol, (key, g[key], ro[key])
+    assert abs(g["mass"] - ro["mass"]) <= l1_tol
+    if T_gpu is not None:
+        To = oracle.plan_blocks(w, z, p.C, eps)
+        l1 = p.n * np.abs(T_gpu.astype(np.float64) - To).sum()
+        assert l1 <= l1_tol, ("plan L1", l1)
+        # marginal vectors of the returned plan (full scale, L1)
+        r_g, c_g = T_gpu.astype(np.float64).sum(axis=(0, 2)), T_gpu.astype(np.float64).sum(axis=(0, 1))
+        assert p.n * np.abs(r_g - ro["r"]).sum() <= l1_tol
+        assert p.n * np.abs(c_g - ro["c"]).sum() <= l1_tol
+    return g, ro
+
+
+def test_c1_fp64_to_tolerance():
+    """C1 (configs[0]): fp64 template, run to n*sum|c - beta| <= 1e-9 checked every iteration; the GPU stops at
+    the same iteration as the oracle and matches it to 1e-10."""
+    p = synthetic.c1_tiny()
+    w, z, t, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 100000, tol=p.tol)
+    prob, T, rep, it, conv = _gpu_run(p, t + 25, tol=p.tol)
+    assert conv[0] == 1 and it[0] == t
+    _compare(p, rep[0], T, w, z, obj_rtol=1e-10, l1_tol=1e-10)
+    w_g, z_g = prob.w_hat.cpu().numpy(), prob.z_hat.cpu().numpy()
+    eps = float(p.eps[0])
+    assert np.abs(w_g * eps - w).max() < 1e-10 and np.abs(z_g * eps - z).max() < 1e-10
+
+
+def test_c1_solve_api():
+    p = synthetic.c1_tiny()
+    w, z, t, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 100000, tol=p.tol)
+    wg, zg, T, reps = cot.cerot_solve(_dev(p.C), _dev(p.alpha), _dev(p.beta), p.eps, tol=p.tol, max_iter=10000,
+                                      check_every=1, T_blocks=True)
+    assert reps[0]["converged"] and reps[0]["iters"] == t and reps[0]["status"] == "COT_OK"
+    _compare(p, np.array([reps[0][f] for f in cot.REPORT_FIELDS]), T.cpu().numpy(), w, z, 1e-10, 1e-10)
+
+
+@pytest.mark.parametrize("eps_factor", [1e-1, 1e-2, 1e-3])
+def test_c2_500_iterations(eps_factor):
+    """C2 (configs[1]): ring, fp32, 500 iterations at each eps; iterate parity (not converged at 1e-3)."""
+    p = synthetic.c2_ring(eps_factor=eps_factor)
+    w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 500, form="kernel")
+    _, T, rep, it, _ = _gpu_run(p, 500)
+    assert it[0] == 500
+    _compare(p, rep[0], T, w, z)
+
+
+def test_c3_image_500_iterations():
+    """C3 (configs[2]): 64x64 rotation-symmetric histograms (stand-in for Table 2's NYU images), eps = 1e-2."""
+    p = synthetic.c3_image(pair=0)
+    w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 500, form="kernel")
+    _, T, rep, _, _ = _gpu_run(p, 500)
+    _compare(p, rep[0], T, w, z)
+
+
+def test_c3_converges_like_oracle():
+    p = synthetic.c3_image(pair=1)
+    w, z, t, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 5000, tol=1e-9, form="kernel",
+                                        check_every=10)
+    assert t < 4000
+    _, T, rep, it, conv = _gpu_run(p, t + 50, tol=1e-9, check_every=10)
+    assert conv[0] == 1 and it[0] == t
+    _compare(p, rep[0], T, w, z)
+
+
+def test_c4_full_size_500_iterations():
+    """C4 (configs[3]) at full size (n = 64, m = 1024, 256 MiB of cost), 500 iterations, the bench's
+    launch configuration; the oracle runs Alg. 2 with K precomputed (pinned equal to the streaming form)."""
+    p = synthetic.c4_large()
+    w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 500, form="kernel")
+    _, T, rep, it, _ = _gpu_run(p, 500, T_blocks=False)
+    g, ro = _compare(p, rep[0], None, w, z)
+    assert g["row_l1"] > 1e-4    # not converged at 500 iterations: the comparison is iterate-for-iterate
+
+
+def test_c4_full_size_3_iterations_stream_oracle():
+    p = synthetic.c4_large()
+    w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 3, form="stream")
+    _, T, rep, _, _ = _gpu_run(p, 3, T_blocks=True)
+    _compare(p, rep[0], T, w, z)
+
+
+def test_c5_sample_batched_200_iterations():
+    """C5 (configs[4]) sample: 8 problems with their own eps in one batched call, 200 iterations."""
+    p = synthetic.c5_batched(B=8, first=100)
+    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps))
+    prob.init().iterate(200)
+    T, rep = prob.plan(T_blocks=True)
+    T = T.cpu().numpy()
+    rep = rep.cpu().numpy()
+    for b in range(p.B):
+        q = p.single(b)
+        w, z, _, _ = oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, float(q.eps[0]), 200, form="kernel")
+        _compare(q, rep[b], T[b], w, z)
+
+
+@pytest.mark.parametrize("n,m,dt", [(3, 1, np.float64), (1, 24, np.float32), (5, 37, np.float32),
+                                    (4, 130, np.float32), (2, 7, np.float64), (7, 300, np.float32)])
+def test_edge_shapes(n, m, dt):
+    """Ragged tails (m not a multiple of the vector width or of the CTA), n = 1, m = 1."""
+    p = synthetic.random_cyclic(seed=n * 1000 + m, n=n, m=m, dtype=dt, eps=0.05)
+    w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, 0.05, 30)
+    _, T, rep, _, _ = _gpu_run(p, 30)
+    tol = 1e-10 if dt == np.float64 else 1e-6
+    _compare(p, rep[0], T, w, z, obj_rtol=tol, l1_tol=1e-5 if dt == np.float32 else 1e-10)
+
+
+def test_batch_freeze_rule_matches_oracle():
+    """tol > 0 in a batch: each problem stops at its own iteration (rule of SURVEY Q1), others continue."""
+    p = synthetic.random_cyclic(seed=5, n=4, m=20, B=3, eps=0.1)
+    p.eps = np.array([0.1, 0.05, 0.2])
+    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps))
+    prob.init().iterate(3000, tol=1e-8, check_every=5)
+    T, rep = prob.plan(T_blocks=True)
+    it, conv, _ = prob.state()
+    for b in range(3):
+        q = p.single(b)
+        w, z, t, _ = oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, float(q.eps[0]), 3000, tol=1e-8, check_every=5)
+        assert conv[b] == 1 and it[b] == t
+        _compare(q, rep.cpu().numpy()[b], T.cpu().numpy()[b], w, z, obj_rtol=1e-8, l1_tol=1e-8)
+
+
+def test_warm_start_and_validation():
+    p = synthetic.c2_ring(eps_factor=1e-2)
+    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps))
+    prob.init().iterate(20)
+    prob.init(cold=False).iterate(30)        # warm start: continue from the current z_hat
+    T, rep = prob.plan(T_blocks=True)
+    w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 50, form="kernel")
+    _compare(p, rep.cpu().numpy()[0], T.cpu().numpy(), w, z)
+    bad = p.alpha.copy()
+    bad[3] = 0.0
+    prob2 = cot.CerotProblem(_dev(p.C), _dev(bad), _dev(p.beta), _dev(p.eps))
+    prob2.init().iterate(2)
+    with pytest.raises(cot.CotError) as e:
+        prob2.state()
+    assert e.value.code == -3
