@@ -126,6 +126,17 @@ int cerot_iter(const double* alpha, const double* beta, const void* C, const voi
                int64_t B, int64_t n, int64_t m, int dtype, const double* eps,
                int64_t iters, double tol, int64_t check_every, uint32_t flags,
                double* w_hat, double* z_hat, void* workspace, size_t ws_bytes, void* stream);
+/* The two halves of one cerot_iter iteration, for callers that interleave work between them (the
+ * row-sharded multi-GPU path reduces the column sums across ranks in between; bench.py times the row
+ * pass alone). `parity` (0/1) selects the column-partial buffer; use the iteration index & 1.
+ *   cerot_rows: the p-update of every held row + fp64 column partials (the streamed n*m^2 pass).
+ *   cerot_cols: deterministic column reduction, q-update, monitor and freeze rule.                    */
+int cerot_rows(const double* alpha, const void* C, const void* G, int64_t B, int64_t n, int64_t m, int dtype,
+               const double* eps, uint32_t flags, const double* z_hat, double* w_hat,
+               void* workspace, size_t ws_bytes, int parity, void* stream);
+int cerot_cols(const double* beta, int64_t B, int64_t n, int64_t m, int dtype, double tol, int64_t check_every,
+               double* z_hat, void* workspace, size_t ws_bytes, int parity, void* stream);
+
 /* Synchronises `stream` and copies the per-problem state to HOST arrays (any may be NULL):         */
 /*   iters_done[B] (int64), converged[B] (int32), residual[B] (double). Returns COT_E_MARGINAL,     */
 /*   COT_E_UNDERFLOW if the device flagged one, else COT_OK.                                          */

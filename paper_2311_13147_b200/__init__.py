@@ -50,6 +50,9 @@ _SIGS = {
     "cerot_init": (ctypes.c_int, [_vp, _vp, _i64, _i64, _u32, _vp, _vp, _sz, _vp]),
     "cerot_iter": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl, _i64, _u32,
                                   _vp, _vp, _vp, _sz, _vp]),
+    "cerot_rows": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _u32, _vp, _vp, _vp, _sz,
+                                  ctypes.c_int, _vp]),
+    "cerot_cols": (ctypes.c_int, [_vp, _i64, _i64, _i64, ctypes.c_int, _dbl, _i64, _vp, _vp, _sz, ctypes.c_int, _vp]),
     "cerot_state": (ctypes.c_int, [_vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp]),
     "cerot_plan": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _sz, _vp]),
@@ -187,6 +190,17 @@ class CerotProblem:
                                 self.m, self.dt, _ptr(self.eps), iters, tol, check_every, flags, _ptr(self.w_hat),
                                 _ptr(self.z_hat), _ptr(self.ws), self.ws.numel(), _stream(self.stream)), "cerot_iter")
         return self
+
+    def rows(self, parity: int, flags: int = 0):
+        """The p-update pass alone (cerot_rows)."""
+        _check(lib().cerot_rows(_ptr(self.alpha), _ptr(self.C), _ptr(self.G), self.B, self.n, self.m, self.dt,
+                                _ptr(self.eps), flags, _ptr(self.z_hat), _ptr(self.w_hat), _ptr(self.ws),
+                                self.ws.numel(), parity, _stream(self.stream)), "cerot_rows")
+
+    def cols(self, parity: int, tol: float = 0.0, check_every: int = 1):
+        """The column reduction + q-update alone (cerot_cols)."""
+        _check(lib().cerot_cols(_ptr(self.beta), self.B, self.n, self.m, self.dt, tol, check_every, _ptr(self.z_hat),
+                                _ptr(self.ws), self.ws.numel(), parity, _stream(self.stream)), "cerot_cols")
 
     def state(self):
         it = (ctypes.c_int64 * self.B)()

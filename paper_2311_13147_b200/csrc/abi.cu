@@ -55,6 +55,7 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int dtype, i
   Workspace w{};
   w.state = reinterpret_cast<SolverState*>(take((size_t)B * sizeof(SolverState)));
   w.counters = reinterpret_cast<unsigned*>(take((size_t)B * 4));
+  w.grid_bar = reinterpret_cast<unsigned*>(take(16));
   w.nonfinite = reinterpret_cast<int32_t*>(take(4));
   w.report = reinterpret_cast<double*>(take((size_t)B * kReportDoubles * 8));
   w.resid_part = reinterpret_cast<double*>(take((size_t)(B * ntiles) * 8));
@@ -154,7 +155,7 @@ int cerot_init(const double* alpha, const double* beta, int64_t B, int64_t m, ui
   if (!alpha || !beta || !z_hat) return arg_error("cerot_init: alpha, beta, z_hat must be non-NULL");
   // the state block is at the start of the workspace for every (n, dtype) (see carve_workspace)
   Workspace ws;
-  const size_t need = (size_t)B * (sizeof(SolverState) + 4) + 1024;
+  const size_t need = (size_t)B * (sizeof(SolverState) + 4) + 2048;
   if (!workspace || ws_bytes < need) {
     set_error("workspace too small");
     return COT_E_WORKSPACE;
@@ -201,10 +202,48 @@ int cerot_iter(const double* alpha, const double* beta, const void* C, const voi
   const IterArgs a = make_args(alpha, beta, C, G, B, n, m, dtype, eps, tol, check_every, flags, w_hat, z_hat);
   const UnitPlan up = unit_plan(B, m, device_sm_count());
   cudaStream_t s = (cudaStream_t)stream;
+  if (iters > 0 && tma_eligible(a)) {
+    COT_CHECK_CUDA(launch_iter_tma(a, ws, (int)iters, false, 0, s));
+    return COT_OK;
+  }
   for (int64_t t = 0; t < iters; ++t) {
     COT_CHECK_CUDA(launch_rows(a, ws, up, (int)(t & 1), s));
     COT_CHECK_CUDA(launch_cols(a, ws, up, (int)(t & 1), s));
   }
+  return COT_OK;
+}
+
+int cerot_rows(const double* alpha, const void* C, const void* G, int64_t B, int64_t n, int64_t m, int dtype,
+               const double* eps, uint32_t flags, const double* z_hat, double* w_hat, void* workspace,
+               size_t ws_bytes, int parity, void* stream) {
+  int st = check_shape(B, n, m, dtype);
+  if (st) return st;
+  if (!alpha || !C || !G || !eps || !w_hat || !z_hat) return arg_error("cerot_rows: NULL argument");
+  Workspace ws;
+  st = check_ws(workspace, ws_bytes, B, n, m, dtype, &ws);
+  if (st) return st;
+  const IterArgs a = make_args(alpha, nullptr, C, G, B, n, m, dtype, eps, 0.0, 1, flags, w_hat,
+                               const_cast<double*>(z_hat));
+  if (tma_eligible(a)) {
+    COT_CHECK_CUDA(launch_iter_tma(a, ws, 1, true, parity & 1, (cudaStream_t)stream));
+    return COT_OK;
+  }
+  COT_CHECK_CUDA(launch_rows(a, ws, unit_plan(B, m, device_sm_count()), parity & 1, (cudaStream_t)stream));
+  return COT_OK;
+}
+
+int cerot_cols(const double* beta, int64_t B, int64_t n, int64_t m, int dtype, double tol, int64_t check_every,
+               double* z_hat, void* workspace, size_t ws_bytes, int parity, void* stream) {
+  int st = check_shape(B, n, m, dtype);
+  if (st) return st;
+  if (!beta || !z_hat) return arg_error("cerot_cols: NULL argument");
+  if (tol < 0) return arg_error("cerot_cols: tol >= 0 required");
+  Workspace ws;
+  st = check_ws(workspace, ws_bytes, B, n, m, dtype, &ws);
+  if (st) return st;
+  const IterArgs a = make_args(nullptr, beta, nullptr, nullptr, B, n, m, dtype, nullptr, tol, check_every, 0, nullptr,
+                               z_hat);
+  COT_CHECK_CUDA(launch_cols(a, ws, unit_plan(B, m, device_sm_count()), parity & 1, (cudaStream_t)stream));
   return COT_OK;
 }
 
@@ -276,9 +315,13 @@ int cerot_solve(const double* alpha, const double* beta, const void* C, int64_t 
   int64_t done = 0;
   while (done < max_iter) {
     const int64_t chunk = std::min<int64_t>(check_every, max_iter - done);
-    for (int64_t t = 0; t < chunk; ++t) {
-      COT_CHECK_CUDA(launch_rows(a, ws, up, (int)((done + t) & 1), s));
-      COT_CHECK_CUDA(launch_cols(a, ws, up, (int)((done + t) & 1), s));
+    if (tma_eligible(a)) {
+      COT_CHECK_CUDA(launch_iter_tma(a, ws, (int)chunk, false, 0, s));
+    } else {
+      for (int64_t t = 0; t < chunk; ++t) {
+        COT_CHECK_CUDA(launch_rows(a, ws, up, (int)((done + t) & 1), s));
+        COT_CHECK_CUDA(launch_cols(a, ws, up, (int)((done + t) & 1), s));
+      }
     }
     done += chunk;
     if (tol > 0.0 || done >= max_iter) {

@@ -40,6 +40,7 @@ struct Workspace {
   double* resid_part;      // [B][ceil(m/32)]
   SolverState* state;      // [B]
   unsigned* counters;      // [B] last-block-done tickets (self-resetting)
+  unsigned* grid_bar;      // [4] two device-wide barriers of the persistent TMA kernel (count, generation)
   int32_t* nonfinite;      // [1]
   double* report;          // [B][kReportDoubles]
 };
@@ -77,6 +78,11 @@ cudaError_t launch_init(const double* alpha, const double* beta, int64_t B, int6
 cudaError_t launch_rows(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int parity, cudaStream_t s);
 // Column pass (deterministic reduction + q-update + monitor) reading ws.partials[parity].
 cudaError_t launch_cols(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int parity, cudaStream_t s);
+bool tma_eligible(const IterArgs& a);
+// Persistent TMA kernel: `iters` full iterations (cooperative launch), or the row pass of one iteration
+// into ws.partials[parity] when rows_only.
+cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, bool rows_only, int parity,
+                            cudaStream_t s);
 cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& up, void* T_blocks, double* d_report,
                         cudaStream_t s);
 

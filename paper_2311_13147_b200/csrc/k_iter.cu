@@ -264,9 +264,16 @@ __global__ void __launch_bounds__(256) k_cols(const double* __restrict__ partial
 // optional cold start z_hat = 0 (q = 1_m, Alg. 2 line 2). One block per problem.
 __global__ void __launch_bounds__(256) k_init(const double* __restrict__ alpha, const double* __restrict__ beta,
                                               int64_t m, uint32_t flags, double* __restrict__ z_hat,
-                                              SolverState* __restrict__ state, unsigned* __restrict__ counters) {
+                                              SolverState* __restrict__ state, unsigned* __restrict__ counters,
+                                              unsigned* __restrict__ grid_bar) {
   __shared__ double sh[32];
   const int64_t b = blockIdx.x;
+  if (b == 0 && threadIdx.x == 0) {
+    grid_bar[0] = 0u;
+    grid_bar[1] = 0u;
+    grid_bar[2] = 0u;
+    grid_bar[3] = 0u;
+  }
   double sa = 0.0, sb = 0.0, bad = 0.0;
   for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
     const double a = alpha[b * m + j], bb = beta[b * m + j];
@@ -295,7 +302,7 @@ __global__ void __launch_bounds__(256) k_init(const double* __restrict__ alpha, 
 // ------------------------------------------------------------------------------------ launchers
 cudaError_t launch_init(const double* alpha, const double* beta, int64_t B, int64_t m, uint32_t flags, double* z_hat,
                         const Workspace& ws, cudaStream_t s) {
-  k_init<<<(unsigned)B, 256, 0, s>>>(alpha, beta, m, flags, z_hat, ws.state, ws.counters);
+  k_init<<<(unsigned)B, 256, 0, s>>>(alpha, beta, m, flags, z_hat, ws.state, ws.counters, ws.grid_bar);
   return cudaGetLastError();
 }
 

@@ -120,9 +120,9 @@ def test_clot_pipeline_c5_sample():
 
 
 # ------------------------------------------------------------------------------- A3-A5: C-EROT
-def _gpu_run(p, iters, tol=0.0, check_every=1, T_blocks=True):
+def _gpu_run(p, iters, tol=0.0, check_every=1, T_blocks=True, flags=0):
     prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps))
-    prob.init().iterate(iters, tol=tol, check_every=check_every)
+    prob.init().iterate(iters, tol=tol, check_every=check_every, flags=flags)
     T, rep = prob.plan(T_blocks=T_blocks)
     torch.cuda.synchronize()
     it, conv, res = prob.state()
@@ -172,11 +172,13 @@ def test_c1_solve_api():
 
 
 @pytest.mark.parametrize("eps_factor", [1e-1, 1e-2, 1e-3])
-def test_c2_500_iterations(eps_factor):
-    """C2 (configs[1]): ring, fp32, 500 iterations at each eps; iterate parity (not converged at 1e-3)."""
+@pytest.mark.parametrize("path", ["tma", "ldg"])
+def test_c2_500_iterations(eps_factor, path):
+    """C2 (configs[1]): ring, fp32, 500 iterations at each eps; iterate parity (not converged at 1e-3).
+    Both row paths: the persistent TMA kernel and the generic LDG kernels (COT_FORCE_LDG)."""
     p = synthetic.c2_ring(eps_factor=eps_factor)
     w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 500, form="kernel")
-    _, T, rep, it, _ = _gpu_run(p, 500)
+    _, T, rep, it, _ = _gpu_run(p, 500, flags=cot.COT_FORCE_LDG if path == "ldg" else 0)
     assert it[0] == 500
     _compare(p, rep[0], T, w, z)
 
@@ -271,3 +273,17 @@ def test_warm_start_and_validation():
     with pytest.raises(cot.CotError) as e:
         prob2.state()
     assert e.value.code == -3
+
+
+def test_split_rows_cols_api_matches_iter():
+    """cerot_rows + cerot_cols (the split used by the sharded path) == cerot_iter's iterate."""
+    p = synthetic.c2_ring(eps_factor=1e-2)
+    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps)).init()
+    for t in range(25):
+        prob.rows(t & 1)
+        prob.cols(t & 1)
+    T, rep = prob.plan(T_blocks=True)
+    w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 25, form="kernel")
+    _compare(p, rep.cpu().numpy()[0], T.cpu().numpy(), w, z)
+    it, _, _ = prob.state()
+    assert it[0] == 25
