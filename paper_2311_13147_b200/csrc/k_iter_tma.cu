@@ -1,23 +1,34 @@
 // K-ITER (TMA path): a persistent, warp-specialised cyclic Sinkhorn kernel for one problem (B == 1) with
-// fp32 costs and m % 4 == 0. Same arithmetic as k_rows_ldg + k_cols (k_iter.cu), organised for HBM:
+// fp32 costs and m % 4 == 0. Same arithmetic as k_rows_ldg + k_cols (k_iter.cu), organised for HBM.
+// Three warp roles per CTA (one CTA per SM, one unit of consecutive rows per CTA):
 //
-//   producer warp (1 elected lane): streams the rows of C owned by this CTA through an NSLOT-deep ring of
-//     shared-memory slots with 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP); each slot holds KS
-//     consecutive k-rows C[k][i][0..m) of one row i; completion is tracked by mbarrier transaction
-//     counts (full[]), reuse by consumer-warp arrivals (empty[]). The producer does not depend on the
-//     potentials, so it runs ahead across row epilogues, grid barriers and iteration boundaries.
-//   consumer warps: per row, s_ij = sum_k exp2((G_ij - C_ijk) * log2e/eps) from the slots (one FFMA + one
-//     MUFU.EX2 + one FADD per element), then the fp64 row epilogue (M_i, r_i, w_hat_i, column partials).
-//     After all rows: device-wide barrier; each CTA reduces its slice of columns over all units in a fixed
-//     order (deterministic), updates z_hat (q-update) and its monitor partial; device-wide barrier; every
-//     CTA sums the monitor partials in the same order and applies the same freeze rule.
+//   producer warp (1 elected lane): streams the CTA's rows of C through an NSLOT-deep ring of shared-
+//     memory slots with 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP); a slot holds KS consecutive
+//     k-rows C[k][i][0..m) of one row i; completion via mbarrier transaction counts (full[]), reuse via
+//     consumer-warp arrivals (empty[]). It never depends on the potentials, so it runs ahead across
+//     epilogues, device-wide syncs and iteration boundaries.
+//   consumer warps (VEC consecutive columns per thread): per row, the streamed k-sum
+//     s_ij = sum_k exp2((G_ij - C_ijk) * log2e/eps) (one FFMA + one MUFU.EX2 + one FADD per element), then
+//     the fp64 epilogue: x_ij = z_hat_j - G_ij/eps, r_i = sum_j s_ij exp(x_ij - M'_i) and M_i = max_j x_ij in
+//     ONE combined block reduction against the previous iteration's row maximum M'_i (exact exponent split:
+//     no precision cost), w_hat_i = log alpha_i - M'_i - log r_i, P_j += (alpha_i / r_i) s_ij exp(x_ij - M'_i).
+//     Rows whose potentials are not ready yet (the previous q-update is still in flight) are parked in
+//     shared memory; k-sums run at most one iteration ahead of epilogues.
+//   sync warp: owns every device-wide step, off the consumers' critical path: waits for the consumers to
+//     publish the CTA's column partial (bar.arrive / bar.sync), arrives on device barrier B1, reduces this
+//     CTA's slice of columns over all units in a fixed order (deterministic), applies the q-update
+//     z_hat_j += log beta_j - log c_j, arrives on B2, evaluates the monitor / freeze rule, and publishes the
+//     new z generation to the consumers through shared memory (st.release / ld.acquire at CTA scope).
 //
-// The grid is co-resident (cooperative launch, one CTA per SM), which the device-wide barrier requires.
-// With rows_only = 1 the kernel performs only the row pass of one iteration (no barriers): cerot_rows.
+// The grid is co-resident (cooperative launch). With rows_only = 1 the kernel performs only the row pass
+// of one iteration (no device-wide steps): cerot_rows.
 #include "common.cuh"
 #include "internal.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 namespace cot {
 
@@ -38,48 +49,74 @@ struct TmaParams {
   double* partials;      // [U][m]
   double* resid_part;    // [gridDim.x]
   SolverState* state;    // [1]
-  unsigned* bar;         // [2]: device-wide barrier arrival count, generation
+  unsigned* bar;         // [4]: two device-wide barriers {arrival count, generation}
   int evict_last_rows;   // rows [0, evict_last_rows) of every block are streamed with an L2 evict_last hint
+  int diag;              // COT_DIAG_* bits (diagnostics only)
+  unsigned long long* trace;   // diagnostics: [grid][8] cycle counters, or nullptr
 };
 
 __device__ __forceinline__ void cbar(int nthreads) {   // consumer-only named barrier
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
-__device__ __forceinline__ unsigned ld_volatile(const unsigned* p) {
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned x) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(x) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned x) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+}
+__device__ __forceinline__ void st_relaxed(unsigned* p, unsigned x) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+}
 __device__ __forceinline__ unsigned lds_volatile(const unsigned* p) { return *(volatile const unsigned*)p; }
+__device__ __forceinline__ unsigned lds_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+// Hand-off barrier between the consumer warps (arrive, non-blocking) and the sync warp (sync).
+__device__ __forceinline__ void handoff_arrive(int nthreads) {
+  asm volatile("bar.arrive 2, %0;" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void handoff_sync(int nthreads) {
+  asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+}
 
 // Device-wide barrier among the consumer warps of all CTAs, split into arrive / wait so that independent
-// work can run in between. bar = {arrival count, generation}; arrive returns the generation to wait past.
-__device__ __forceinline__ unsigned grid_arrive(unsigned* bar, int nct) {
-  __shared__ unsigned gen_sh;
+// work can run in between. bar = {arrival count, generation}. Ordering uses release/acquire atomics at gpu
+// scope (the CTA barrier before the arrival makes it cumulative over the CTA's writes); no fence.sc, which
+// would also stall this SM's in-flight TMA traffic.
+__device__ __forceinline__ unsigned grid_arrive(unsigned* bar, int nct, unsigned* gen_sh) {
   cbar(nct);
   if (threadIdx.x == 0) {
-    const unsigned gen = ld_volatile(bar + 1);
-    __threadfence();
-    const unsigned arrived = atomicAdd(bar, 1u);
+    const unsigned gen = ld_acquire(bar + 1);
+    const unsigned arrived = atom_add_acq_rel(bar, 1u);
     if (arrived == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+      st_relaxed(bar, 0u);
+      red_add_release(bar + 1, 1u);
     }
-    gen_sh = gen;
+    *gen_sh = gen;
   }
   cbar(nct);
-  return gen_sh;
+  return *gen_sh;
 }
 __device__ __forceinline__ void grid_wait(unsigned* bar, unsigned gen, int nct) {
   if (threadIdx.x == 0) {
-    while (ld_volatile(bar + 1) == gen) __nanosleep(20);
-    __threadfence();
+    while (ld_acquire(bar + 1) == gen) __nanosleep(20);
   }
   cbar(nct);
 }
-__device__ __forceinline__ void grid_barrier(unsigned* bar, int nct) { grid_wait(bar, grid_arrive(bar, nct), nct); }
 
+// Two-cbar block reduction for rare uses (monitor partial).
 __device__ __forceinline__ double cblk_sum(double v, double* sh, int nct) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   v = warp_sum(v);
@@ -90,46 +127,97 @@ __device__ __forceinline__ double cblk_sum(double v, double* sh, int nct) {
   cbar(nct);
   return t;
 }
-__device__ __forceinline__ double cblk_max(double v, double* sh, int nct) {
+// One-cbar block reductions for the epilogues: double-buffered scratch (`buf` alternates; the next
+// reduction's cbar orders every read of this buffer before its reuse two reductions later).
+__device__ __forceinline__ void cblk_maxsum(double& mx, double& sm, double* red2, int& buf, int nct) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  v = warp_max(v);
-  if (lane == 0) sh[wid] = v;
+  mx = warp_max(mx);
+  sm = warp_sum(sm);
+  double* r = red2 + buf * 64;
+  if (lane == 0) {
+    r[wid] = mx;
+    r[32 + wid] = sm;
+  }
   cbar(nct);
-  double t = sh[0];
-  for (int w = 1; w < (nct >> 5); ++w) t = fmax(t, sh[w]);
-  cbar(nct);
-  return t;
+  double M = r[0], S = r[32];
+  for (int w = 1; w < (nct >> 5); ++w) {
+    M = fmax(M, r[w]);
+    S += r[32 + w];
+  }
+  mx = M;
+  sm = S;
+  buf ^= 1;
+}
+__device__ __forceinline__ double cblk_max1(double v, double* red2, int& buf, int nct) {
+  double s = 0.0;
+  cblk_maxsum(v, s, red2, buf, nct);
+  return v;
+}
+__device__ __forceinline__ double cblk_sum1(double v, double* red2, int& buf, int nct) {
+  double m = -INFINITY;
+  cblk_maxsum(m, v, red2, buf, nct);
+  return v;
 }
 
-template <int CPT, int KS>
-__global__ void __launch_bounds__(288, 1) k_iter_tma(TmaParams p) {
+// exp(d) for d in fp64, |d| < ~700: 2^(round) exactly in fp64 times MUFU 2^frac with |frac| <= 1/2, so the
+// fp32 rounding of the argument costs < 3e-8 relative regardless of |d|.
+__device__ __forceinline__ double exp_split(double d) {
+  const double a = d * COT_LOG2E;
+  const double ai = fmax(rint(a), -1022.0);   // below 2^-1022: f is very negative and ex2(f) flushes to 0
+  const float f = (float)(a - ai);
+  const long long e = (long long)ai + 1023;
+  return (double)ex2(f) * __longlong_as_double(e << 52);
+}
+
+template <int VEC>
+struct VecF;
+template <>
+struct VecF<2> {
+  using type = float2;
+  __device__ static void get(const type& v, float* o) { o[0] = v.x; o[1] = v.y; }
+  __device__ static type make(const float* o) { return make_float2(o[0], o[1]); }
+};
+template <>
+struct VecF<4> {
+  using type = float4;
+  __device__ static void get(const type& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+  __device__ static type make(const float* o) { return make_float4(o[0], o[1], o[2], o[3]); }
+};
+
+template <int VEC, int CPT, int KS>
+__global__ void __launch_bounds__(576, 1) k_iter_tma(TmaParams p) {
+  using VT = typename VecF<VEC>::type;
   extern __shared__ __align__(128) unsigned char smem[];
   const int nwarps = blockDim.x >> 5;
-  const int ncw = nwarps - 1;                 // consumer warps; the last warp produces
+  const int ncw = nwarps - 2;                 // consumer warps; then the producer warp and the sync warp
   const int nct = ncw * 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m = p.m, mv = m >> 2;
+  const int m = p.m, mv = m / VEC;
+  const int n = p.n, R = p.R;
+  const int U = p.U, rpu = p.rpu;
   const size_t slot_floats = (size_t)KS * m;
+  // ---- shared memory layout
   float* ring = reinterpret_cast<float*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)p.nslot * slot_floats * 4 + 1024);
+  unsigned char* defer = smem + (size_t)p.nslot * slot_floats * 4 + 1024;     // [2][rpu][m] floats
+  double* rowstat = reinterpret_cast<double*>(defer + (size_t)2 * rpu * m * 4);  // [rpu][4]: M', M, r, log a
+  uint64_t* full = reinterpret_cast<uint64_t*>(rowstat + (size_t)rpu * 4);
   uint64_t* empty = full + p.nslot;
-  unsigned* ctl = reinterpret_cast<unsigned*>(empty + p.nslot);   // [0] issued, [1] producer done, [2] stop
-  double* red = reinterpret_cast<double*>(ctl + 4);               // 32 doubles
+  unsigned* ctl = reinterpret_cast<unsigned*>(empty + p.nslot);   // [0] issued [1] producer done [2] stop
+  // [3] consumer broadcast [4] z generation (completed q-updates) [5] halt (frozen) [6] sync-warp scratch
+  double* red2 = reinterpret_cast<double*>(ctl + 8);              // [2][64] (one-cbar reductions)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nslot; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], ncw);
     }
-    ctl[0] = 0;
-    ctl[1] = 0;
-    ctl[2] = 0;
+    for (int c = 0; c < 8; ++c) ctl[c] = 0;
     fence_mbar_init();
   }
   __syncthreads();
 
-  const int n = p.n, R = p.R;
-  const int U = p.U, rpu = p.rpu;
+  const int u = blockIdx.x;                 // one unit of rows per CTA (the launcher sets grid == U)
+  const int i0 = u * rpu, i1 = min(R, i0 + rpu), nrows = i1 - i0;
 
   if (warp == ncw) {
     // ===================================================================== producer (one lane)
@@ -138,35 +226,132 @@ __global__ void __launch_bounds__(288, 1) k_iter_tma(TmaParams p) {
       const uint64_t pol_last = policy_evict_last();
       uint32_t slot = 0, phase = 0;
       unsigned issued = 0;
+      long long prod_wait = 0;
+      const long long tp0 = clock64();
       const uint32_t row_bytes = (uint32_t)m * 4u;
       for (int t = 0; t < p.iters; ++t) {
-        for (int u = blockIdx.x; u < U; u += gridDim.x) {
-          const int i0 = u * rpu, i1 = min(R, i0 + rpu);
-          for (int i = i0; i < i1; ++i) {
-            const uint64_t pol = i < p.evict_last_rows ? pol_last : pol_first;
-            for (int k0 = 0; k0 < n; k0 += KS) {
-              if (lds_volatile(&ctl[2])) goto producer_done;
-              const int kk = min(KS, n - k0);
-              mbar_wait(&empty[slot], phase ^ 1u);
-              mbar_arrive_expect_tx(&full[slot], (uint32_t)kk * row_bytes);
-              float* dst = ring + (size_t)slot * slot_floats;
-              for (int q = 0; q < kk; ++q)
-                bulk_g2s(dst + (size_t)q * m, p.C + ((size_t)(k0 + q) * R + i) * m, row_bytes, &full[slot], pol);
-              ++issued;
-              *(volatile unsigned*)&ctl[0] = issued;
-              if (++slot == (uint32_t)p.nslot) {
-                slot = 0;
-                phase ^= 1u;
-              }
+        for (int i = i0; i < i1; ++i) {
+          const uint64_t pol = i < p.evict_last_rows ? pol_last : pol_first;
+          for (int k0 = 0; k0 < n; k0 += KS) {
+            if (lds_volatile(&ctl[2])) goto producer_done;
+            const int kk = min(KS, n - k0);
+            const long long tw0 = p.trace ? clock64() : 0;
+            mbar_wait(&empty[slot], phase ^ 1u);
+            if (p.trace) prod_wait += clock64() - tw0;
+            mbar_arrive_expect_tx(&full[slot], (uint32_t)kk * row_bytes);
+            float* dst = ring + (size_t)slot * slot_floats;
+            for (int q = 0; q < kk; ++q)
+              bulk_g2s(dst + (size_t)q * m, p.C + ((size_t)(k0 + q) * R + i) * m, row_bytes, &full[slot], pol);
+            ++issued;
+            *(volatile unsigned*)&ctl[0] = issued;
+            if (++slot == (uint32_t)p.nslot) {
+              slot = 0;
+              phase ^= 1u;
             }
           }
         }
       }
     producer_done:
+      if (p.trace) {
+        p.trace[blockIdx.x * 8 + 0] = prod_wait;
+        p.trace[blockIdx.x * 8 + 1] = clock64() - tp0;
+      }
       __threadfence_block();
       *(volatile unsigned*)&ctl[1] = 1u;
     }
     __syncwarp();
+  } else if (warp == ncw + 1) {
+    // ===================================================================== sync warp
+    // Per iteration t: wait until the consumers published the CTA's column partial of t; B1; column pass
+    // of this CTA's slice; B2; monitor / freeze rule; publish z generation t+1 to the consumers.
+    SolverState st = p.state[0];
+    const long long iters0 = st.iters;
+    const bool sync = !p.rows_only && !(p.diag & COT_DIAG_NO_SYNC);
+    const int cols_per_cta = (m + gridDim.x - 1) / gridDim.x;
+    const int col0 = blockIdx.x * cols_per_cta;
+    const int col1 = min(m, col0 + cols_per_cta);
+    const int nct_h = nct + 32;               // hand-off barrier: consumers + this warp
+    bool active = st.active != 0;
+    if (!p.rows_only && active) {
+      for (int t = 0; t < p.iters; ++t) {
+        handoff_sync(nct_h);                  // consumers published partial t (and w_hat of t)
+        if (!sync) {
+          st.iters += 1;
+          if (lane == 0) sts_release(&ctl[4], (unsigned)(t + 1));
+          continue;
+        }
+        // ---- B1: every CTA's partial of iteration t is published
+        if (lane == 0) {
+          const unsigned gen = ld_acquire(p.bar + 1);
+          if (atom_add_acq_rel(p.bar, 1u) == gridDim.x - 1) {
+            st_relaxed(p.bar, 0u);
+            red_add_release(p.bar + 1, 1u);
+          }
+          while (ld_acquire(p.bar + 1) == gen) __nanosleep(20);
+        }
+        __syncwarp();
+        // ---- column pass: c_j = sum_u P_uj (fixed order: lane-strided units, then the warp_sum tree)
+        const long long itg = iters0 + t + 1;
+        const bool need_resid = (p.tol > 0.0 && itg % p.check_every == 0) || t == p.iters - 1;
+        double dev = 0.0;
+        for (int cb = col0; cb < col1; cb += 8) {
+          double acc[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+          for (int u2 = lane; u2 < U; u2 += 32) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              if (cb + c < col1) acc[c] += __ldcg(p.partials + (size_t)u2 * m + cb + c);
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[c] = warp_sum(acc[c]);
+          const int c = lane;
+          if (c < 8 && cb + c < col1) {
+            double cj = acc[0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q) cj = (c == q) ? acc[q] : cj;
+            const int j = cb + c;
+            const double bj = p.beta[j];
+            dev += fabs(cj - bj);
+            if (!(cj >= 1e-28)) atomicOr(&p.state[0].flags, (int)STATE_UNDERFLOW);
+            p.z_hat[j] = __ldcg(p.z_hat + j) + (log(bj) - log(cj));
+          }
+        }
+        dev = warp_sum(dev);
+        // ---- B2: every q-update of iteration t is written
+        if (lane == 0) {
+          if (need_resid) p.resid_part[blockIdx.x] = dev;
+          const unsigned gen = ld_acquire(p.bar + 3);
+          if (atom_add_acq_rel(p.bar + 2, 1u) == gridDim.x - 1) {
+            st_relaxed(p.bar + 2, 0u);
+            red_add_release(p.bar + 3, 1u);
+          }
+          while (ld_acquire(p.bar + 3) == gen) __nanosleep(20);
+        }
+        __syncwarp();
+        st.iters += 1;
+        if (need_resid) {   // every CTA sums the monitor partials in the same order
+          double r = 0.0;
+          for (int b2 = lane; b2 < (int)gridDim.x; b2 += 32) r += __ldcg(p.resid_part + b2);
+          st.residual = warp_sum(r) * (double)n;
+        }
+        if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
+          st.active = 0;
+          st.converged = 1;
+          if (lane == 0) sts_release(&ctl[5], 1u);   // halt: the consumers discard iteration t+1
+          break;
+        }
+        if (lane == 0) sts_release(&ctl[4], (unsigned)(t + 1));
+      }
+      if (blockIdx.x == 0 && lane == 0) {
+        SolverState out = p.state[0];
+        out.iters = st.iters;
+        out.residual = st.residual;
+        out.active = st.active;
+        out.converged = st.converged;
+        p.state[0] = out;
+      }
+    }
   } else {
     // ===================================================================== consumers
     const int ct = threadIdx.x;
@@ -174,194 +359,273 @@ __global__ void __launch_bounds__(288, 1) k_iter_tma(TmaParams p) {
     const float c2 = (float)(COT_LOG2E * inv_eps);
     uint32_t slot = 0, phase = 0;
     unsigned consumed = 0;
-    SolverState st = p.state[0];
-    bool active = st.active != 0;
-    const int cols_per_cta = (m + gridDim.x - 1) / gridDim.x;
-    const int col0 = blockIdx.x * cols_per_cta;
-    const int col1 = min(m, col0 + cols_per_cta);
-    bool pending = false;       // a q-update barrier whose wait is deferred to the next epilogue
-    unsigned pending_gen = 0;
-    for (int t = 0; t < p.iters && active; ++t) {
-      for (int u = blockIdx.x; u < U; u += gridDim.x) {
-        const int i0 = u * rpu, i1 = min(R, i0 + rpu);
-        double z[CPT][4], P[CPT][4];
-        float4 gnext[CPT];
+    int rbuf = 0;                             // red2 buffer parity (uniform)
+    const bool active0 = p.state[0].active != 0;
+    const int nct_h = nct + 32;
+    long long c_ksum = 0, c_epi = 0, c_sync = 0;
+    const long long tc0 = clock64();
+
+    // per-row constants: log alpha_i; no previous row maximum yet (NaN => exact two-pass epilogue)
+    for (int r = ct; r < nrows; r += nct) {
+      const double a = p.alpha[p.row_begin + i0 + r];
+      rowstat[r * 4 + 0] = __longlong_as_double(0x7ff8000000000000LL);
+      rowstat[r * 4 + 3] = log(a);
+    }
+    cbar(nct);
+
+    double z[CPT][VEC], P[CPT][VEC];
+    VT gnext[CPT];
+    auto load_z = [&]() {
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const int jv = q * nct + ct;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) z[q][v] = jv < mv ? __ldcg(p.z_hat + VEC * jv + v) : 0.0;
+      }
+    };
+    auto load_g = [&](int row) {
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const int jv = q * nct + ct;
+        float zero[VEC] = {};
+        gnext[q] = jv < mv ? __ldg(reinterpret_cast<const VT*>(p.G + (size_t)row * m) + jv) : VecF<VEC>::make(zero);
+      }
+    };
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      ++consumed;
+      if (++slot == (uint32_t)p.nslot) {
+        slot = 0;
+        phase ^= 1u;
+      }
+    };
+    auto ksum_slot = [&](const VT* sb, int kk, const float (&gc)[CPT][VEC], float (&s)[CPT][VEC]) {
+      for (int q2 = 0; q2 < kk; ++q2) {
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
-          const int jv = q * nct + ct;
-          const bool ok = jv < mv;
+          float c[VEC];
+          VecF<VEC>::get(sb[q2 * mv + q * nct + ct], c);
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            z[q][v] = (ok && !pending) ? __ldcg(p.z_hat + 4 * jv + v) : 0.0;
-            P[q][v] = 0.0;
-          }
-          gnext[q] = ok ? __ldg(reinterpret_cast<const float4*>(p.G + (size_t)i0 * m) + jv) : make_float4(0, 0, 0, 0);
+          for (int v = 0; v < VEC; ++v) s[q][v] += ex2(fmaf(-c[v], c2, gc[q][v]));
         }
-        for (int i = i0; i < i1; ++i) {
-          float g[CPT][4], gc[CPT][4], s[CPT][4];
-          const bool first_row = (i == i0) && (u == (int)blockIdx.x);
+      }
+    };
+    // ---- the streamed k-sum of one row over its slots. Threads past the last column read (in-bounds)
+    //      smem garbage that the epilogue masks out, so the body has no per-column branches.
+    auto ksum = [&](const float (&gc)[CPT][VEC], float (&s)[CPT][VEC]) {
+      const long long tk0 = p.trace ? clock64() : 0;
+      int k0 = 0;
+      for (; k0 + KS <= n; k0 += KS) {
+        mbar_wait(&full[slot], phase);
+        const VT* sb = reinterpret_cast<const VT*>(ring + (size_t)slot * slot_floats);
+        if (!(p.diag & COT_DIAG_NO_COMPUTE)) {
 #pragma unroll
-          for (int q = 0; q < CPT; ++q) {
-            g[q][0] = gnext[q].x;
-            g[q][1] = gnext[q].y;
-            g[q][2] = gnext[q].z;
-            g[q][3] = gnext[q].w;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              gc[q][v] = g[q][v] * c2;
-              s[q][v] = 0.f;
-            }
-            const int jv = q * nct + ct;
-            if (i + 1 < i1 && jv < mv) gnext[q] = __ldg(reinterpret_cast<const float4*>(p.G + (size_t)(i + 1) * m) + jv);
-          }
-          // ---- the streamed k-sum over this row's slots. Threads past the last column read (in-bounds)
-          //      smem garbage that the epilogue masks out, so the body has no per-column branches.
-          int k0 = 0;
-          for (; k0 + KS <= n; k0 += KS) {
-            mbar_wait(&full[slot], phase);
-            const float4* sb = reinterpret_cast<const float4*>(ring + (size_t)slot * slot_floats);
-#pragma unroll
-            for (int q2 = 0; q2 < KS; ++q2) {
-#pragma unroll
-              for (int q = 0; q < CPT; ++q) {
-                const float4 c = sb[q2 * mv + q * nct + ct];
-                s[q][0] += ex2(fmaf(-c.x, c2, gc[q][0]));
-                s[q][1] += ex2(fmaf(-c.y, c2, gc[q][1]));
-                s[q][2] += ex2(fmaf(-c.z, c2, gc[q][2]));
-                s[q][3] += ex2(fmaf(-c.w, c2, gc[q][3]));
-              }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);
-            ++consumed;
-            if (++slot == (uint32_t)p.nslot) {
-              slot = 0;
-              phase ^= 1u;
-            }
-          }
-          if (k0 < n) {   // ragged last slot of the row (n % KS != 0)
-            const int kk = n - k0;
-            mbar_wait(&full[slot], phase);
-            const float4* sb = reinterpret_cast<const float4*>(ring + (size_t)slot * slot_floats);
-            for (int q2 = 0; q2 < kk; ++q2) {
-#pragma unroll
-              for (int q = 0; q < CPT; ++q) {
-                const float4 c = sb[q2 * mv + q * nct + ct];
-                s[q][0] += ex2(fmaf(-c.x, c2, gc[q][0]));
-                s[q][1] += ex2(fmaf(-c.y, c2, gc[q][1]));
-                s[q][2] += ex2(fmaf(-c.z, c2, gc[q][2]));
-                s[q][3] += ex2(fmaf(-c.w, c2, gc[q][3]));
-              }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);
-            ++consumed;
-            if (++slot == (uint32_t)p.nslot) {
-              slot = 0;
-              phase ^= 1u;
-            }
-          }
-          // ---- fp64 row epilogue (needs z_hat of the previous q-update: wait for that barrier here,
-          //      after this row's k-sum, which does not depend on z)
-          if (first_row && pending) {
-            grid_wait(p.bar + 2, pending_gen, nct);
-            pending = false;
+          for (int q2 = 0; q2 < KS; ++q2) {
 #pragma unroll
             for (int q = 0; q < CPT; ++q) {
-              const int jv = q * nct + ct;
+              float c[VEC];
+              VecF<VEC>::get(sb[q2 * mv + q * nct + ct], c);
 #pragma unroll
-              for (int v = 0; v < 4; ++v) z[q][v] = jv < mv ? __ldcg(p.z_hat + 4 * jv + v) : 0.0;
+              for (int v = 0; v < VEC; ++v) s[q][v] += ex2(fmaf(-c[v], c2, gc[q][v]));
             }
           }
-          double x[CPT][4];
-          double lmax = -INFINITY;
-#pragma unroll
-          for (int q = 0; q < CPT; ++q) {
-            const bool ok = q * nct + ct < mv;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              x[q][v] = ok ? z[q][v] - (double)g[q][v] * inv_eps : -INFINITY;
-              lmax = fmax(lmax, x[q][v]);
-            }
-          }
-          const double M = cblk_max(lmax, red, nct);
-          double tt[CPT][4];
-          double lsum = 0.0;
-#pragma unroll
-          for (int q = 0; q < CPT; ++q) {
-            const bool ok = q * nct + ct < mv;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const double e = (double)ex2((float)((x[q][v] - M) * COT_LOG2E));
-              tt[q][v] = ok ? (double)s[q][v] * e : 0.0;
-              lsum += tt[q][v];
-            }
-          }
-          const double r = cblk_sum(lsum, red, nct);
-          const double a = p.alpha[p.row_begin + i];
-          if (ct == 0) p.w_hat[p.row_begin + i] = log(a) - M - log(r);
-          const double rho = a / r;
-#pragma unroll
-          for (int q = 0; q < CPT; ++q)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) P[q][v] = fma(rho, tt[q][v], P[q][v]);
         }
+        release();
+      }
+      if (k0 < n) {   // ragged last slot of the row (n % KS != 0)
+        mbar_wait(&full[slot], phase);
+        if (!(p.diag & COT_DIAG_NO_COMPUTE))
+          ksum_slot(reinterpret_cast<const VT*>(ring + (size_t)slot * slot_floats), n - k0, gc, s);
+        release();
+      }
+      if (p.trace) c_ksum += clock64() - tk0;
+    };
+    // ---- fp64 row epilogue of row r (global row i0 + r): p-update statistics and the column partial
+    auto epilogue = [&](int r, const float (&g)[CPT][VEC], const float (&s)[CPT][VEC]) {
+      const long long te0 = p.trace ? clock64() : 0;
+      double x[CPT][VEC];
+      double lmax = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const bool ok = q * nct + ct < mv;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          x[q][v] = ok ? z[q][v] - (double)g[q][v] * inv_eps : -INFINITY;
+          lmax = fmax(lmax, x[q][v]);
+        }
+      }
+      double Mref = rowstat[r * 4 + 0];
+      double tt[CPT][VEC];
+      double Mtrue, rsum;
+      bool exact = !(Mref == Mref);            // no previous maximum: two-pass
+      if (!exact) {
+        double lsum = 0.0;
+#pragma unroll
+        for (int q = 0; q < CPT; ++q)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            tt[q][v] = (x[q][v] == -INFINITY) ? 0.0 : (double)s[q][v] * exp_split(x[q][v] - Mref);
+            lsum += tt[q][v];
+          }
+        Mtrue = lmax;
+        rsum = lsum;
+        cblk_maxsum(Mtrue, rsum, red2, rbuf, nct);
+        exact = !(fabs(Mtrue - Mref) < 500.0);  // shifted sum out of the safe fp64 range: redo exactly
+      } else {
+        Mtrue = cblk_max1(lmax, red2, rbuf, nct);
+      }
+      if (exact) {
+        Mref = Mtrue;
+        double lsum = 0.0;
+#pragma unroll
+        for (int q = 0; q < CPT; ++q)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            tt[q][v] = (x[q][v] == -INFINITY) ? 0.0 : (double)s[q][v] * exp_split(x[q][v] - Mref);
+            lsum += tt[q][v];
+          }
+        rsum = cblk_sum1(lsum, red2, rbuf, nct);
+      }
+      // alpha_i / r_i with a fast reciprocal and two Newton steps (fp64 accuracy)
+      double rinv = (double)__frcp_rn((float)rsum);
+      rinv = rinv * fma(-rsum, rinv, 2.0);
+      rinv = rinv * fma(-rsum, rinv, 2.0);
+      const double rho = p.alpha[p.row_begin + i0 + r] * rinv;
+      if (ct == 0) {
+        rowstat[r * 4 + 0] = Mtrue;            // reference for the next iteration
+        rowstat[r * 4 + 1] = Mref;             // shift used for r_i
+        rowstat[r * 4 + 2] = rsum;
+      }
+#pragma unroll
+      for (int q = 0; q < CPT; ++q)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) P[q][v] = fma(rho, tt[q][v], P[q][v]);
+      if (p.trace) c_epi += clock64() - te0;
+    };
+    // deferred rows: s and g parked in shared memory (each thread keeps its own columns)
+    VT* spend = reinterpret_cast<VT*>(defer);
+    VT* gpend = spend + (size_t)rpu * mv;
+    auto park = [&](int r, const float (&g)[CPT][VEC], const float (&s)[CPT][VEC]) {
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const int jv = q * nct + ct;
+        if (jv < mv) {
+          spend[(size_t)r * mv + jv] = VecF<VEC>::make(s[q]);
+          gpend[(size_t)r * mv + jv] = VecF<VEC>::make(g[q]);
+        }
+      }
+    };
+    auto unpark_epilogue = [&](int r) {
+      float g[CPT][VEC], s[CPT][VEC];
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const int jv = q * nct + ct;
+        if (jv < mv) {
+          VecF<VEC>::get(spend[(size_t)r * mv + jv], s[q]);
+          VecF<VEC>::get(gpend[(size_t)r * mv + jv], g[q]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) s[q][v] = g[q][v] = 0.f;
+        }
+      }
+      epilogue(r, g, s);
+    };
+    // CTA-uniform view of the sync warp's progress: returns the z generation; sets `halt`.
+    auto observe = [&](bool block, unsigned need, bool& halt) -> unsigned {
+      if (ct == 0) {
+        unsigned zg = lds_acquire(&ctl[4]);
+        unsigned h = lds_acquire(&ctl[5]);
+        while (block && zg < need && !h) {
+          __nanosleep(32);
+          zg = lds_acquire(&ctl[4]);
+          h = lds_acquire(&ctl[5]);
+        }
+        ctl[3] = h ? 0xffffffffu : zg;
+      }
+      cbar(nct);
+      const unsigned v = ctl[3];
+      cbar(nct);
+      halt = (v == 0xffffffffu);
+      return halt ? 0u : v;
+    };
+
+#pragma unroll
+    for (int q = 0; q < CPT; ++q)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
+    if (active0) {
+      load_z();
+      load_g(i0);
+    }
+    // Iteration t needs the q-update of iteration t-1: z generation >= t. k-sums of iteration t stream
+    // as slots arrive; epilogues run as soon as that generation is visible (parked rows first).
+    bool z_ready = true, halt = false;
+    int t = 0, kr = 0, er = 0;
+    while (active0 && t < p.iters) {
+      if (kr < nrows) {
+        float g[CPT][VEC], gc[CPT][VEC], s[CPT][VEC];
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          VecF<VEC>::get(gnext[q], g[q]);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            gc[q][v] = g[q][v] * c2;
+            s[q][v] = 0.f;
+          }
+        }
+        load_g(kr + 1 < nrows ? i0 + kr + 1 : i0);
+        ksum(gc, s);
+        if (z_ready && er == kr) {
+          epilogue(kr, g, s);
+          ++er;
+        } else {
+          park(kr, g, s);
+        }
+        ++kr;
+      }
+      if (!z_ready) {
+        const long long ts0 = p.trace ? clock64() : 0;
+        const unsigned zg = observe(kr == nrows, (unsigned)t, halt);
+        if (p.trace) c_sync += clock64() - ts0;
+        if (halt) break;                      // frozen after iteration t-1: iteration t is discarded
+        if (zg >= (unsigned)t) {
+          load_z();
+          z_ready = true;
+        }
+      }
+      if (z_ready)
+        while (er < kr) {
+          unpark_epilogue(er);
+          ++er;
+        }
+      if (er == nrows) {                      // iteration t complete on this CTA: publish
+        cbar(nct);
+        for (int r = ct; r < nrows; r += nct)
+          p.w_hat[p.row_begin + i0 + r] = rowstat[r * 4 + 3] - rowstat[r * 4 + 1] - log(rowstat[r * 4 + 2]);
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
           const int jv = q * nct + ct;
-          if (jv < mv)
-            reinterpret_cast<double4*>(p.partials + (size_t)u * m)[jv] = make_double4(P[q][0], P[q][1], P[q][2], P[q][3]);
+          if (jv < mv) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) p.partials[(size_t)u * m + (size_t)VEC * jv + v] = P[q][v];
+          }
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
         }
-      }
-      if (p.rows_only) break;
-      // ---- column pass over this CTA's column slice (fixed order => deterministic)
-      grid_barrier(p.bar, nct);
-      double dev = 0.0;
-      for (int j = col0 + warp; j < col1; j += ncw) {
-        double acc = 0.0;
-        for (int u = lane; u < U; u += 32) acc += __ldcg(p.partials + (size_t)u * m + j);
-        acc = warp_sum(acc);
-        if (lane == 0) {
-          const double bj = p.beta[j];
-          dev += fabs(acc - bj);
-          if (!(acc >= 1e-28)) atomicOr(&p.state[0].flags, (int)STATE_UNDERFLOW);
-          p.z_hat[j] = __ldcg(p.z_hat + j) + (log(bj) - log(acc));
-        }
-      }
-      // the monitor is needed at check iterations (freeze rule) and after the last iteration (report)
-      const bool need_resid = (p.tol > 0.0 && (st.iters + 1) % p.check_every == 0) || (t == p.iters - 1);
-      if (need_resid) {
-        dev = cblk_sum(dev, red, nct);
-        if (ct == 0) p.resid_part[blockIdx.x] = dev;
-        grid_barrier(p.bar + 2, nct);
-        if (warp == 0) {
-          double r = 0.0;
-          for (int b2 = lane; b2 < (int)gridDim.x; b2 += 32) r += __ldcg(p.resid_part + b2);
-          r = warp_sum(r);
-          if (lane == 0) red[0] = r * (double)n;
-        }
-        cbar(nct);
-        st.residual = red[0];
-        cbar(nct);
-      } else {
-        pending_gen = grid_arrive(p.bar + 2, nct);
-        pending = true;
-      }
-      st.iters += 1;
-      if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
-        st.active = 0;
-        st.converged = 1;
-        active = false;
+        if (p.rows_only) break;
+        handoff_arrive(nct_h);                // to the sync warp (orders these writes before its B1)
+        ++t;
+        kr = 0;
+        er = 0;
+        z_ready = false;
       }
     }
-    if (pending) grid_wait(p.bar + 2, pending_gen, nct);
-    if (blockIdx.x == 0 && ct == 0 && !p.rows_only) {
-      SolverState out = p.state[0];
-      out.iters = st.iters;
-      out.residual = st.residual;
-      out.active = st.active;
-      out.converged = st.converged;
-      p.state[0] = out;
+    if (p.trace && ct == 0) {
+      p.trace[blockIdx.x * 8 + 3] = c_ksum;
+      p.trace[blockIdx.x * 8 + 4] = c_epi;
+      p.trace[blockIdx.x * 8 + 5] = c_sync;
+      p.trace[blockIdx.x * 8 + 6] = clock64() - tc0;
     }
     // ---- drain: stop the producer and consume whatever it already issued
     if (ct == 0) *(volatile unsigned*)&ctl[2] = 1u;
@@ -372,13 +636,7 @@ __global__ void __launch_bounds__(288, 1) k_iter_tma(TmaParams p) {
       const unsigned iss = lds_volatile(&ctl[0]);
       if (consumed < iss) {
         mbar_wait(&full[slot], phase);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        ++consumed;
-        if (++slot == (uint32_t)p.nslot) {
-          slot = 0;
-          phase ^= 1u;
-        }
+        release();
       } else if (done) {
         if (consumed >= lds_volatile(&ctl[0])) break;
       }
@@ -412,13 +670,18 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
   p.U = (int)up.U;
   const int row_bytes = (int)a.m * 4;
   int KS = 1;
-  while (KS * 2 <= 16 && KS * 2 * row_bytes <= 16384 && KS * 2 <= (int)a.n) KS *= 2;
+  int ks_bytes = 32768;
+  if (const char* ev = getenv("COT_SLOT_BYTES")) ks_bytes = atoi(ev);   // tuning experiments
+  while (KS * 2 <= 16 && KS * 2 * row_bytes <= ks_bytes && KS * 2 <= (int)a.n) KS *= 2;
   p.KS = KS;
   const size_t slot_bytes = (size_t)p.KS * row_bytes;
-  const size_t budget = 200 * 1024;
-  p.nslot = (int)std::max<size_t>(2, std::min<size_t>(64, (budget - 2048) / slot_bytes));
-  // ring + 1 KiB pad (branch-free over-reads past the last column stay in-bounds) + barriers + control
-  const size_t smem = (size_t)p.nslot * slot_bytes + 1024 + (size_t)p.nslot * 16 + 16 + 32 * 8 + 64;
+  const size_t defer_bytes = (size_t)2 * p.rpu * a.m * 4 + (size_t)p.rpu * 4 * 8;
+  const size_t budget = 210 * 1024;
+  if (defer_bytes + 2 * slot_bytes + 4096 > budget) return cudaErrorInvalidConfiguration;
+  p.nslot = (int)std::max<size_t>(2, std::min<size_t>(64, (budget - defer_bytes - 4096) / slot_bytes));
+  // ring + 1 KiB pad (branch-free over-reads past the last column stay in-bounds) + deferred rows +
+  // row statistics + barriers + control + reduction scratch
+  const size_t smem = (size_t)p.nslot * slot_bytes + 1024 + defer_bytes + (size_t)p.nslot * 16 + 32 + 128 * 8 + 64;
   p.iters = rows_only ? 1 : iters;
   p.rows_only = rows_only ? 1 : 0;
   p.tol = a.tol;
@@ -428,21 +691,32 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
   p.state = ws.state;
   p.bar = ws.grid_bar;
   p.evict_last_rows = 0;
-  const int mv = (int)a.m / 4;
-  int ncw = (mv + 31) / 32;
-  int cpt = 1;
-  while (ncw > 8) {
-    cpt *= 2;
-    ncw = (mv / cpt + 31) / 32;
+  p.diag = (int)(a.flags & (COT_DIAG_NO_COMPUTE | COT_DIAG_NO_SYNC));
+  if (const char* ev = getenv("COT_EVICT_LAST_ROWS")) p.evict_last_rows = atoi(ev);   // L2 residency experiment
+  p.trace = nullptr;
+  static unsigned long long* trace_buf = nullptr;   // diagnostics only (COT_TRACE=1)
+  if (getenv("COT_TRACE")) {
+    if (!trace_buf) cudaMalloc(&trace_buf, 4096 * 8 * sizeof(unsigned long long));
+    p.trace = trace_buf;
   }
-  const int threads = (ncw + 1) * 32;
+  // columns per thread: VEC (2 or 4) x CPT; up to 16 consumer warps
+  const int m = (int)a.m;
+  int VEC = 2, cpt = 1;
+  if (m >= 512) VEC = 4;
+  if (const char* ev = getenv("COT_VEC")) VEC = std::max(VEC, atoi(ev));   // tuning experiments
+  int ncw = (m / VEC + 31) / 32;
+  while (ncw > 16) {
+    cpt *= 2;
+    ncw = (m / VEC / cpt + 31) / 32;
+  }
+  const int threads = (ncw + 2) * 32;
   cudaError_t e;
   void* fn = nullptr;
-#define COT_PICK(C_, K_) \
-  if (cpt == C_ && KS == K_) fn = (void*)k_iter_tma<C_, K_>;
-  COT_PICK(1, 1) COT_PICK(1, 2) COT_PICK(1, 4) COT_PICK(1, 8) COT_PICK(1, 16)
-  COT_PICK(2, 1) COT_PICK(2, 2) COT_PICK(2, 4) COT_PICK(2, 8) COT_PICK(2, 16)
-  COT_PICK(4, 1) COT_PICK(4, 2) COT_PICK(4, 4) COT_PICK(4, 8) COT_PICK(4, 16)
+#define COT_PICK(V_, C_, K_) \
+  if (VEC == V_ && cpt == C_ && KS == K_) fn = (void*)k_iter_tma<V_, C_, K_>;
+  COT_PICK(2, 1, 1) COT_PICK(2, 1, 2) COT_PICK(2, 1, 4) COT_PICK(2, 1, 8) COT_PICK(2, 1, 16)
+  COT_PICK(4, 1, 1) COT_PICK(4, 1, 2) COT_PICK(4, 1, 4) COT_PICK(4, 1, 8) COT_PICK(4, 1, 16)
+  COT_PICK(4, 2, 1) COT_PICK(4, 2, 2) COT_PICK(4, 2, 4) COT_PICK(4, 2, 8) COT_PICK(4, 2, 16)
 #undef COT_PICK
   if (!fn) return cudaErrorInvalidValue;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -451,10 +725,29 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
-  const int grid = (int)std::min<int64_t>(up.U, (int64_t)occ * sms);
+  if (up.U > (int64_t)occ * sms) return cudaErrorInvalidConfiguration;   // one unit per co-resident CTA
+  const int grid = (int)up.U;
   void* args[] = {&p};
   if (rows_only) return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, s);
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, s);
+  e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, s);
+  if (e == cudaSuccess && p.trace) {   // diagnostics: print cycle breakdown (averaged over CTAs)
+    std::vector<unsigned long long> h((size_t)grid * 8);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    double acc[8] = {0}, mx[8] = {0};
+    for (int b = 0; b < grid; ++b)
+      for (int k = 0; k < 8; ++k) {
+        acc[k] += (double)h[(size_t)b * 8 + k] / grid;
+        mx[k] = std::max(mx[k], (double)h[(size_t)b * 8 + k]);
+      }
+    const double it = iters > 0 ? iters : 1;
+    fprintf(stderr,
+            "[cot trace] iters=%d per-iter cycles (mean/max over CTAs): prod_wait %.0f/%.0f prod_total %.0f/%.0f "
+            "cons_ksum %.0f/%.0f cons_epi %.0f/%.0f cons_sync %.0f/%.0f cons_total %.0f/%.0f\n",
+            iters, acc[0] / it, mx[0] / it, acc[1] / it, mx[1] / it, acc[3] / it, mx[3] / it, acc[4] / it,
+            mx[4] / it, acc[5] / it, mx[5] / it, acc[6] / it, mx[6] / it);
+  }
+  return e;
 }
 
 }  // namespace cot
