@@ -50,6 +50,7 @@ struct TmaParams {
   double* resid_part;    // [gridDim.x]
   SolverState* state;    // [1]
   unsigned* bar;         // [4]: two device-wide barriers {arrival count, generation}
+  int nk, ne, qn;        // k-sum warps, epilogue warps, row-queue depth
   int evict_last_rows;   // rows [0, evict_last_rows) of every block are streamed with an L2 evict_last hint
   int diag;              // COT_DIAG_* bits (diagnostics only)
   unsigned long long* trace;   // diagnostics: [grid][8] cycle counters, or nullptr
@@ -129,8 +130,9 @@ __device__ __forceinline__ double cblk_sum(double v, double* sh, int nct) {
 }
 // One-cbar block reductions for the epilogues: double-buffered scratch (`buf` alternates; the next
 // reduction's cbar orders every read of this buffer before its reuse two reductions later).
-__device__ __forceinline__ void cblk_maxsum(double& mx, double& sm, double* red2, int& buf, int nct) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+__device__ __forceinline__ void cblk_maxsum(double& mx, double& sm, double* red2, int& buf, int nct,
+                                            int wbase) {
+  const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) - wbase;   // warp index within the group
   mx = warp_max(mx);
   sm = warp_sum(sm);
   double* r = red2 + buf * 64;
@@ -148,14 +150,14 @@ __device__ __forceinline__ void cblk_maxsum(double& mx, double& sm, double* red2
   sm = S;
   buf ^= 1;
 }
-__device__ __forceinline__ double cblk_max1(double v, double* red2, int& buf, int nct) {
+__device__ __forceinline__ double cblk_max1(double v, double* red2, int& buf, int nct, int wbase) {
   double s = 0.0;
-  cblk_maxsum(v, s, red2, buf, nct);
+  cblk_maxsum(v, s, red2, buf, nct, wbase);
   return v;
 }
-__device__ __forceinline__ double cblk_sum1(double v, double* red2, int& buf, int nct) {
+__device__ __forceinline__ double cblk_sum1(double v, double* red2, int& buf, int nct, int wbase) {
   double m = -INFINITY;
-  cblk_maxsum(m, v, red2, buf, nct);
+  cblk_maxsum(m, v, red2, buf, nct, wbase);
   return v;
 }
 
@@ -184,44 +186,55 @@ struct VecF<4> {
   __device__ static type make(const float* o) { return make_float4(o[0], o[1], o[2], o[3]); }
 };
 
-template <int VEC, int CPT, int KS>
-__global__ void __launch_bounds__(576, 1) k_iter_tma(TmaParams p) {
-  using VT = typename VecF<VEC>::type;
+template <int CPT, int EPT, int KS>
+__global__ void __launch_bounds__(448, 1) k_iter_tma(TmaParams p) {
+  constexpr int VEC = 4;
+  using VT = float4;
   extern __shared__ __align__(128) unsigned char smem[];
-  const int nwarps = blockDim.x >> 5;
-  const int ncw = nwarps - 2;                 // consumer warps; then the producer warp and the sync warp
-  const int nct = ncw * 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = p.nk, ne = p.ne;             // k-sum warps, epilogue warps; then producer, sync warps
+  const int nkt = nk * 32, net = ne * 32;
+  const int wprod = nk + ne, wsync = nk + ne + 1;
   const int m = p.m, mv = m / VEC;
   const int n = p.n, R = p.R;
-  const int U = p.U, rpu = p.rpu;
+  const int U = p.U, rpu = p.rpu, QN = p.qn;
   const size_t slot_floats = (size_t)KS * m;
   // ---- shared memory layout
   float* ring = reinterpret_cast<float*>(smem);
-  unsigned char* defer = smem + (size_t)p.nslot * slot_floats * 4 + 1024;     // [2][rpu][m] floats
-  double* rowstat = reinterpret_cast<double*>(defer + (size_t)2 * rpu * m * 4);  // [rpu][4]: M', M, r, log a
+  float* queue = reinterpret_cast<float*>(smem + (size_t)p.nslot * slot_floats * 4 + 1024);   // [QN][m]
+  double* rowstat = reinterpret_cast<double*>(queue + (size_t)QN * m);   // [rpu][4]: M', M, r, log alpha
   uint64_t* full = reinterpret_cast<uint64_t*>(rowstat + (size_t)rpu * 4);
   uint64_t* empty = full + p.nslot;
-  unsigned* ctl = reinterpret_cast<unsigned*>(empty + p.nslot);   // [0] issued [1] producer done [2] stop
-  // [3] consumer broadcast [4] z generation (completed q-updates) [5] halt (frozen) [6] sync-warp scratch
-  double* red2 = reinterpret_cast<double*>(ctl + 8);              // [2][64] (one-cbar reductions)
+  uint64_t* qfull = empty + p.nslot;
+  uint64_t* qempty = qfull + QN;
+  unsigned* ctl = reinterpret_cast<unsigned*>(qempty + QN);
+  // ctl: [0] TMA slots issued [1] producer done [2] stop producer [4] z generation (completed q-updates)
+  //      [5] halt (frozen) [6] rows produced by the k-sum warps [7] k-sum warps done
+  //      [8] k-sum broadcast [9] epilogue broadcast
+  double* red2 = reinterpret_cast<double*>(ctl + 16);   // [2][64]
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nslot; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], ncw);
+      mbar_init(&empty[s], nk);
     }
-    for (int c = 0; c < 8; ++c) ctl[c] = 0;
+    for (int q = 0; q < QN; ++q) {
+      mbar_init(&qfull[q], nk);
+      mbar_init(&qempty[q], ne);
+    }
+    for (int c = 0; c < 16; ++c) ctl[c] = 0;
     fence_mbar_init();
   }
   __syncthreads();
 
   const int u = blockIdx.x;                 // one unit of rows per CTA (the launcher sets grid == U)
   const int i0 = u * rpu, i1 = min(R, i0 + rpu), nrows = i1 - i0;
+  const bool active0 = p.state[0].active != 0;
+  const double inv_eps = 1.0 / p.eps[0];
 
-  if (warp == ncw) {
+  if (warp == wprod) {
     // ===================================================================== producer (one lane)
-    if (lane == 0) {
+    if (lane == 0 && active0) {
       const uint64_t pol_first = policy_evict_first();
       const uint64_t pol_last = policy_evict_last();
       uint32_t slot = 0, phase = 0;
@@ -256,25 +269,25 @@ __global__ void __launch_bounds__(576, 1) k_iter_tma(TmaParams p) {
         p.trace[blockIdx.x * 8 + 0] = prod_wait;
         p.trace[blockIdx.x * 8 + 1] = clock64() - tp0;
       }
+    }
+    if (lane == 0) {
       __threadfence_block();
       *(volatile unsigned*)&ctl[1] = 1u;
     }
     __syncwarp();
-  } else if (warp == ncw + 1) {
+  } else if (warp == wsync) {
     // ===================================================================== sync warp
-    // Per iteration t: wait until the consumers published the CTA's column partial of t; B1; column pass
-    // of this CTA's slice; B2; monitor / freeze rule; publish z generation t+1 to the consumers.
+    // Per iteration t: wait until the epilogue warps published the CTA's column partial of t; B1; column
+    // pass of this CTA's slice; B2; monitor / freeze rule; publish z generation t+1 (or halt).
     SolverState st = p.state[0];
     const long long iters0 = st.iters;
     const bool sync = !p.rows_only && !(p.diag & COT_DIAG_NO_SYNC);
     const int cols_per_cta = (m + gridDim.x - 1) / gridDim.x;
     const int col0 = blockIdx.x * cols_per_cta;
     const int col1 = min(m, col0 + cols_per_cta);
-    const int nct_h = nct + 32;               // hand-off barrier: consumers + this warp
-    bool active = st.active != 0;
-    if (!p.rows_only && active) {
+    if (!p.rows_only && active0) {
       for (int t = 0; t < p.iters; ++t) {
-        handoff_sync(nct_h);                  // consumers published partial t (and w_hat of t)
+        handoff_sync(net + 32);               // epilogue warps published partial t (and w_hat of t)
         if (!sync) {
           st.iters += 1;
           if (lane == 0) sts_release(&ctl[4], (unsigned)(t + 1));
@@ -338,7 +351,7 @@ __global__ void __launch_bounds__(576, 1) k_iter_tma(TmaParams p) {
         if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
           st.active = 0;
           st.converged = 1;
-          if (lane == 0) sts_release(&ctl[5], 1u);   // halt: the consumers discard iteration t+1
+          if (lane == 0) sts_release(&ctl[5], 1u);   // halt: iteration t+1 is discarded
           break;
         }
         if (lane == 0) sts_release(&ctl[4], (unsigned)(t + 1));
@@ -352,43 +365,23 @@ __global__ void __launch_bounds__(576, 1) k_iter_tma(TmaParams p) {
         p.state[0] = out;
       }
     }
-  } else {
-    // ===================================================================== consumers
-    const int ct = threadIdx.x;
-    const double inv_eps = 1.0 / p.eps[0];
+  } else if (warp < nk) {
+    // ===================================================================== k-sum warps
+    // s_ij = sum_k exp2((G_ij - C_ijk) log2e/eps) for every row, streamed from the TMA ring into the row
+    // queue; never waits for the potentials. Threads past the last column compute (in-bounds) garbage that
+    // the epilogue masks out, so the slot body has no per-column branches.
+    const int kt = threadIdx.x;
     const float c2 = (float)(COT_LOG2E * inv_eps);
-    uint32_t slot = 0, phase = 0;
-    unsigned consumed = 0;
-    int rbuf = 0;                             // red2 buffer parity (uniform)
-    const bool active0 = p.state[0].active != 0;
-    const int nct_h = nct + 32;
-    long long c_ksum = 0, c_epi = 0, c_sync = 0;
-    const long long tc0 = clock64();
-
-    // per-row constants: log alpha_i; no previous row maximum yet (NaN => exact two-pass epilogue)
-    for (int r = ct; r < nrows; r += nct) {
-      const double a = p.alpha[p.row_begin + i0 + r];
-      rowstat[r * 4 + 0] = __longlong_as_double(0x7ff8000000000000LL);
-      rowstat[r * 4 + 3] = log(a);
-    }
-    cbar(nct);
-
-    double z[CPT][VEC], P[CPT][VEC];
+    uint32_t slot = 0, phase = 0, qs = 0, qph = 0;
+    unsigned consumed = 0, produced = 0;
+    long long c_ksum = 0;
     VT gnext[CPT];
-    auto load_z = [&]() {
-#pragma unroll
-      for (int q = 0; q < CPT; ++q) {
-        const int jv = q * nct + ct;
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) z[q][v] = jv < mv ? __ldcg(p.z_hat + VEC * jv + v) : 0.0;
-      }
-    };
     auto load_g = [&](int row) {
 #pragma unroll
       for (int q = 0; q < CPT; ++q) {
-        const int jv = q * nct + ct;
-        float zero[VEC] = {};
-        gnext[q] = jv < mv ? __ldg(reinterpret_cast<const VT*>(p.G + (size_t)row * m) + jv) : VecF<VEC>::make(zero);
+        const int jv = q * nkt + kt;
+        gnext[q] = jv < mv ? __ldg(reinterpret_cast<const VT*>(p.G + (size_t)row * m) + jv)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     };
     auto release = [&]() {
@@ -400,20 +393,27 @@ __global__ void __launch_bounds__(576, 1) k_iter_tma(TmaParams p) {
         phase ^= 1u;
       }
     };
-    auto ksum_slot = [&](const VT* sb, int kk, const float (&gc)[CPT][VEC], float (&s)[CPT][VEC]) {
-      for (int q2 = 0; q2 < kk; ++q2) {
+    if (active0) load_g(i0);
+    const int total_rows = p.iters * nrows;
+    for (int rr = 0; active0 && rr < total_rows; ++rr) {
+      // CTA-uniform (k-sum warps) check of the halt flag
+      if (kt == 0) ctl[8] = lds_acquire(&ctl[5]);
+      asm volatile("bar.sync 3, %0;" ::"r"(nkt) : "memory");
+      const bool halt = ctl[8] != 0;
+      asm volatile("bar.sync 3, %0;" ::"r"(nkt) : "memory");
+      if (halt) break;
+      const int r = rr % nrows;
+      float gc[CPT][VEC], s[CPT][VEC];
 #pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-          float c[VEC];
-          VecF<VEC>::get(sb[q2 * mv + q * nct + ct], c);
+      for (int q = 0; q < CPT; ++q) {
+        gc[q][0] = gnext[q].x * c2;
+        gc[q][1] = gnext[q].y * c2;
+        gc[q][2] = gnext[q].z * c2;
+        gc[q][3] = gnext[q].w * c2;
 #pragma unroll
-          for (int v = 0; v < VEC; ++v) s[q][v] += ex2(fmaf(-c[v], c2, gc[q][v]));
-        }
+        for (int v = 0; v < VEC; ++v) s[q][v] = 0.f;
       }
-    };
-    // ---- the streamed k-sum of one row over its slots. Threads past the last column read (in-bounds)
-    //      smem garbage that the epilogue masks out, so the body has no per-column branches.
-    auto ksum = [&](const float (&gc)[CPT][VEC], float (&s)[CPT][VEC]) {
+      load_g(r + 1 < nrows ? i0 + r + 1 : i0);
       const long long tk0 = p.trace ? clock64() : 0;
       int k0 = 0;
       for (; k0 + KS <= n; k0 += KS) {
@@ -424,212 +424,60 @@ __global__ void __launch_bounds__(576, 1) k_iter_tma(TmaParams p) {
           for (int q2 = 0; q2 < KS; ++q2) {
 #pragma unroll
             for (int q = 0; q < CPT; ++q) {
-              float c[VEC];
-              VecF<VEC>::get(sb[q2 * mv + q * nct + ct], c);
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) s[q][v] += ex2(fmaf(-c[v], c2, gc[q][v]));
+              const float4 c = sb[q2 * mv + q * nkt + kt];
+              s[q][0] += ex2(fmaf(-c.x, c2, gc[q][0]));
+              s[q][1] += ex2(fmaf(-c.y, c2, gc[q][1]));
+              s[q][2] += ex2(fmaf(-c.z, c2, gc[q][2]));
+              s[q][3] += ex2(fmaf(-c.w, c2, gc[q][3]));
             }
           }
         }
         release();
       }
       if (k0 < n) {   // ragged last slot of the row (n % KS != 0)
+        const int kk = n - k0;
         mbar_wait(&full[slot], phase);
-        if (!(p.diag & COT_DIAG_NO_COMPUTE))
-          ksum_slot(reinterpret_cast<const VT*>(ring + (size_t)slot * slot_floats), n - k0, gc, s);
+        const VT* sb = reinterpret_cast<const VT*>(ring + (size_t)slot * slot_floats);
+        if (!(p.diag & COT_DIAG_NO_COMPUTE)) {
+          for (int q2 = 0; q2 < kk; ++q2) {
+#pragma unroll
+            for (int q = 0; q < CPT; ++q) {
+              const float4 c = sb[q2 * mv + q * nkt + kt];
+              s[q][0] += ex2(fmaf(-c.x, c2, gc[q][0]));
+              s[q][1] += ex2(fmaf(-c.y, c2, gc[q][1]));
+              s[q][2] += ex2(fmaf(-c.z, c2, gc[q][2]));
+              s[q][3] += ex2(fmaf(-c.w, c2, gc[q][3]));
+            }
+          }
+        }
         release();
       }
       if (p.trace) c_ksum += clock64() - tk0;
-    };
-    // ---- fp64 row epilogue of row r (global row i0 + r): p-update statistics and the column partial
-    auto epilogue = [&](int r, const float (&g)[CPT][VEC], const float (&s)[CPT][VEC]) {
-      const long long te0 = p.trace ? clock64() : 0;
-      double x[CPT][VEC];
-      double lmax = -INFINITY;
+      // ---- hand the row's k-sums to the epilogue warps through the queue
+      mbar_wait(&qempty[qs], qph ^ 1u);
+      VT* qrow = reinterpret_cast<VT*>(queue + (size_t)qs * m);
 #pragma unroll
       for (int q = 0; q < CPT; ++q) {
-        const bool ok = q * nct + ct < mv;
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          x[q][v] = ok ? z[q][v] - (double)g[q][v] * inv_eps : -INFINITY;
-          lmax = fmax(lmax, x[q][v]);
-        }
+        const int jv = q * nkt + kt;
+        if (jv < mv) qrow[jv] = make_float4(s[q][0], s[q][1], s[q][2], s[q][3]);
       }
-      double Mref = rowstat[r * 4 + 0];
-      double tt[CPT][VEC];
-      double Mtrue, rsum;
-      bool exact = !(Mref == Mref);            // no previous maximum: two-pass
-      if (!exact) {
-        double lsum = 0.0;
-#pragma unroll
-        for (int q = 0; q < CPT; ++q)
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            tt[q][v] = (x[q][v] == -INFINITY) ? 0.0 : (double)s[q][v] * exp_split(x[q][v] - Mref);
-            lsum += tt[q][v];
-          }
-        Mtrue = lmax;
-        rsum = lsum;
-        cblk_maxsum(Mtrue, rsum, red2, rbuf, nct);
-        exact = !(fabs(Mtrue - Mref) < 500.0);  // shifted sum out of the safe fp64 range: redo exactly
-      } else {
-        Mtrue = cblk_max1(lmax, red2, rbuf, nct);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qfull[qs]);
+      if (++qs == (uint32_t)QN) {
+        qs = 0;
+        qph ^= 1u;
       }
-      if (exact) {
-        Mref = Mtrue;
-        double lsum = 0.0;
-#pragma unroll
-        for (int q = 0; q < CPT; ++q)
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            tt[q][v] = (x[q][v] == -INFINITY) ? 0.0 : (double)s[q][v] * exp_split(x[q][v] - Mref);
-            lsum += tt[q][v];
-          }
-        rsum = cblk_sum1(lsum, red2, rbuf, nct);
-      }
-      // alpha_i / r_i with a fast reciprocal and two Newton steps (fp64 accuracy)
-      double rinv = (double)__frcp_rn((float)rsum);
-      rinv = rinv * fma(-rsum, rinv, 2.0);
-      rinv = rinv * fma(-rsum, rinv, 2.0);
-      const double rho = p.alpha[p.row_begin + i0 + r] * rinv;
-      if (ct == 0) {
-        rowstat[r * 4 + 0] = Mtrue;            // reference for the next iteration
-        rowstat[r * 4 + 1] = Mref;             // shift used for r_i
-        rowstat[r * 4 + 2] = rsum;
-      }
-#pragma unroll
-      for (int q = 0; q < CPT; ++q)
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) P[q][v] = fma(rho, tt[q][v], P[q][v]);
-      if (p.trace) c_epi += clock64() - te0;
-    };
-    // deferred rows: s and g parked in shared memory (each thread keeps its own columns)
-    VT* spend = reinterpret_cast<VT*>(defer);
-    VT* gpend = spend + (size_t)rpu * mv;
-    auto park = [&](int r, const float (&g)[CPT][VEC], const float (&s)[CPT][VEC]) {
-#pragma unroll
-      for (int q = 0; q < CPT; ++q) {
-        const int jv = q * nct + ct;
-        if (jv < mv) {
-          spend[(size_t)r * mv + jv] = VecF<VEC>::make(s[q]);
-          gpend[(size_t)r * mv + jv] = VecF<VEC>::make(g[q]);
-        }
-      }
-    };
-    auto unpark_epilogue = [&](int r) {
-      float g[CPT][VEC], s[CPT][VEC];
-#pragma unroll
-      for (int q = 0; q < CPT; ++q) {
-        const int jv = q * nct + ct;
-        if (jv < mv) {
-          VecF<VEC>::get(spend[(size_t)r * mv + jv], s[q]);
-          VecF<VEC>::get(gpend[(size_t)r * mv + jv], g[q]);
-        } else {
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) s[q][v] = g[q][v] = 0.f;
-        }
-      }
-      epilogue(r, g, s);
-    };
-    // CTA-uniform view of the sync warp's progress: returns the z generation; sets `halt`.
-    auto observe = [&](bool block, unsigned need, bool& halt) -> unsigned {
-      if (ct == 0) {
-        unsigned zg = lds_acquire(&ctl[4]);
-        unsigned h = lds_acquire(&ctl[5]);
-        while (block && zg < need && !h) {
-          __nanosleep(32);
-          zg = lds_acquire(&ctl[4]);
-          h = lds_acquire(&ctl[5]);
-        }
-        ctl[3] = h ? 0xffffffffu : zg;
-      }
-      cbar(nct);
-      const unsigned v = ctl[3];
-      cbar(nct);
-      halt = (v == 0xffffffffu);
-      return halt ? 0u : v;
-    };
-
-#pragma unroll
-    for (int q = 0; q < CPT; ++q)
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
-    if (active0) {
-      load_z();
-      load_g(i0);
+      ++produced;
+      if (kt == 0) *(volatile unsigned*)&ctl[6] = produced;
     }
-    // Iteration t needs the q-update of iteration t-1: z generation >= t. k-sums of iteration t stream
-    // as slots arrive; epilogues run as soon as that generation is visible (parked rows first).
-    bool z_ready = true, halt = false;
-    int t = 0, kr = 0, er = 0;
-    while (active0 && t < p.iters) {
-      if (kr < nrows) {
-        float g[CPT][VEC], gc[CPT][VEC], s[CPT][VEC];
-#pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-          VecF<VEC>::get(gnext[q], g[q]);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            gc[q][v] = g[q][v] * c2;
-            s[q][v] = 0.f;
-          }
-        }
-        load_g(kr + 1 < nrows ? i0 + kr + 1 : i0);
-        ksum(gc, s);
-        if (z_ready && er == kr) {
-          epilogue(kr, g, s);
-          ++er;
-        } else {
-          park(kr, g, s);
-        }
-        ++kr;
-      }
-      if (!z_ready) {
-        const long long ts0 = p.trace ? clock64() : 0;
-        const unsigned zg = observe(kr == nrows, (unsigned)t, halt);
-        if (p.trace) c_sync += clock64() - ts0;
-        if (halt) break;                      // frozen after iteration t-1: iteration t is discarded
-        if (zg >= (unsigned)t) {
-          load_z();
-          z_ready = true;
-        }
-      }
-      if (z_ready)
-        while (er < kr) {
-          unpark_epilogue(er);
-          ++er;
-        }
-      if (er == nrows) {                      // iteration t complete on this CTA: publish
-        cbar(nct);
-        for (int r = ct; r < nrows; r += nct)
-          p.w_hat[p.row_begin + i0 + r] = rowstat[r * 4 + 3] - rowstat[r * 4 + 1] - log(rowstat[r * 4 + 2]);
-#pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-          const int jv = q * nct + ct;
-          if (jv < mv) {
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) p.partials[(size_t)u * m + (size_t)VEC * jv + v] = P[q][v];
-          }
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
-        }
-        if (p.rows_only) break;
-        handoff_arrive(nct_h);                // to the sync warp (orders these writes before its B1)
-        ++t;
-        kr = 0;
-        er = 0;
-        z_ready = false;
-      }
+    if (p.trace && kt == 0) p.trace[blockIdx.x * 8 + 3] = c_ksum;
+    asm volatile("bar.sync 3, %0;" ::"r"(nkt) : "memory");
+    if (kt == 0) {
+      __threadfence_block();
+      *(volatile unsigned*)&ctl[7] = 1u;
+      *(volatile unsigned*)&ctl[2] = 1u;     // stop the producer
     }
-    if (p.trace && ct == 0) {
-      p.trace[blockIdx.x * 8 + 3] = c_ksum;
-      p.trace[blockIdx.x * 8 + 4] = c_epi;
-      p.trace[blockIdx.x * 8 + 5] = c_sync;
-      p.trace[blockIdx.x * 8 + 6] = clock64() - tc0;
-    }
-    // ---- drain: stop the producer and consume whatever it already issued
-    if (ct == 0) *(volatile unsigned*)&ctl[2] = 1u;
-    cbar(nct);
+    // ---- drain the TMA ring: consume whatever the producer already issued
     while (true) {
       const unsigned done = lds_volatile(&ctl[1]);
       __threadfence_block();
@@ -641,13 +489,196 @@ __global__ void __launch_bounds__(576, 1) k_iter_tma(TmaParams p) {
         if (consumed >= lds_volatile(&ctl[0])) break;
       }
     }
+  } else {
+    // ===================================================================== epilogue warps
+    // Per row (in order): wait for its k-sums in the queue and, at the first row of an iteration, for the
+    // previous q-update; then the fp64 epilogue: x_ij = z_hat_j - G_ij/eps, r_i = sum_j s_ij exp(x_ij - M'_i)
+    // and M_i = max_j x_ij in ONE block reduction against the previous row maximum M'_i (exact exponent
+    // split), w_hat_i = log alpha_i - M'_i - log r_i (lazily, once per iteration), P_j += (alpha_i/r_i) t_ij.
+    const int et = threadIdx.x - nkt;
+    const int ewarp = warp - nk;
+    uint32_t qs = 0, qph = 0;
+    unsigned consumed = 0;
+    int rbuf = 0;
+    long long c_epi = 0, c_wait = 0;
+    for (int r = et; r < nrows; r += net) {
+      const double a = p.alpha[p.row_begin + i0 + r];
+      rowstat[r * 4 + 0] = __longlong_as_double(0x7ff8000000000000LL);   // no previous maximum yet
+      rowstat[r * 4 + 3] = log(a);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+    double z[EPT][VEC], P[EPT][VEC];
+    auto load_z = [&]() {
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) {
+        const int jv = q * net + et;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) z[q][v] = jv < mv ? __ldcg(p.z_hat + VEC * jv + v) : 0.0;
+      }
+    };
+#pragma unroll
+    for (int q = 0; q < EPT; ++q)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
+    bool halted = false;
+    if (active0) load_z();
+    for (int t = 0; active0 && t < p.iters && !halted; ++t) {
+      if (t > 0) {   // z generation >= t: the q-update of iteration t-1 is visible
+        const long long tw0 = p.trace ? clock64() : 0;
+        if (et == 0) {
+          unsigned zg = lds_acquire(&ctl[4]), h = lds_acquire(&ctl[5]);
+          while (zg < (unsigned)t && !h) {
+            __nanosleep(32);
+            zg = lds_acquire(&ctl[4]);
+            h = lds_acquire(&ctl[5]);
+          }
+          ctl[9] = h ? 1u : 0u;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+        halted = ctl[9] != 0;
+        asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+        if (p.trace) c_wait += clock64() - tw0;
+        if (halted) break;
+        load_z();
+      }
+      for (int r = 0; r < nrows; ++r) {
+        // G row (read-only) first, so its latency overlaps the queue wait
+        float g[EPT][VEC];
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+          const int jv = q * net + et;
+          const float4 gv = jv < mv ? __ldg(reinterpret_cast<const VT*>(p.G + (size_t)(i0 + r) * m) + jv)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+          g[q][0] = gv.x;
+          g[q][1] = gv.y;
+          g[q][2] = gv.z;
+          g[q][3] = gv.w;
+        }
+        mbar_wait(&qfull[qs], qph);
+        const long long te0 = p.trace ? clock64() : 0;
+        float s[EPT][VEC];
+        const VT* qrow = reinterpret_cast<const VT*>(queue + (size_t)qs * m);
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+          const int jv = q * net + et;
+          const float4 sv = jv < mv ? qrow[jv] : make_float4(0.f, 0.f, 0.f, 0.f);
+          s[q][0] = sv.x;
+          s[q][1] = sv.y;
+          s[q][2] = sv.z;
+          s[q][3] = sv.w;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&qempty[qs]);
+        ++consumed;
+        if (++qs == (uint32_t)QN) {
+          qs = 0;
+          qph ^= 1u;
+        }
+        // ---- the row epilogue
+        double x[EPT][VEC];
+        double lmax = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+          const bool ok = q * net + et < mv;
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            x[q][v] = ok ? z[q][v] - (double)g[q][v] * inv_eps : -INFINITY;
+            lmax = fmax(lmax, x[q][v]);
+          }
+        }
+        double Mref = rowstat[r * 4 + 0];
+        double tt[EPT][VEC];
+        double Mtrue, rsum;
+        bool exact = !(Mref == Mref);          // no previous maximum: two-pass
+        if (!exact) {
+          double lsum = 0.0;
+#pragma unroll
+          for (int q = 0; q < EPT; ++q)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              tt[q][v] = (x[q][v] == -INFINITY) ? 0.0 : (double)s[q][v] * exp_split(x[q][v] - Mref);
+              lsum += tt[q][v];
+            }
+          Mtrue = lmax;
+          rsum = lsum;
+          cblk_maxsum(Mtrue, rsum, red2, rbuf, net, nk);
+          exact = !(fabs(Mtrue - Mref) < 500.0);   // shifted sum out of the safe fp64 range: redo exactly
+        } else {
+          Mtrue = cblk_max1(lmax, red2, rbuf, net, nk);
+        }
+        if (exact) {
+          Mref = Mtrue;
+          double lsum = 0.0;
+#pragma unroll
+          for (int q = 0; q < EPT; ++q)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              tt[q][v] = (x[q][v] == -INFINITY) ? 0.0 : (double)s[q][v] * exp_split(x[q][v] - Mref);
+              lsum += tt[q][v];
+            }
+          rsum = cblk_sum1(lsum, red2, rbuf, net, nk);
+        }
+        double rinv = (double)__frcp_rn((float)rsum);   // alpha_i / r_i: fast reciprocal + 2 Newton steps
+        rinv = rinv * fma(-rsum, rinv, 2.0);
+        rinv = rinv * fma(-rsum, rinv, 2.0);
+        const double rho = p.alpha[p.row_begin + i0 + r] * rinv;
+        if (et == 0) {
+          rowstat[r * 4 + 0] = Mtrue;           // reference for the next iteration
+          rowstat[r * 4 + 1] = Mref;            // shift used for r_i
+          rowstat[r * 4 + 2] = rsum;
+        }
+#pragma unroll
+        for (int q = 0; q < EPT; ++q)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) P[q][v] = fma(rho, tt[q][v], P[q][v]);
+        if (p.trace) c_epi += clock64() - te0;
+      }
+      // ---- publish iteration t: w_hat of this CTA's rows (parallel logs) and the column partial
+      asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+      for (int r = et; r < nrows; r += net)
+        p.w_hat[p.row_begin + i0 + r] = rowstat[r * 4 + 3] - rowstat[r * 4 + 1] - log(rowstat[r * 4 + 2]);
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) {
+        const int jv = q * net + et;
+        if (jv < mv)
+          reinterpret_cast<double4*>(p.partials + (size_t)u * m)[jv] =
+              make_double4(P[q][0], P[q][1], P[q][2], P[q][3]);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
+      }
+      if (p.rows_only) break;
+      handoff_arrive(net + 32);               // to the sync warp (orders these writes before its B1)
+    }
+    if (p.trace && et == 0) {
+      p.trace[blockIdx.x * 8 + 4] = c_epi;
+      p.trace[blockIdx.x * 8 + 5] = c_wait;
+    }
+    // ---- drain the queue after a halt: consume every row the k-sum warps still produce
+    (void)ewarp;
+    while (true) {
+      const unsigned done = lds_volatile(&ctl[7]);
+      __threadfence_block();
+      const unsigned prod = lds_volatile(&ctl[6]);
+      if (consumed < prod) {
+        mbar_wait(&qfull[qs], qph);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&qempty[qs]);
+        ++consumed;
+        if (++qs == (uint32_t)QN) {
+          qs = 0;
+          qph ^= 1u;
+        }
+      } else if (done) {
+        if (consumed >= lds_volatile(&ctl[6])) break;
+      }
+    }
   }
   __syncthreads();
 }
 
 // ------------------------------------------------------------------------------------------ launcher
 bool tma_eligible(const IterArgs& a) {
-  return a.dtype == COT_F32 && a.B == 1 && a.m % 4 == 0 && a.m <= 4096 && !(a.flags & COT_FORCE_LDG);
+  return a.dtype == COT_F32 && a.B == 1 && a.m % 4 == 0 && a.m <= 1024 && !(a.flags & COT_FORCE_LDG);
 }
 
 cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, bool rows_only, int parity,
@@ -668,20 +699,34 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
   const UnitPlan up = unit_plan(1, a.R, sms);
   p.rpu = (int)up.rpu;
   p.U = (int)up.U;
-  const int row_bytes = (int)a.m * 4;
+  // ---- warp roles: k-sum warps (4 columns x CPT per thread, <= 8 warps), epilogue warps (4 x EPT)
+  const int m = (int)a.m, mv = m / 4;
+  int cpt = 1;
+  while ((mv + 32 * cpt - 1) / (32 * cpt) > 8) cpt *= 2;
+  p.nk = (mv + 32 * cpt - 1) / (32 * cpt);
+  p.ne = std::max(std::max(1, p.nk / 2), (mv + 63) / 64);   // <= 2 float4 per epilogue thread
+  if (const char* ev = getenv("COT_NE")) p.ne = std::max(1, std::min(8, atoi(ev)));   // tuning experiments
+  int ept = 1;
+  while ((mv + 32 * p.ne - 1) / (32 * p.ne) > ept) ept *= 2;
+  if (cpt > 1 || ept > 2) return cudaErrorInvalidValue;
+  // ---- TMA ring and row queue
+  const int row_bytes = m * 4;
   int KS = 1;
-  int ks_bytes = 32768;
+  int ks_bytes = 65536;
   if (const char* ev = getenv("COT_SLOT_BYTES")) ks_bytes = atoi(ev);   // tuning experiments
   while (KS * 2 <= 16 && KS * 2 * row_bytes <= ks_bytes && KS * 2 <= (int)a.n) KS *= 2;
   p.KS = KS;
   const size_t slot_bytes = (size_t)p.KS * row_bytes;
-  const size_t defer_bytes = (size_t)2 * p.rpu * a.m * 4 + (size_t)p.rpu * 4 * 8;
-  const size_t budget = 210 * 1024;
-  if (defer_bytes + 2 * slot_bytes + 4096 > budget) return cudaErrorInvalidConfiguration;
-  p.nslot = (int)std::max<size_t>(2, std::min<size_t>(64, (budget - defer_bytes - 4096) / slot_bytes));
-  // ring + 1 KiB pad (branch-free over-reads past the last column stay in-bounds) + deferred rows +
-  // row statistics + barriers + control + reduction scratch
-  const size_t smem = (size_t)p.nslot * slot_bytes + 1024 + defer_bytes + (size_t)p.nslot * 16 + 32 + 128 * 8 + 64;
+  p.qn = std::max(1, std::min(p.rpu, 8));
+  if (const char* ev = getenv("COT_QN")) p.qn = std::max(1, atoi(ev));
+  const size_t queue_bytes = (size_t)p.qn * row_bytes + (size_t)p.rpu * 4 * 8;
+  const size_t budget = 220 * 1024;
+  if (queue_bytes + 2 * slot_bytes + 4096 > budget) return cudaErrorInvalidConfiguration;
+  p.nslot = (int)std::max<size_t>(2, std::min<size_t>(64, (budget - queue_bytes - 4096) / slot_bytes));
+  // ring + 1 KiB pad (branch-free over-reads past the last column stay in-bounds) + row queue + row
+  // statistics + barriers + control + reduction scratch
+  const size_t smem = (size_t)p.nslot * slot_bytes + 1024 + queue_bytes + ((size_t)p.nslot + p.qn) * 16 + 64 +
+                      128 * 8 + 64;
   p.iters = rows_only ? 1 : iters;
   p.rows_only = rows_only ? 1 : 0;
   p.tol = a.tol;
@@ -697,26 +742,18 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
   static unsigned long long* trace_buf = nullptr;   // diagnostics only (COT_TRACE=1)
   if (getenv("COT_TRACE")) {
     if (!trace_buf) cudaMalloc(&trace_buf, 4096 * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace_buf, 0, 4096 * 8 * sizeof(unsigned long long), s);
     p.trace = trace_buf;
   }
-  // columns per thread: VEC (2 or 4) x CPT; up to 16 consumer warps
-  const int m = (int)a.m;
-  int VEC = 2, cpt = 1;
-  if (m >= 512) VEC = 4;
-  if (const char* ev = getenv("COT_VEC")) VEC = std::max(VEC, atoi(ev));   // tuning experiments
-  int ncw = (m / VEC + 31) / 32;
-  while (ncw > 16) {
-    cpt *= 2;
-    ncw = (m / VEC / cpt + 31) / 32;
-  }
-  const int threads = (ncw + 2) * 32;
+  const int threads = (p.nk + p.ne + 2) * 32;
   cudaError_t e;
   void* fn = nullptr;
-#define COT_PICK(V_, C_, K_) \
-  if (VEC == V_ && cpt == C_ && KS == K_) fn = (void*)k_iter_tma<V_, C_, K_>;
-  COT_PICK(2, 1, 1) COT_PICK(2, 1, 2) COT_PICK(2, 1, 4) COT_PICK(2, 1, 8) COT_PICK(2, 1, 16)
-  COT_PICK(4, 1, 1) COT_PICK(4, 1, 2) COT_PICK(4, 1, 4) COT_PICK(4, 1, 8) COT_PICK(4, 1, 16)
-  COT_PICK(4, 2, 1) COT_PICK(4, 2, 2) COT_PICK(4, 2, 4) COT_PICK(4, 2, 8) COT_PICK(4, 2, 16)
+#define COT_PICK(C_, E_, K_) \
+  if (cpt == C_ && ept == E_ && KS == K_) fn = (void*)k_iter_tma<C_, E_, K_>;
+#define COT_PICK_K(C_, E_) \
+  COT_PICK(C_, E_, 1) COT_PICK(C_, E_, 2) COT_PICK(C_, E_, 4) COT_PICK(C_, E_, 8) COT_PICK(C_, E_, 16)
+  COT_PICK_K(1, 1) COT_PICK_K(1, 2)
+#undef COT_PICK_K
 #undef COT_PICK
   if (!fn) return cudaErrorInvalidValue;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -743,9 +780,9 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
     const double it = iters > 0 ? iters : 1;
     fprintf(stderr,
             "[cot trace] iters=%d per-iter cycles (mean/max over CTAs): prod_wait %.0f/%.0f prod_total %.0f/%.0f "
-            "cons_ksum %.0f/%.0f cons_epi %.0f/%.0f cons_sync %.0f/%.0f cons_total %.0f/%.0f\n",
+            "ksum %.0f/%.0f epi_busy %.0f/%.0f epi_wait_z %.0f/%.0f\n",
             iters, acc[0] / it, mx[0] / it, acc[1] / it, mx[1] / it, acc[3] / it, mx[3] / it, acc[4] / it,
-            mx[4] / it, acc[5] / it, mx[5] / it, acc[6] / it, mx[6] / it);
+            mx[4] / it, acc[5] / it, mx[5] / it);
   }
   return e;
 }

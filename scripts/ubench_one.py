@@ -1,0 +1,14 @@
+"""One persistent C4 launch (ITERS iterations, FLAGS) for ncu capture."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2311_13147_b200 as cot
+import synthetic
+p = synthetic.c4_large()
+dev = torch.device("cuda:0")
+prob = cot.CerotProblem(torch.as_tensor(p.C, device=dev), torch.as_tensor(p.alpha, device=dev),
+                        torch.as_tensor(p.beta, device=dev), p.eps)
+for _ in range(2):
+    prob.init().iterate(int(os.environ.get("ITERS", "30")), flags=int(os.environ.get("FLAGS", "0")))
+torch.cuda.synchronize()
+print("ok")
