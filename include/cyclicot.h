@@ -165,6 +165,50 @@ int cerot_solve(const double* alpha, const double* beta, const void* C,
                 double* w_hat, double* z_hat, void* T_blocks,
                 void* workspace, size_t ws_bytes, cot_report* report, void* stream);
 
+/* ---------------------------------------------------------------------------------------------- */
+/* Row sharding across GPUs (B == 1). GPU g holds rows [row_begin, row_begin + R) of every */
+/* block: C_local [n][R][m], G_local [R][m] (clot_aggregate of C_local with m columns and R rows, i.e.    */
+/* call it with the shard viewed as [n][R][m] -- see paper_2311_13147_b200.dist), while alpha, beta,     */
+/* w_hat, z_hat stay full length [m] (w_hat is written only on the held rows; z_hat is replicated).       */
+/* The p-update of the held rows is local; the plan column sums are summed across GPUs with ONE           */
+/* m-length fp64 ncclAllReduce per iteration; every GPU then applies the identical q-update. NCCL is     */
+/* loaded at run time (libnccl.so.2, the copy torch uses); `comm` == NULL means a single GPU.            */
+size_t cot_workspace_bytes_sharded(int64_t n, int64_t m, int64_t R, int dtype);
+/* G, argmin of the held rows: C_local [n][R][m] -> G_local, argmin_local [R][m] (as clot_aggregate). */
+int clot_aggregate_shard(const void* C_local, int64_t n, int64_t R, int64_t m, int dtype, void* G_local,
+                         int32_t* argmin_local, int32_t* d_nonfinite, void* stream);
+/* The held rows of the dense d x d plan: T_rows [n][R][d], row (r, i) = full-plan row r*m + row_begin + i  */
+/* (as clot_expand; S_local = argmin_local ? S [R][m] : T_local [n][R][m]).                              */
+int clot_expand_shard(const void* S_local, const int32_t* argmin_local, int64_t n, int64_t R, int64_t m, int dtype,
+                      void* T_rows, void* stream);
+/* Writes a new 128-byte ncclUniqueId to id128 (HOST memory; broadcast it to every rank). */
+int cot_nccl_unique_id(void* id128);
+/* Creates the communicator of `rank` among `nranks` (ncclCommInitRank; current CUDA device). Owned by    */
+/* the caller; release with cot_comm_destroy.                                                            */
+int cot_comm_init(const void* id128, int nranks, int rank, void** comm);
+int cot_comm_destroy(void* comm);
+/* Row pass of one iteration on the held rows + their column sums c_local[m] (DEVICE, fp64; not yet      */
+/* reduced across GPUs).                                                                                  */
+int cerot_rows_shard(const double* alpha, const void* C_local, const void* G_local, int64_t n, int64_t m,
+                     int64_t row_begin, int64_t R, int dtype, const double* eps, uint32_t flags,
+                     const double* z_hat, double* w_hat, double* c_local, void* workspace, size_t ws_bytes,
+                     void* stream);
+/* q-update from the fully reduced column sums c[m] (DEVICE): z_hat_j += log beta_j - log c_j, monitor,    */
+/* iteration count and freeze rule in the workspace state.                                               */
+int cerot_zupdate(const double* beta, const double* c, int64_t n, int64_t m, double tol, int64_t check_every,
+                  double* z_hat, void* workspace, size_t ws_bytes, void* stream);
+/* `iters` iterations: cerot_rows_shard -> ncclAllReduce(c) (if comm) -> cerot_zupdate, all on `stream`.  */
+int cerot_iter_sharded(const double* alpha, const double* beta, const void* C_local, const void* G_local,
+                       int64_t n, int64_t m, int64_t row_begin, int64_t R, int dtype, const double* eps,
+                       int64_t iters, double tol, int64_t check_every, uint32_t flags, double* w_hat,
+                       double* z_hat, void* workspace, size_t ws_bytes, void* comm, void* stream);
+/* Plan of the held rows (T_local [n][R][m] if non-NULL) + report reduced across GPUs (identical on every */
+/* GPU; d_report DEVICE [8] doubles, cot_report field order).                                            */
+int cerot_plan_sharded(const double* alpha, const double* beta, const void* C_local, const void* G_local,
+                       int64_t n, int64_t m, int64_t row_begin, int64_t R, int dtype, const double* eps,
+                       const double* w_hat, const double* z_hat, void* T_local, double* d_report,
+                       void* workspace, size_t ws_bytes, void* comm, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

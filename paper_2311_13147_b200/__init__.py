@@ -58,6 +58,20 @@ _SIGS = {
                                   _sz, _vp]),
     "cerot_solve": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _dbl, _i64, _i64, _u32, _vp,
                                    _vp, _vp, _vp, _sz, ctypes.POINTER(cot_report), _vp]),
+    # row sharding (dist.py)
+    "cot_workspace_bytes_sharded": (_sz, [_i64, _i64, _i64, ctypes.c_int]),
+    "clot_aggregate_shard": (ctypes.c_int, [_vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "clot_expand_shard": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp]),
+    "cot_nccl_unique_id": (ctypes.c_int, [_vp]),
+    "cot_comm_init": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "cot_comm_destroy": (ctypes.c_int, [_vp]),
+    "cerot_rows_shard": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _u32, _vp, _vp, _vp,
+                                        _vp, _sz, _vp]),
+    "cerot_zupdate": (ctypes.c_int, [_vp, _vp, _i64, _i64, _dbl, _i64, _vp, _vp, _sz, _vp]),
+    "cerot_iter_sharded": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl,
+                                          _i64, _u32, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "cerot_plan_sharded": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp,
+                                          _vp, _vp, _vp, _sz, _vp, _vp]),
 }
 
 

@@ -6,11 +6,25 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcyclicot.so")
-SOURCES = ["abi.cu", "k_aggregate.cu", "k_expand.cu", "k_iter.cu", "k_iter_tma.cu", "k_plan.cu"]
+SOURCES = ["abi.cu", "k_aggregate.cu", "k_expand.cu", "k_iter.cu", "k_iter_tma.cu", "k_plan.cu", "k_shard.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
+
+
+def _nccl_include() -> str:
+    """Header of the NCCL torch loads (pip nvidia-nccl 2.28.x), not /usr/include's older copy. Only types and
+    prototypes are used: the library dlopen()s libnccl.so.2 at run time."""
+    try:
+        import nvidia.nccl
+        for base in nvidia.nccl.__path__:
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    return "/usr/include"
 
 
 def _stale() -> bool:
@@ -26,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *srcs]
+    cmd = [NVCC, *FLAGS, "-I", _nccl_include(), "-o", LIB + ".tmp", *srcs, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

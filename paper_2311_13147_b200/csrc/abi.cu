@@ -1,11 +1,15 @@
-// C ABI of libcyclicot (include/cyclicot.h): argument validation, workspace carving, launch sequencing.
-// No compute happens here: every step of the path is one of the kernels in k_*.cu.
+// C ABI of libcyclicot (include/cyclicot.h): argument validation, workspace carving, launch sequencing and
+// the NCCL communicator of the row-sharded path. No compute happens here: every step of the path is one of
+// the kernels in k_*.cu (or an NCCL collective between them).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <stdint.h>
 #include <string.h>
 
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -39,9 +43,10 @@ UnitPlan unit_plan(int64_t B, int64_t R, int sm_count) {
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int dtype, int sm_count, Workspace* ws) {
+size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, int dtype, int sm_count,
+                       Workspace* ws) {
   (void)n;
-  const UnitPlan up = unit_plan(B, m, sm_count);
+  const UnitPlan up = unit_plan(B, R, sm_count);
   const size_t esz = dtype == COT_F32 ? 4 : 8;
   const int64_t ntiles = (m + 31) / 32;
   size_t off = 0;
@@ -51,21 +56,58 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int dtype, i
     return base ? static_cast<char*>(base) + o : nullptr;
   };
   // Order matters: the per-problem state comes first so its offset depends on B only (cerot_init and
-  // cerot_state find it without knowing n or the dtype); the dtype-sized G comes last.
+  // cerot_state find it without knowing n, R or the dtype); the dtype-sized G comes last.
   Workspace w{};
   w.state = reinterpret_cast<SolverState*>(take((size_t)B * sizeof(SolverState)));
   w.counters = reinterpret_cast<unsigned*>(take((size_t)B * 4));
   w.grid_bar = reinterpret_cast<unsigned*>(take(16));
   w.nonfinite = reinterpret_cast<int32_t*>(take(4));
   w.report = reinterpret_cast<double*>(take((size_t)B * kReportDoubles * 8));
-  w.resid_part = reinterpret_cast<double*>(take((size_t)(B * ntiles) * 8));
+  w.resid_part = reinterpret_cast<double*>(take((size_t)std::max<int64_t>(B * ntiles, sm_count) * 8));
   w.plan_scal = reinterpret_cast<double*>(take((size_t)up.U * kPlanScalars * 8));
   w.partials[0] = reinterpret_cast<double*>(take((size_t)(up.U * m) * 8));
   w.partials[1] = reinterpret_cast<double*>(take((size_t)(up.U * m) * 8));
-  w.A = reinterpret_cast<int32_t*>(take((size_t)(B * m * m) * 4));
-  w.G = take((size_t)(B * m * m) * esz);
+  w.c_local = reinterpret_cast<double*>(take((size_t)(B * m) * 8));
+  w.c_global = reinterpret_cast<double*>(take((size_t)(B * m) * 8));
+  w.plan_buf = reinterpret_cast<double*>(take((size_t)(B * (kPlanBufHead + m)) * 8));
+  w.A = reinterpret_cast<int32_t*>(take((size_t)(B * R * m) * 4));
+  w.G = take((size_t)(B * R * m) * esz);
   if (ws) *ws = w;
   return off;
+}
+
+// ------------------------------------------------------------------------------------------- NCCL
+// NCCL is loaded at run time (the copy torch already loaded when present): the library itself loads and
+// runs on one GPU without it; only the communicator functions need it.
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* e = dlerror();
+      api.err = std::string("cannot load libnccl.so.2: ") + (e ? e : "unknown error");
+      return;
+    }
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString;
+    if (!api.ok) api.err = "libnccl.so.2 lacks a required symbol";
+  });
+  return api;
 }
 
 }  // namespace cot
@@ -78,6 +120,15 @@ using namespace cot;
     if (_e != cudaSuccess) {                                                      \
       set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));              \
       return COT_E_CUDA;                                                          \
+    }                                                                             \
+  } while (0)
+
+#define COT_CHECK_NCCL(expr)                                                      \
+  do {                                                                            \
+    ncclResult_t _r = (expr);                                                     \
+    if (_r != ncclSuccess) {                                                      \
+      set_error(std::string(#expr) + ": " + nccl().GetErrorString(_r));          \
+      return COT_E_NCCL;                                                          \
     }                                                                             \
   } while (0)
 
@@ -94,8 +145,9 @@ static int check_shape(int64_t B, int64_t n, int64_t m, int dtype) {
   return COT_OK;
 }
 
-static int check_ws(void* workspace, size_t ws_bytes, int64_t B, int64_t n, int64_t m, int dtype, Workspace* ws) {
-  const size_t need = carve_workspace(nullptr, B, n, m, dtype, device_sm_count(), nullptr);
+static int check_ws(void* workspace, size_t ws_bytes, int64_t B, int64_t n, int64_t m, int64_t R, int dtype,
+                    Workspace* ws) {
+  const size_t need = carve_workspace(nullptr, B, n, m, R, dtype, device_sm_count(), nullptr);
   if (!workspace || ws_bytes < need) {
     set_error("workspace too small: need " + std::to_string(need) + " bytes, got " + std::to_string(ws_bytes));
     return COT_E_WORKSPACE;
@@ -104,7 +156,50 @@ static int check_ws(void* workspace, size_t ws_bytes, int64_t B, int64_t n, int6
     set_error("workspace must be 256-byte aligned");
     return COT_E_WORKSPACE;
   }
-  carve_workspace(workspace, B, n, m, dtype, device_sm_count(), ws);
+  carve_workspace(workspace, B, n, m, R, dtype, device_sm_count(), ws);
+  return COT_OK;
+}
+
+static IterArgs make_args(const double* alpha, const double* beta, const void* C, const void* G, int64_t B, int64_t n,
+                          int64_t m, int dtype, const double* eps, double tol, int64_t check_every, uint32_t flags,
+                          double* w_hat, double* z_hat, int64_t row_begin = 0, int64_t R = -1) {
+  IterArgs a;
+  a.alpha = alpha;
+  a.beta = beta;
+  a.C = C;
+  a.G = G;
+  a.eps = eps;
+  a.w_hat = w_hat;
+  a.z_hat = z_hat;
+  a.B = B;
+  a.n = n;
+  a.m = m;
+  a.R = R < 0 ? m : R;
+  a.row_begin = row_begin;
+  a.dtype = dtype;
+  a.tol = tol;
+  a.check_every = check_every > 0 ? check_every : 1;
+  a.flags = flags;
+  return a;
+}
+
+// One iteration of the row pass into ws.partials[parity] on the held rows (TMA rows-only or LDG).
+static cudaError_t rows_pass(const IterArgs& a, const Workspace& ws, int parity, cudaStream_t s) {
+  if (tma_eligible(a)) return launch_iter_tma(a, ws, 1, true, parity & 1, s);
+  return launch_rows(a, ws, unit_plan(a.B, a.R, device_sm_count()), parity & 1, s);
+}
+
+// Plan pass + local reductions (+ allreduce over comm when given) + report.
+static int plan_and_report(const IterArgs& a, const Workspace& ws, void* T_blocks, double* d_report, void* comm,
+                           cudaStream_t s) {
+  const UnitPlan up = unit_plan(a.B, a.R, device_sm_count());
+  COT_CHECK_CUDA(launch_plan(a, ws, up, T_blocks, s));
+  COT_CHECK_CUDA(launch_plan_reduce_local(a, ws, up, ws.plan_buf, s));
+  if (comm) {
+    COT_CHECK_NCCL(nccl().AllReduce(ws.plan_buf, ws.plan_buf, (size_t)(a.B * (kPlanBufHead + a.m)), ncclFloat64,
+                                    ncclSum, (ncclComm_t)comm, s));
+  }
+  COT_CHECK_CUDA(launch_plan_finalize_buf(a, ws, ws.plan_buf, d_report ? d_report : ws.report, s));
   return COT_OK;
 }
 
@@ -116,7 +211,12 @@ const char* cot_last_error(void) { return g_last_error.c_str(); }
 
 size_t cot_workspace_bytes(int64_t B, int64_t n, int64_t m, int dtype) {
   if (B < 1 || n < 1 || m < 1) return 0;
-  return carve_workspace(nullptr, B, n, m, dtype, device_sm_count(), nullptr);
+  return carve_workspace(nullptr, B, n, m, m, dtype, device_sm_count(), nullptr);
+}
+
+size_t cot_workspace_bytes_sharded(int64_t n, int64_t m, int64_t R, int dtype) {
+  if (n < 1 || m < 1 || R < 1 || R > m) return 0;
+  return carve_workspace(nullptr, 1, n, m, R, dtype, device_sm_count(), nullptr);
 }
 
 int clot_aggregate(const void* C, int64_t B, int64_t n, int64_t m, int dtype, void* G, int32_t* argmin,
@@ -153,39 +253,16 @@ int cerot_init(const double* alpha, const double* beta, int64_t B, int64_t m, ui
                void* workspace, size_t ws_bytes, void* stream) {
   if (B < 1 || m < 1) return arg_error("B, m must be >= 1");
   if (!alpha || !beta || !z_hat) return arg_error("cerot_init: alpha, beta, z_hat must be non-NULL");
-  // the state block is at the start of the workspace for every (n, dtype) (see carve_workspace)
+  // the state block is at the start of the workspace for every (n, R, dtype) (see carve_workspace)
   Workspace ws;
   const size_t need = (size_t)B * (sizeof(SolverState) + 4) + 2048;
   if (!workspace || ws_bytes < need) {
     set_error("workspace too small");
     return COT_E_WORKSPACE;
   }
-  carve_workspace(workspace, B, 1, m, COT_F32, device_sm_count(), &ws);
+  carve_workspace(workspace, B, 1, m, m, COT_F32, device_sm_count(), &ws);
   COT_CHECK_CUDA(launch_init(alpha, beta, B, m, flags, z_hat, ws, (cudaStream_t)stream));
   return COT_OK;
-}
-
-static IterArgs make_args(const double* alpha, const double* beta, const void* C, const void* G, int64_t B, int64_t n,
-                          int64_t m, int dtype, const double* eps, double tol, int64_t check_every, uint32_t flags,
-                          double* w_hat, double* z_hat) {
-  IterArgs a;
-  a.alpha = alpha;
-  a.beta = beta;
-  a.C = C;
-  a.G = G;
-  a.eps = eps;
-  a.w_hat = w_hat;
-  a.z_hat = z_hat;
-  a.B = B;
-  a.n = n;
-  a.m = m;
-  a.R = m;
-  a.row_begin = 0;
-  a.dtype = dtype;
-  a.tol = tol;
-  a.check_every = check_every > 0 ? check_every : 1;
-  a.flags = flags;
-  return a;
 }
 
 int cerot_iter(const double* alpha, const double* beta, const void* C, const void* G, int64_t B, int64_t n, int64_t m,
@@ -195,9 +272,8 @@ int cerot_iter(const double* alpha, const double* beta, const void* C, const voi
   if (st) return st;
   if (!alpha || !beta || !C || !G || !eps || !w_hat || !z_hat) return arg_error("cerot_iter: NULL argument");
   if (iters < 0 || tol < 0 || !(tol == tol)) return arg_error("cerot_iter: iters >= 0 and tol >= 0 required");
-  // the state lives in the same place for every (n, dtype): carve with the caller's shape
   Workspace ws;
-  st = check_ws(workspace, ws_bytes, B, n, m, dtype, &ws);
+  st = check_ws(workspace, ws_bytes, B, n, m, m, dtype, &ws);
   if (st) return st;
   const IterArgs a = make_args(alpha, beta, C, G, B, n, m, dtype, eps, tol, check_every, flags, w_hat, z_hat);
   const UnitPlan up = unit_plan(B, m, device_sm_count());
@@ -220,15 +296,11 @@ int cerot_rows(const double* alpha, const void* C, const void* G, int64_t B, int
   if (st) return st;
   if (!alpha || !C || !G || !eps || !w_hat || !z_hat) return arg_error("cerot_rows: NULL argument");
   Workspace ws;
-  st = check_ws(workspace, ws_bytes, B, n, m, dtype, &ws);
+  st = check_ws(workspace, ws_bytes, B, n, m, m, dtype, &ws);
   if (st) return st;
   const IterArgs a = make_args(alpha, nullptr, C, G, B, n, m, dtype, eps, 0.0, 1, flags, w_hat,
                                const_cast<double*>(z_hat));
-  if (tma_eligible(a)) {
-    COT_CHECK_CUDA(launch_iter_tma(a, ws, 1, true, parity & 1, (cudaStream_t)stream));
-    return COT_OK;
-  }
-  COT_CHECK_CUDA(launch_rows(a, ws, unit_plan(B, m, device_sm_count()), parity & 1, (cudaStream_t)stream));
+  COT_CHECK_CUDA(rows_pass(a, ws, parity, (cudaStream_t)stream));
   return COT_OK;
 }
 
@@ -239,7 +311,7 @@ int cerot_cols(const double* beta, int64_t B, int64_t n, int64_t m, int dtype, d
   if (!beta || !z_hat) return arg_error("cerot_cols: NULL argument");
   if (tol < 0) return arg_error("cerot_cols: tol >= 0 required");
   Workspace ws;
-  st = check_ws(workspace, ws_bytes, B, n, m, dtype, &ws);
+  st = check_ws(workspace, ws_bytes, B, n, m, m, dtype, &ws);
   if (st) return st;
   const IterArgs a = make_args(nullptr, beta, nullptr, nullptr, B, n, m, dtype, nullptr, tol, check_every, 0, nullptr,
                                z_hat);
@@ -251,7 +323,7 @@ int cerot_state(const void* workspace, int64_t B, int64_t m, int64_t n, int dtyp
                 int32_t* converged, double* residual, void* stream) {
   if (B < 1 || m < 1 || !workspace) return arg_error("cerot_state: bad arguments");
   Workspace ws;
-  carve_workspace(const_cast<void*>(workspace), B, n, m, dtype, device_sm_count(), &ws);
+  carve_workspace(const_cast<void*>(workspace), B, n, m, m, dtype, device_sm_count(), &ws);
   std::vector<SolverState> h((size_t)B);
   COT_CHECK_CUDA(cudaMemcpyAsync(h.data(), ws.state, (size_t)B * sizeof(SolverState), cudaMemcpyDeviceToHost,
                                  (cudaStream_t)stream));
@@ -281,13 +353,11 @@ int cerot_plan(const double* alpha, const double* beta, const void* C, const voi
   if (st) return st;
   if (!alpha || !beta || !C || !G || !eps || !w_hat || !z_hat) return arg_error("cerot_plan: NULL argument");
   Workspace ws;
-  st = check_ws(workspace, ws_bytes, B, n, m, dtype, &ws);
+  st = check_ws(workspace, ws_bytes, B, n, m, m, dtype, &ws);
   if (st) return st;
   IterArgs a = make_args(alpha, beta, C, G, B, n, m, dtype, eps, 0.0, 1, 0, const_cast<double*>(w_hat),
                          const_cast<double*>(z_hat));
-  const UnitPlan up = unit_plan(B, m, device_sm_count());
-  COT_CHECK_CUDA(launch_plan(a, ws, up, T_blocks, d_report, (cudaStream_t)stream));
-  return COT_OK;
+  return plan_and_report(a, ws, T_blocks, d_report, nullptr, (cudaStream_t)stream);
 }
 
 int cerot_solve(const double* alpha, const double* beta, const void* C, int64_t B, int64_t n, int64_t m, int dtype,
@@ -298,7 +368,7 @@ int cerot_solve(const double* alpha, const double* beta, const void* C, int64_t 
   if (!alpha || !beta || !C || !eps || !w_hat || !z_hat || !report) return arg_error("cerot_solve: NULL argument");
   if (max_iter < 0 || tol < 0) return arg_error("cerot_solve: max_iter >= 0 and tol >= 0 required");
   Workspace ws;
-  st = check_ws(workspace, ws_bytes, B, n, m, dtype, &ws);
+  st = check_ws(workspace, ws_bytes, B, n, m, m, dtype, &ws);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if (check_every < 1) check_every = 1;
@@ -332,7 +402,8 @@ int cerot_solve(const double* alpha, const double* beta, const void* C, int64_t 
       if (all) break;
     }
   }
-  COT_CHECK_CUDA(launch_plan(a, ws, up, T_blocks, ws.report, s));
+  st = plan_and_report(a, ws, T_blocks, ws.report, nullptr, s);
+  if (st) return st;
   std::vector<double> rep((size_t)B * kReportDoubles);
   COT_CHECK_CUDA(cudaMemcpyAsync(rep.data(), ws.report, rep.size() * 8, cudaMemcpyDeviceToHost, s));
   st = cerot_state(workspace, B, m, n, dtype, it.data(), conv.data(), res.data(), stream);
@@ -355,6 +426,153 @@ int cerot_solve(const double* alpha, const double* beta, const void* C, int64_t 
     all_conv = all_conv && (r.status == COT_OK);
   }
   return all_conv ? COT_OK : COT_NOT_CONVERGED;
+}
+
+// ------------------------------------------------------------------------------------- row sharding
+int cot_nccl_unique_id(void* id128) {
+  if (!id128) return arg_error("cot_nccl_unique_id: NULL output");
+  if (!nccl().ok) {
+    set_error(nccl().err);
+    return COT_E_NCCL;
+  }
+  ncclUniqueId id;
+  COT_CHECK_NCCL(nccl().GetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id128, &id, sizeof(id));
+  return COT_OK;
+}
+
+int cot_comm_init(const void* id128, int nranks, int rank, void** comm) {
+  if (!id128 || !comm || nranks < 1 || rank < 0 || rank >= nranks) return arg_error("cot_comm_init: bad arguments");
+  if (!nccl().ok) {
+    set_error(nccl().err);
+    return COT_E_NCCL;
+  }
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  ncclComm_t c = nullptr;
+  COT_CHECK_NCCL(nccl().CommInitRank(&c, nranks, id, rank));
+  *comm = c;
+  return COT_OK;
+}
+
+int cot_comm_destroy(void* comm) {
+  if (!comm) return COT_OK;
+  if (!nccl().ok) {
+    set_error(nccl().err);
+    return COT_E_NCCL;
+  }
+  COT_CHECK_NCCL(nccl().CommDestroy((ncclComm_t)comm));
+  return COT_OK;
+}
+
+int clot_aggregate_shard(const void* C_local, int64_t n, int64_t R, int64_t m, int dtype, void* G_local,
+                         int32_t* argmin_local, int32_t* d_nonfinite, void* stream) {
+  int st = check_shape(1, n, m, dtype);
+  if (st) return st;
+  if (R < 1 || R > m) return arg_error("clot_aggregate_shard: 1 <= R <= m required");
+  if (!C_local || !G_local || !argmin_local) return arg_error("clot_aggregate_shard: NULL argument");
+  COT_CHECK_CUDA(launch_aggregate(C_local, 1, n, m, dtype, G_local, argmin_local, d_nonfinite, (cudaStream_t)stream, R));
+  return COT_OK;
+}
+
+int clot_expand_shard(const void* S_local, const int32_t* argmin_local, int64_t n, int64_t R, int64_t m, int dtype,
+                      void* T_rows, void* stream) {
+  int st = check_shape(1, n, m, dtype);
+  if (st) return st;
+  if (R < 1 || R > m) return arg_error("clot_expand_shard: 1 <= R <= m required");
+  if (!S_local || !T_rows) return arg_error("clot_expand_shard: NULL argument");
+  COT_CHECK_CUDA(launch_expand(S_local, argmin_local, 1, n, m, dtype, T_rows, (cudaStream_t)stream, R));
+  return COT_OK;
+}
+
+int cerot_rows_shard(const double* alpha, const void* C_local, const void* G_local, int64_t n, int64_t m,
+                     int64_t row_begin, int64_t R, int dtype, const double* eps, uint32_t flags, const double* z_hat,
+                     double* w_hat, double* c_local, void* workspace, size_t ws_bytes, void* stream) {
+  int st = check_shape(1, n, m, dtype);
+  if (st) return st;
+  if (R < 1 || row_begin < 0 || row_begin + R > m) return arg_error("cerot_rows_shard: bad row range");
+  if (!alpha || !C_local || !G_local || !eps || !z_hat || !w_hat || !c_local)
+    return arg_error("cerot_rows_shard: NULL argument");
+  Workspace ws;
+  st = check_ws(workspace, ws_bytes, 1, n, m, R, dtype, &ws);
+  if (st) return st;
+  const IterArgs a = make_args(alpha, nullptr, C_local, G_local, 1, n, m, dtype, eps, 0.0, 1, flags, w_hat,
+                               const_cast<double*>(z_hat), row_begin, R);
+  cudaStream_t s = (cudaStream_t)stream;
+  COT_CHECK_CUDA(rows_pass(a, ws, 0, s));
+  COT_CHECK_CUDA(launch_colsum(ws, unit_plan(1, R, device_sm_count()), 1, m, 0, c_local, s));
+  return COT_OK;
+}
+
+int cerot_zupdate(const double* beta, const double* c, int64_t n, int64_t m, double tol, int64_t check_every,
+                  double* z_hat, void* workspace, size_t ws_bytes, void* stream) {
+  if (n < 1 || m < 1 || !beta || !c || !z_hat) return arg_error("cerot_zupdate: bad arguments");
+  if (tol < 0) return arg_error("cerot_zupdate: tol >= 0 required");
+  const size_t need = carve_workspace(nullptr, 1, n, m, 1, COT_F32, device_sm_count(), nullptr);
+  if (!workspace || ws_bytes < need) {
+    set_error("workspace too small");
+    return COT_E_WORKSPACE;
+  }
+  Workspace ws;   // only the state / counters / monitor offsets are used (they do not depend on R, n, dtype)
+  carve_workspace(workspace, 1, n, m, 1, COT_F32, device_sm_count(), &ws);
+  COT_CHECK_CUDA(launch_zupdate(c, beta, 1, m, n, tol, check_every, z_hat, ws, (cudaStream_t)stream));
+  return COT_OK;
+}
+
+int cerot_iter_sharded(const double* alpha, const double* beta, const void* C_local, const void* G_local, int64_t n,
+                       int64_t m, int64_t row_begin, int64_t R, int dtype, const double* eps, int64_t iters,
+                       double tol, int64_t check_every, uint32_t flags, double* w_hat, double* z_hat, void* workspace,
+                       size_t ws_bytes, void* comm, void* stream) {
+  int st = check_shape(1, n, m, dtype);
+  if (st) return st;
+  if (R < 1 || row_begin < 0 || row_begin + R > m) return arg_error("cerot_iter_sharded: bad row range");
+  if (!alpha || !beta || !C_local || !G_local || !eps || !w_hat || !z_hat)
+    return arg_error("cerot_iter_sharded: NULL argument");
+  if (iters < 0 || tol < 0) return arg_error("cerot_iter_sharded: iters >= 0 and tol >= 0 required");
+  if (comm && !nccl().ok) {
+    set_error(nccl().err);
+    return COT_E_NCCL;
+  }
+  Workspace ws;
+  st = check_ws(workspace, ws_bytes, 1, n, m, R, dtype, &ws);
+  if (st) return st;
+  const IterArgs a = make_args(alpha, beta, C_local, G_local, 1, n, m, dtype, eps, tol, check_every, flags, w_hat,
+                               z_hat, row_begin, R);
+  const UnitPlan up = unit_plan(1, R, device_sm_count());
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int64_t t = 0; t < iters; ++t) {
+    COT_CHECK_CUDA(rows_pass(a, ws, (int)(t & 1), s));
+    COT_CHECK_CUDA(launch_colsum(ws, up, 1, m, (int)(t & 1), ws.c_local, s));
+    const double* c = ws.c_local;
+    if (comm) {   // the exchange step: one m-length fp64 allreduce over NVLink / NVSwitch per iteration
+      COT_CHECK_NCCL(nccl().AllReduce(ws.c_local, ws.c_global, (size_t)m, ncclFloat64, ncclSum, (ncclComm_t)comm, s));
+      c = ws.c_global;
+    }
+    COT_CHECK_CUDA(launch_zupdate(c, beta, 1, m, n, tol, check_every, z_hat, ws, s));
+  }
+  return COT_OK;
+}
+
+int cerot_plan_sharded(const double* alpha, const double* beta, const void* C_local, const void* G_local, int64_t n,
+                       int64_t m, int64_t row_begin, int64_t R, int dtype, const double* eps, const double* w_hat,
+                       const double* z_hat, void* T_local, double* d_report, void* workspace, size_t ws_bytes,
+                       void* comm, void* stream) {
+  int st = check_shape(1, n, m, dtype);
+  if (st) return st;
+  if (R < 1 || row_begin < 0 || row_begin + R > m) return arg_error("cerot_plan_sharded: bad row range");
+  if (!alpha || !beta || !C_local || !G_local || !eps || !w_hat || !z_hat)
+    return arg_error("cerot_plan_sharded: NULL argument");
+  if (comm && !nccl().ok) {
+    set_error(nccl().err);
+    return COT_E_NCCL;
+  }
+  Workspace ws;
+  st = check_ws(workspace, ws_bytes, 1, n, m, R, dtype, &ws);
+  if (st) return st;
+  IterArgs a = make_args(alpha, beta, C_local, G_local, 1, n, m, dtype, eps, 0.0, 1, 0, const_cast<double*>(w_hat),
+                         const_cast<double*>(z_hat), row_begin, R);
+  return plan_and_report(a, ws, T_local, d_report, comm, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -31,6 +31,7 @@ UnitPlan unit_plan(int64_t B, int64_t R, int sm_count);
 
 constexpr int kReportDoubles = 8;   // cot_report field order: objective .. residual
 constexpr int kPlanScalars = 4;     // per unit: transport, entropy sum, row |r - alpha| sum, mass
+constexpr int kPlanBufHead = 5;     // plan buffer: 4 scalars + sum_{held rows} w_hat_i alpha_i, then m column sums
 
 struct Workspace {
   void* G;                 // [B][m][m] dtype
@@ -43,18 +44,24 @@ struct Workspace {
   unsigned* grid_bar;      // [4] two device-wide barriers of the persistent TMA kernel (count, generation)
   int32_t* nonfinite;      // [1]
   double* report;          // [B][kReportDoubles]
+  double* c_local;         // [B][m] column sums over the held rows (sharded path)
+  double* c_global;        // [B][m] column sums after the cross-GPU reduction
+  double* plan_buf;        // [B][kPlanBufHead + m] local plan reductions (allreduced in place)
 };
-// Lays the workspace out from `base` (may be NULL to only size it). Returns the byte count.
-size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int dtype, int sm_count, Workspace* ws);
+// Lays the workspace out from `base` (may be NULL to only size it). Returns the byte count. R = rows held
+// per problem (m unless row-sharded).
+size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, int dtype, int sm_count,
+                       Workspace* ws);
 
 int device_sm_count();
 void set_error(const std::string& msg);
 
 // ------------------------------------------------------------------------------- launchers
+// R = rows held per block (-1: m, unsharded)
 cudaError_t launch_aggregate(const void* C, int64_t B, int64_t n, int64_t m, int dtype, void* G, int32_t* A,
-                             int32_t* nonfinite, cudaStream_t s);
+                             int32_t* nonfinite, cudaStream_t s, int64_t R = -1);
 cudaError_t launch_expand(const void* S, const int32_t* A, int64_t B, int64_t n, int64_t m, int dtype, void* out,
-                          cudaStream_t s);
+                          cudaStream_t s, int64_t R = -1);
 
 struct IterArgs {
   const double* alpha;
@@ -83,7 +90,15 @@ bool tma_eligible(const IterArgs& a);
 // into ws.partials[parity] when rows_only.
 cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, bool rows_only, int parity,
                             cudaStream_t s);
-cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& up, void* T_blocks, double* d_report,
-                        cudaStream_t s);
+// Plan pass over the held rows: T blocks (optional) + unit partials in the workspace (no finalisation).
+cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& up, void* T_blocks, cudaStream_t s);
+cudaError_t launch_colsum(const Workspace& ws, const UnitPlan& up, int64_t B, int64_t m, int parity, double* c,
+                          cudaStream_t s);
+cudaError_t launch_zupdate(const double* c, const double* beta, int64_t B, int64_t m, int64_t n, double tol,
+                           int64_t check_every, double* z_hat, const Workspace& ws, cudaStream_t s);
+cudaError_t launch_plan_reduce_local(const IterArgs& a, const Workspace& ws, const UnitPlan& up, double* buf,
+                                     cudaStream_t s);
+cudaError_t launch_plan_finalize_buf(const IterArgs& a, const Workspace& ws, const double* buf, double* report,
+                                     cudaStream_t s);
 
 }  // namespace cot

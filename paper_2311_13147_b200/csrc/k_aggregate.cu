@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(256) k_aggregate(const T* __restrict__ C, int6
 }
 
 cudaError_t launch_aggregate(const void* C, int64_t B, int64_t n, int64_t m, int dtype, void* G, int32_t* A,
-                             int32_t* nonfinite, cudaStream_t s) {
-  const int64_t mm = m * m;
+                             int32_t* nonfinite, cudaStream_t s, int64_t R) {
+  const int64_t mm = (R < 0 ? m : R) * m;   // elements per block (R rows of m columns)
   if (nonfinite) {
     cudaError_t e = cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;

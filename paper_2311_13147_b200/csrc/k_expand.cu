@@ -34,34 +34,35 @@ struct VecT<T, 1> {
 };
 
 // Work unit = (b, k, i): one source row segment. Threads of the CTA cover (r, j-vector) pairs.
+// Source blocks hold R rows (R = m unsharded); destination row (r, i) is r*R + i with row stride d.
 template <typename T, int V>
 __global__ void __launch_bounds__(256) k_expand(const T* __restrict__ S, const int32_t* __restrict__ A, int64_t B,
-                                                int n, int64_t m, T* __restrict__ out) {
+                                                int n, int64_t m, int64_t R, T* __restrict__ out) {
   using VT = typename VecT<T, V>::type;
   const int64_t mv = m / V;            // vectors per row segment
   const int64_t d = (int64_t)n * m;
-  const int64_t units = B * n * m;
+  const int64_t units = B * n * R;
   const int64_t items = (int64_t)n * mv;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const int64_t b = u / (n * m);
-    const int64_t rem = u - b * n * m;
-    const int k = (int)(rem / m);
-    const int64_t i = rem - (int64_t)k * m;
-    T* ob = out + b * d * d;
+    const int64_t b = u / (n * R);
+    const int64_t rem = u - b * n * R;
+    const int k = (int)(rem / R);
+    const int64_t i = rem - (int64_t)k * R;
+    T* ob = out + b * (int64_t)n * R * d;
     for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
       const int r = (int)(it / mv);
       const int64_t jv = it - (int64_t)r * mv;
       VT v;
       if (A == nullptr) {
-        v = reinterpret_cast<const VT*>(S + ((b * n + k) * m + i) * m)[jv];
+        v = reinterpret_cast<const VT*>(S + ((b * n + k) * R + i) * m)[jv];
       } else {
-        const VT sv = reinterpret_cast<const VT*>(S + (b * m + i) * m)[jv];
-        const int32_t* ar = A + (b * m + i) * m + jv * V;
+        const VT sv = reinterpret_cast<const VT*>(S + (b * R + i) * m)[jv];
+        const int32_t* ar = A + (b * R + i) * m + jv * V;
 #pragma unroll
         for (int q = 0; q < V; ++q) VecT<T, V>::set(v, q, ar[q] == k ? VecT<T, V>::get(sv, q) : T(0));
       }
       const int s = (r + k) % n;        // block (r, s) holds source block (s - r) mod n = k
-      VT* dst = reinterpret_cast<VT*>(ob + ((int64_t)r * m + i) * d + (int64_t)s * m) + jv;
+      VT* dst = reinterpret_cast<VT*>(ob + ((int64_t)r * R + i) * d + (int64_t)s * m) + jv;
       __stcs(dst, v);
     }
   }
@@ -73,37 +74,37 @@ __global__ void __launch_bounds__(256) k_expand(const T* __restrict__ S, const i
 // Two smem slots alternate; bulk-async group accounting guards their reuse.
 template <typename T>
 __global__ void __launch_bounds__(128) k_expand_bulk(const T* __restrict__ S, const int32_t* __restrict__ A,
-                                                     int64_t B, int n, int64_t m, T* __restrict__ out) {
+                                                     int64_t B, int n, int64_t m, int64_t R, T* __restrict__ out) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int64_t mpad = (m + 31) & ~int64_t(31);
   T* bufs = reinterpret_cast<T*>(smem_raw);
   const int64_t d = (int64_t)n * m;
-  const int64_t units = B * n * m;
+  const int64_t units = B * n * R;
   const uint32_t seg_bytes = (uint32_t)(m * sizeof(T));
   int slot = 0;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x, slot ^= 1) {
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     __syncthreads();
-    const int64_t b = u / (n * m);
-    const int64_t rem = u - b * n * m;
-    const int k = (int)(rem / m);
-    const int64_t i = rem - (int64_t)k * m;
+    const int64_t b = u / (n * R);
+    const int64_t rem = u - b * n * R;
+    const int k = (int)(rem / R);
+    const int64_t i = rem - (int64_t)k * R;
     T* buf = bufs + slot * mpad;
     if (A == nullptr) {
-      const T* src = S + ((b * n + k) * m + i) * m;
+      const T* src = S + ((b * n + k) * R + i) * m;
       for (int64_t j = threadIdx.x; j < m; j += blockDim.x) buf[j] = __ldg(src + j);
     } else {
-      const T* src = S + (b * m + i) * m;
-      const int32_t* ar = A + (b * m + i) * m;
+      const T* src = S + (b * R + i) * m;
+      const int32_t* ar = A + (b * R + i) * m;
       for (int64_t j = threadIdx.x; j < m; j += blockDim.x) buf[j] = (__ldg(ar + j) == k) ? __ldg(src + j) : T(0);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
-      T* ob = out + b * d * d + i * d;
+      T* ob = out + b * (int64_t)n * R * d + i * d;
       const uint32_t sbuf = smem_u32(buf);
       for (int r = 0, s = k; r < n; ++r, s = (s + 1 == n) ? 0 : s + 1) {   // block (r, s), s = (r + k) mod n
-        T* dst = ob + (int64_t)r * m * d + (int64_t)s * m;
+        T* dst = ob + (int64_t)r * R * d + (int64_t)s * m;
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sbuf),
                      "r"(seg_bytes)
                      : "memory");
@@ -115,9 +116,10 @@ __global__ void __launch_bounds__(128) k_expand_bulk(const T* __restrict__ S, co
 }
 
 cudaError_t launch_expand(const void* S, const int32_t* A, int64_t B, int64_t n, int64_t m, int dtype, void* out,
-                          cudaStream_t s) {
+                          cudaStream_t s, int64_t R) {
+  if (R < 0) R = m;
   const int sms = device_sm_count();
-  const int64_t units = B * n * m;
+  const int64_t units = B * n * R;
   const int grid = (int)(units < (int64_t)sms * 16 ? units : (int64_t)sms * 16);
   const size_t esz = dtype == COT_F32 ? 4 : 8;
   if ((m * esz) % 16 == 0 && m * esz <= 32768) {
@@ -127,24 +129,24 @@ cudaError_t launch_expand(const void* S, const int32_t* A, int64_t B, int64_t n,
     if (dtype == COT_F32) {
       e = cudaFuncSetAttribute(k_expand_bulk<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      k_expand_bulk<float><<<grid, 128, smem, s>>>((const float*)S, A, B, (int)n, m, (float*)out);
+      k_expand_bulk<float><<<grid, 128, smem, s>>>((const float*)S, A, B, (int)n, m, R, (float*)out);
     } else {
       e = cudaFuncSetAttribute(k_expand_bulk<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      k_expand_bulk<double><<<grid, 128, smem, s>>>((const double*)S, A, B, (int)n, m, (double*)out);
+      k_expand_bulk<double><<<grid, 128, smem, s>>>((const double*)S, A, B, (int)n, m, R, (double*)out);
     }
     return cudaGetLastError();
   }
   if (dtype == COT_F32) {
     if (m % 4 == 0)
-      k_expand<float, 4><<<grid, 256, 0, s>>>((const float*)S, A, B, (int)n, m, (float*)out);
+      k_expand<float, 4><<<grid, 256, 0, s>>>((const float*)S, A, B, (int)n, m, R, (float*)out);
     else
-      k_expand<float, 1><<<grid, 256, 0, s>>>((const float*)S, A, B, (int)n, m, (float*)out);
+      k_expand<float, 1><<<grid, 256, 0, s>>>((const float*)S, A, B, (int)n, m, R, (float*)out);
   } else {
     if (m % 2 == 0)
-      k_expand<double, 2><<<grid, 256, 0, s>>>((const double*)S, A, B, (int)n, m, (double*)out);
+      k_expand<double, 2><<<grid, 256, 0, s>>>((const double*)S, A, B, (int)n, m, R, (double*)out);
     else
-      k_expand<double, 1><<<grid, 256, 0, s>>>((const double*)S, A, B, (int)n, m, (double*)out);
+      k_expand<double, 1><<<grid, 256, 0, s>>>((const double*)S, A, B, (int)n, m, R, (double*)out);
   }
   return cudaGetLastError();
 }

@@ -157,52 +157,6 @@ __global__ void __launch_bounds__(256) k_plan(PlanParams p) {
   }
 }
 
-// One block per problem: fixed-order sums of the unit partials -> the report (cot_report field order).
-__global__ void __launch_bounds__(256) k_plan_finalize(const double* __restrict__ partials,
-                                                       const double* __restrict__ scal, int64_t upp, int64_t m,
-                                                       int64_t n, const double* __restrict__ alpha,
-                                                       const double* __restrict__ beta,
-                                                       const double* __restrict__ w_hat,
-                                                       const double* __restrict__ z_hat,
-                                                       const double* __restrict__ eps,
-                                                       const SolverState* __restrict__ state,
-                                                       double* __restrict__ report) {
-  __shared__ double sh[32];
-  const int64_t b = blockIdx.x;
-  double cl1 = 0.0, cl2 = 0.0, dot = 0.0;
-  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
-    double c = 0.0;
-    for (int64_t u = 0; u < upp; ++u) c += partials[(b * upp + u) * m + j];
-    const double dv = c - beta[b * m + j];
-    cl1 += fabs(dv);
-    cl2 += dv * dv;
-    dot += w_hat[b * m + j] * alpha[b * m + j] + z_hat[b * m + j] * beta[b * m + j];
-  }
-  cl1 = pblk_sum(cl1, sh);
-  cl2 = pblk_sum(cl2, sh);
-  dot = pblk_sum(dot, sh);
-  if (threadIdx.x == 0) {
-    double tr = 0.0, en = 0.0, rl1 = 0.0, mass = 0.0;
-    for (int64_t u = 0; u < upp; ++u) {
-      const double* sc = scal + (b * upp + u) * kPlanScalars;
-      tr += sc[0];
-      en += sc[1];
-      rl1 += sc[2];
-      mass += sc[3];
-    }
-    const double nn = (double)n, e = eps[b];
-    double* rep = report + b * kReportDoubles;
-    rep[0] = nn * tr;                       // objective: transport cost of the full plan
-    rep[1] = nn * (tr + e * en);            // regularised primal
-    rep[2] = nn * e * (dot - mass);         // dual (phi*(y) = eps e^{y/eps})
-    rep[3] = nn * rl1;                      // ||T 1 - a||_1
-    rep[4] = nn * cl1;                      // ||T^T 1 - b||_1
-    rep[5] = sqrt(nn * cl2);                // ||T^T 1 - b||_2
-    rep[6] = nn * mass;                     // full plan mass
-    rep[7] = state ? state[b].residual : 0.0;
-  }
-}
-
 template <typename T, int V>
 static cudaError_t plan_dispatch(const PlanParams& pp, int grid, int64_t m, cudaStream_t s) {
   const int64_t mv = m / V;
@@ -222,8 +176,7 @@ static cudaError_t plan_dispatch(const PlanParams& pp, int grid, int64_t m, cuda
   return cudaGetLastError();
 }
 
-cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& up, void* T_blocks, double* d_report,
-                        cudaStream_t s) {
+cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& up, void* T_blocks, cudaStream_t s) {
   PlanParams pp;
   pp.C = a.C;
   pp.G = a.G;
@@ -247,10 +200,7 @@ cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& 
     e = (a.m % 4 == 0) ? plan_dispatch<float, 4>(pp, up.grid, a.m, s) : plan_dispatch<float, 1>(pp, up.grid, a.m, s);
   else
     e = (a.m % 2 == 0) ? plan_dispatch<double, 2>(pp, up.grid, a.m, s) : plan_dispatch<double, 1>(pp, up.grid, a.m, s);
-  if (e != cudaSuccess) return e;
-  k_plan_finalize<<<(unsigned)a.B, 256, 0, s>>>(ws.partials[0], ws.plan_scal, up.upp, a.m, a.n, a.alpha, a.beta,
-                                                a.w_hat, a.z_hat, a.eps, ws.state, d_report ? d_report : ws.report);
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace cot
