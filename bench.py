@@ -15,6 +15,7 @@ iterations), the largest single-GPU configuration the metric is quoted on ("% of
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import math
 import os
@@ -167,7 +168,8 @@ class Runner:
         self.flags = int(os.environ.get("COT_BENCH_FLAGS", "0"))
         # the persistent TMA kernel runs all iterations in one launch (B == 1, fp32, m % 4 == 0)
         self.persistent = (self.B == 1 and self.dt == cot.COT_F32 and self.m % 4 == 0 and not (self.flags & 2))
-        self.launches_per_step = 1 + 1 + (1 if self.persistent else 2 * iters) + 2 + 1
+        self.launches_per_step = 1 + 1 + (1 if self.persistent else 2 * iters) + 3 + 1
+        self.bytes_iter = float(p.B) * (p.n + 1) * p.m * p.m * p.C.itemsize
 
     def _ck(self, code, fn):
         if code != 0:
@@ -197,109 +199,239 @@ class Runner:
         ts = [a.elapsed_time(b) for a, b in self.ev]
         return statistics.mean(ts), statistics.median(ts), len(ts)
 
+    def report_row(self):
+        return self.rep.cpu().numpy()[0]
+
+    def e2e_inputs(self):
+        return self.p.C, self.C, [(self.p.alpha, self.alpha), (self.p.beta, self.beta), (self.p.eps, self.eps)], \
+            [self.rep, self.w, self.z]
+
+
+class stdout_to_stderr:
+    """Route the process's C-level stdout to stderr (NCCL prints its version banner at communicator init);
+    bench.py's stdout carries exactly one JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
+class ShardedRunner:
+    """Row sharding of one problem over the ranks: this rank holds rows
+    [row_begin, row_begin + R) of every block; one fp64 ncclAllReduce of the m column sums per iteration
+    inside libcyclicot (cerot_iter_sharded); plan report reduced across ranks; each rank expands its rows."""
+
+    def __init__(self, p, iters, dev, stream, rank, world):
+        import torch
+        import paper_2311_13147_b200 as cot
+        from paper_2311_13147_b200 import dist as cdist
+        assert not p.batched
+        self.cot, self.cdist, self.L, self.torch = cot, cdist, cot.lib(), torch
+        self.p, self.iters, self.stream = p, iters, stream
+        self.B, self.n, self.m = 1, p.n, p.m
+        self.row_begin, self.R = cdist.row_partition(p.m, world, rank)
+        with stdout_to_stderr():
+            self.comm = cdist.NcclComm()
+        Cl = np.ascontiguousarray(p.C[:, self.row_begin:self.row_begin + self.R, :])
+        self.Cl_host = Cl
+        self.sh = cdist.ShardedCerot(torch.as_tensor(Cl, device=dev), torch.as_tensor(p.alpha, device=dev),
+                                     torch.as_tensor(p.beta, device=dev), float(p.eps[0]), self.row_begin, p.m,
+                                     comm=self.comm, stream=stream)
+        d = p.n * p.m
+        self.Tl = torch.empty_like(self.sh.C)
+        self.Trows = torch.empty((p.n, self.R, d), dtype=self.sh.C.dtype, device=dev)
+        self.rep = torch.empty(8, dtype=torch.float64, device=dev)
+        self.nf = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ev = []
+        self.persistent = False
+        self.launches_per_step = 1 + 1 + 3 * iters + 3 + 1
+        self.bytes_iter = float(p.n + 1) * self.R * p.m * p.C.itemsize
+        q = lambda t: t.data_ptr()
+        self.q = dict(C=q(self.sh.C), G=q(self.sh.G), A=q(self.sh.argmin), a=q(self.sh.alpha), b=q(self.sh.beta),
+                      e=q(self.sh.eps), w=q(self.sh.w_hat), z=q(self.sh.z_hat), ws=q(self.sh.ws), Tl=q(self.Tl),
+                      Tr=q(self.Trows), rep=q(self.rep), nf=q(self.nf))
+        self.s = stream.cuda_stream
+
+    def _ck(self, code, fn):
+        if code != 0:
+            raise RuntimeError(f"{fn} failed ({code}): {self.L.cot_last_error().decode()}")
+
+    def step(self, record=False):
+        L, q, s, sh = self.L, self.q, self.s, self.sh
+        n, m, R, dt, wsn = self.n, self.m, self.R, sh.dt, sh.ws.numel()
+        self._ck(L.clot_aggregate_shard(q["C"], n, R, m, dt, q["G"], q["A"], q["nf"], s), "clot_aggregate_shard")
+        self._ck(L.cerot_init(q["a"], q["b"], 1, m, 1, q["z"], q["ws"], wsn, s), "cerot_init")
+        if record:
+            e0 = self.torch.cuda.Event(enable_timing=True)
+            e1 = self.torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+        self._ck(L.cerot_iter_sharded(q["a"], q["b"], q["C"], q["G"], n, m, self.row_begin, R, dt, q["e"], self.iters,
+                                      0.0, 1, 0, q["w"], q["z"], q["ws"], wsn, self.comm.handle, s),
+                 "cerot_iter_sharded")
+        if record:
+            e1.record(self.stream)
+            self.ev.append((e0, e1))
+        self._ck(L.cerot_plan_sharded(q["a"], q["b"], q["C"], q["G"], n, m, self.row_begin, R, dt, q["e"], q["w"],
+                                      q["z"], q["Tl"], q["rep"], q["ws"], wsn, self.comm.handle, s),
+                 "cerot_plan_sharded")
+        self._ck(L.clot_expand_shard(q["Tl"], None, n, R, m, dt, q["Tr"], s), "clot_expand_shard")
+
+    def iter_kernel_ms(self):
+        ts = [a.elapsed_time(b) for a, b in self.ev]
+        return statistics.mean(ts), statistics.median(ts), len(ts)
+
+    def report_row(self):
+        return self.rep.cpu().numpy()
+
+    def e2e_inputs(self):
+        return self.Cl_host, self.sh.C, [(self.p.alpha, self.sh.alpha), (self.p.beta, self.sh.beta),
+                                         (self.p.eps, self.sh.eps)], [self.rep, self.sh.w_hat, self.sh.z_hat]
+
 
 def run_ours(args, rank, world, local_rank):
     import torch
+    import torch.distributed as tdist
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     from paper_2311_13147_b200 import build as _b
     if rank == 0:
         _b.build()
     if world > 1:
-        torch.distributed.barrier()
+        tdist.barrier()
     p, iters = make_problem(args.workload, args.iters)
-    if world > 1:
-        raise SystemExit("multi-GPU row sharding: see bench_sharded (not in this build)")
+    mode = "single"
+    if world > 1 or os.environ.get("COT_BENCH_SHARDED") == "1":
+        if p.batched:   # problem sharding (C5): a contiguous slice of the batch, no data-path collective
+            from paper_2311_13147_b200 import dist as cdist
+            f, cnt = cdist.problem_partition(p.B, world, rank)
+            p = dataclasses.replace(p, C=p.C[f:f + cnt], alpha=p.alpha[f:f + cnt], beta=p.beta[f:f + cnt],
+                                    eps=p.eps[f:f + cnt])
+            mode = "problem_sharded"
+        else:
+            mode = "row_sharded"
     stream = torch.cuda.Stream(device=dev)
+
+    def barrier():
+        if tdist.is_initialized():
+            tdist.barrier(device_ids=[local_rank])
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
     with torch.cuda.stream(stream):
-        R = Runner(p, iters, dev, stream)
+        R = ShardedRunner(p, iters, dev, stream, rank, world) if mode == "row_sharded" else Runner(p, iters, dev, stream)
         for _ in range(args.warmup):
             R.step()
         stream.synchronize()
-        rep0 = R.rep.cpu().numpy()[0]
+        rep0 = R.report_row()
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         with ClockSampler(local_rank) as clk:
+            barrier()
             torch.cuda.synchronize()
             start.record(stream)
             for _ in range(args.steps):
                 R.step(record=True)
             end.record(stream)
             torch.cuda.synchronize()
-        ms_total = start.elapsed_time(end)
+            barrier()
+        ms_total = max_over_ranks(start.elapsed_time(end))
         ms_step = ms_total / args.steps
         it_mean, it_med, nsamp = R.iter_kernel_ms()
+        it_mean = max_over_ranks(it_mean)
         # ---- e2e: the same step through the C ABI from pinned HOST buffers, copies inside the timed region
-        e2e = run_e2e(R, p, max(1, min(args.steps, 3)), stream) if not args.no_e2e else None
-    evals_step = float(p.B) * p.n * p.m * p.m * iters
+        e2e = None
+        if not args.no_e2e:
+            e2e = run_e2e(R, p, max(1, min(args.steps, 3)), stream)
+            e2e["ms_per_step"] = max_over_ranks(e2e["ms_per_step"])
+    B_total = p.B if mode != "problem_sharded" else int(os.environ.get("COT_C5_B", "4096"))
+    evals_step = float(B_total) * p.n * p.m * p.m * iters
     value = evals_step / (ms_step / 1e3)
+    if e2e:
+        e2e["value"] = evals_step / (e2e["ms_per_step"] / 1e3)
     peak, peak_src = _peaks()
-    bytes_iter = float(p.B) * (p.n + 1) * p.m * p.m * p.C.itemsize     # C and G streamed once per iteration
+    bytes_iter = R.bytes_iter                       # this rank's C and G, streamed once per iteration
     bytes_launch = bytes_iter * iters if R.persistent else bytes_iter
     per_launch_ms = it_mean if R.persistent else it_mean / iters
     achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
     dom_share = it_mean / ms_step
+    kernel = ("k_iter_tma (persistent: all iterations in one launch)" if R.persistent else
+              ("per iteration: k_iter_tma rows-only + k_colsum + ncclAllReduce + k_zupdate" if mode == "row_sharded"
+               else "k_rows_ldg + k_cols (one launch pair per iteration)"))
+    trf = _ncu_traffic_per_iter(args.workload) if world == 1 else None
     out = {
         "metric": _metric(), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32" if p.C.dtype == np.float32 else "f64",
         "data": "synthetic (seeded; BASELINE.json recipe, random-rotation point clouds, no dataset)",
-        "config": {"workload": p.name, "B": p.B, "n": p.n, "m": p.m, "d": p.d, "iters": iters,
+        "config": {"workload": p.name if mode != "problem_sharded" else f"C5_batched_B{B_total}", "B": B_total,
+                   "n": p.n, "m": p.m, "d": p.d, "iters": iters,
                    "eps": float(p.eps[0]) if p.B == 1 else "per-problem 1e-2*mean(C_b)",
-                   "step": "clot_aggregate + cerot_init + iters x (cerot_rows + cerot_cols) + cerot_plan + clot_expand",
-                   "l2": f"inputs ({p.C.nbytes / 1e6:.0f} MB of cost) larger than L2 (126 MB): no flush",
-                   "parallelism": f"rows/units over {torch.cuda.get_device_properties(dev).multi_processor_count} SMs"},
-        "roofline": {"bound": "hbm",
-                     "kernel": ("k_iter_tma (persistent: all iterations in one launch)" if R.persistent
-                                else "k_rows_ldg + k_cols (one launch pair per iteration)"),
+                   "step": "clot_aggregate + cerot_init + iters x (row pass + column pass) + cerot_plan + clot_expand",
+                   "l2": f"inputs ({p.C.nbytes * (world if mode == 'row_sharded' else 1) / 1e6:.0f} MB of cost) "
+                         f"larger than L2 (126 MB) at N=1: no flush",
+                   "parallelism": {"single": "rows over the SMs of one GPU",
+                                   "row_sharded": f"rows over {world} GPUs, 1 ncclAllReduce (m fp64) per iteration",
+                                   "problem_sharded": f"problems over {world} GPUs, no collective"}[mode]},
+        "roofline": {"bound": "hbm", "kernel": kernel,
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src,
-                     "traffic": (None if _ncu_traffic_per_iter(args.workload) is None else
-                                 _ncu_traffic_per_iter(args.workload) * (iters if R.persistent else 1)),
+                     "traffic": None if trf is None else trf * (iters if R.persistent else 1),
                      "algorithmic_bytes_per_launch": bytes_launch, "algorithmic_bytes_per_iter": bytes_iter,
                      "launch_ms_mean": per_launch_ms, "launch_samples": nsamp, "share_of_step": dom_share,
                      "us_per_iter": it_mean * 1e3 / iters},
-        "iter_only_evals_per_s": float(p.B) * p.n * p.m * p.m * iters / (it_mean / 1e3),
+        "iter_only_evals_per_s": evals_step / (it_mean / 1e3),
         "gpu_launches": R.launches_per_step * args.steps,
         "result": {"objective": float(rep0[0]), "dual": float(rep0[2]), "row_l1": float(rep0[3])},
     }
     if e2e:
         out["e2e"] = e2e
-    if not args.no_cpu:
+    if not args.no_cpu and rank == 0:
         out["cpu_baseline"] = cpu_baseline(p, args)
     out["clocks"] = clk.summary()
+    if mode == "row_sharded":
+        R.comm.close()
     return out
 
 
 def run_e2e(R, p, steps, stream):
     """Host buffers -> device (pinned, async) -> step -> report + potentials back to host, per step."""
     import torch
+    hostC, devC, small, results = R.e2e_inputs()
     pin = lambda x: torch.as_tensor(np.ascontiguousarray(x)).pin_memory()
-    hC, ha, hb, he = pin(p.C), pin(p.alpha), pin(p.beta), pin(p.eps)
-    hrep = torch.empty((R.B, 8), dtype=torch.float64).pin_memory()
-    hw = torch.empty_like(R.w, device="cpu").pin_memory()
-    hz = torch.empty_like(R.z, device="cpu").pin_memory()
-    h2d = hC.numel() * hC.element_size() + (ha.numel() + hb.numel() + he.numel()) * 8
-    d2h = (hrep.numel() + hw.numel() + hz.numel()) * 8
+    hC = pin(hostC)
+    hsmall = [(pin(h), d) for h, d in small]
+    hres = [(torch.empty(r.shape, dtype=r.dtype).pin_memory(), r) for r in results]
+    h2d = hC.numel() * hC.element_size() + sum(h.numel() * h.element_size() for h, _ in hsmall)
+    d2h = sum(h.numel() * h.element_size() for h, _ in hres)
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(steps):
-        R.C.copy_(hC, non_blocking=True)
-        R.alpha.copy_(ha, non_blocking=True)
-        R.beta.copy_(hb, non_blocking=True)
-        R.eps.copy_(he, non_blocking=True)
+        devC.copy_(hC, non_blocking=True)
+        for h, d in hsmall:
+            d.copy_(h, non_blocking=True)
         R.step()
-        hrep.copy_(R.rep, non_blocking=True)
-        hw.copy_(R.w, non_blocking=True)
-        hz.copy_(R.z, non_blocking=True)
+        for h, d in hres:
+            h.copy_(d, non_blocking=True)
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
-    evals = float(p.B) * p.n * p.m * p.m * R.iters
-    return {"value": evals / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": ms, "steps": steps, "api": "C ABI (clot_aggregate, cerot_init/rows/cols/plan, clot_expand)"}
+    return {"value": None, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": ms, "steps": steps,
+            "api": "C ABI (clot_aggregate, cerot_init/iter/plan, clot_expand; sharded variants for N>1)"}
 
 
 # ------------------------------------------------------------------------------------------ oracle arm
@@ -377,13 +509,31 @@ def main():
             return 0
         print(json.dumps(run_reference(args)), flush=True)
         return 0
-    if world > 1:
+    force_sharded = os.environ.get("COT_BENCH_SHARDED") == "1"   # exercise the row-sharded path at N = 1
+    if world > 1 or force_sharded:
         import torch
-        torch.distributed.init_process_group("nccl")
+        torch.cuda.set_device(local_rank)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if torch_dist_initialized():
+        import torch.distributed as tdist
+        tdist.destroy_process_group()
     return 0
+
+
+def torch_dist_initialized() -> bool:
+    try:
+        import torch.distributed as tdist
+        return tdist.is_available() and tdist.is_initialized()
+    except Exception:
+        return False
 
 
 if __name__ == "__main__":
