@@ -56,7 +56,8 @@ typedef enum {
 /* Flags for cerot_* */
 #define COT_COLD_START 0x1u   /* start from q = 1_m, i.e. z_hat = 0 (Alg. 2 line 2); otherwise
                                  z_hat is a warm start                                                  */
-#define COT_FORCE_LDG  0x2u   /* use the generic LDG row kernel even where the TMA kernel applies     */
+#define COT_FORCE_LDG  0x2u   /* use the generic LDG row kernels even where the TMA (large problems)  */
+                              /* or cluster-resident (small problems) kernels apply                    */
 /* Diagnostic flags (results are NOT valid with them; used by scripts/ubench_iter.py only):          */
 #define COT_DIAG_NO_COMPUTE 0x100u  /* TMA kernel: consumers only acknowledge slots (pure HBM stream)    */
 #define COT_DIAG_NO_SYNC    0x200u  /* TMA kernel: skip the column pass and device-wide barriers        */

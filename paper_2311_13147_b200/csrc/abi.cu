@@ -278,7 +278,11 @@ int cerot_iter(const double* alpha, const double* beta, const void* C, const voi
   const IterArgs a = make_args(alpha, beta, C, G, B, n, m, dtype, eps, tol, check_every, flags, w_hat, z_hat);
   const UnitPlan up = unit_plan(B, m, device_sm_count());
   cudaStream_t s = (cudaStream_t)stream;
-  if (iters > 0 && tma_eligible(a)) {
+  if (iters > 0 && batch_cluster_eligible(a)) {   // small problems: whole problem on chip (C5, C2)
+    COT_CHECK_CUDA(launch_batch_cluster(a, ws, (int)iters, s));
+    return COT_OK;
+  }
+  if (iters > 0 && tma_eligible(a)) {              // large problem: persistent TMA stream (C3, C4)
     COT_CHECK_CUDA(launch_iter_tma(a, ws, (int)iters, false, 0, s));
     return COT_OK;
   }
@@ -385,7 +389,9 @@ int cerot_solve(const double* alpha, const double* beta, const void* C, int64_t 
   int64_t done = 0;
   while (done < max_iter) {
     const int64_t chunk = std::min<int64_t>(check_every, max_iter - done);
-    if (tma_eligible(a)) {
+    if (batch_cluster_eligible(a)) {
+      COT_CHECK_CUDA(launch_batch_cluster(a, ws, (int)chunk, s));
+    } else if (tma_eligible(a)) {
       COT_CHECK_CUDA(launch_iter_tma(a, ws, (int)chunk, false, 0, s));
     } else {
       for (int64_t t = 0; t < chunk; ++t) {

@@ -86,6 +86,9 @@ cudaError_t launch_rows(const IterArgs& a, const Workspace& ws, const UnitPlan& 
 // Column pass (deterministic reduction + q-update + monitor) reading ws.partials[parity].
 cudaError_t launch_cols(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int parity, cudaStream_t s);
 bool tma_eligible(const IterArgs& a);
+// Cluster-resident small problems (fp32, m <= 256, m % 4 == 0): `iters` full iterations of every problem.
+bool batch_cluster_eligible(const IterArgs& a);
+cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int iters, cudaStream_t s);
 // Persistent TMA kernel: `iters` full iterations (cooperative launch), or the row pass of one iteration
 // into ws.partials[parity] when rows_only.
 cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, bool rows_only, int parity,

@@ -1,0 +1,361 @@
+// K-BATCH: cluster-resident cyclic Sinkhorn for small problems (C5: B = 4096 x (n = 16, m = 128); C2), the
+// same arithmetic as k_rows_ldg + k_cols (k_iter.cu) with the whole problem on chip for all iterations.
+//
+// One thread-block cluster of NCL = 8 CTAs per problem. CTA c holds rows [c*RB, (c+1)*RB) of every cost
+// block in shared memory (RB*n*m fp32; 128 KiB for C5), loaded once with TMA bulk copies, plus its G rows
+// and a replica of z_hat. One warp per row, VEC = 4 columns per lane (x VPL):
+//   k-sum       s_ij = sum_k exp2((G_ij - C_ijk) log2e/eps) from shared memory (FFMA + MUFU.EX2 + FADD);
+//   epilogue    x_ij = z_hat_j - G_ij/eps (fp64), M_i = max_j x_ij and r_i by warp shuffles (no block
+//               barrier: a row lives in one warp), w_hat_i = log alpha_i - M_i - log r_i,
+//               column terms (alpha_i / r_i) s_ij exp(x_ij - M_i) accumulated per warp in fp64;
+//   columns     per-CTA column partials in shared memory; after a cluster barrier CTA c sums the 8 CTAs'
+//               partials of its column slice through DSMEM in CTA order (deterministic), applies the
+//               q-update z_hat_j += log beta_j - log c_j and writes z_hat_j into every CTA's replica (DSMEM);
+//               a second cluster barrier publishes the new z_hat. The monitor n*sum|c_j - beta_j| is combined
+//               through CTA 0's shared memory and read by all CTAs (uniform freeze decision).
+// No HBM traffic per iteration: the bound is the SFU (n*m^2 MUFU.EX2 per iteration per problem) plus two
+// cluster barriers.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace cot {
+
+constexpr int kNCL = 8;   // CTAs per cluster (portable maximum)
+
+struct BatchParams {
+  const float* C;        // [B][n][m][m]
+  const float* G;        // [B][m][m]
+  const double* alpha;   // [B][m]
+  const double* beta;    // [B][m]
+  double* w_hat;         // [B][m]
+  double* z_hat;         // [B][m]
+  const double* eps;     // [B]
+  SolverState* state;    // [B]
+  int n, m, RB;          // rows per CTA
+  int iters;
+  double tol;
+  long long check_every;
+};
+
+template <int VPL>
+__global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int64_t b = blockIdx.x / kNCL;                      // problem of this cluster
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int n = p.n, m = p.m, RB = p.RB, mv = m >> 2;
+  const int r0 = crank * RB;                                // first row of this CTA
+  const int nrows = max(0, min(RB, m - r0));
+  // ---- shared memory: C rows [RB][n][m] f32 | G rows [RB][m] f32 | z [m] f64 | warp partials [nw][m] f64 |
+  //      CTA partial [m] f64 | monitor partials [NCL] f64 | mbarrier
+  float* Cs = reinterpret_cast<float*>(smem);
+  float* Gs = Cs + (size_t)RB * n * m;
+  double* zs = reinterpret_cast<double*>(Gs + (size_t)RB * m);
+  double* wpart = zs + m;
+  double* cpart = wpart + (size_t)nwarps * m;
+  double* mon = cpart + m;
+  double* rstat = mon + kNCL;                                // [RB][4]: M_i, r_i, alpha_i, log alpha_i
+  double* bcol = rstat + (size_t)RB * 4;                     // [m][2]: beta_j, log beta_j
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bcol + (size_t)m * 2);
+  __shared__ int s_flags;
+
+  SolverState st = p.state[b];
+  if (!st.active) return;                                   // cluster-uniform
+  const double inv_eps = 1.0 / p.eps[b];
+  const float c2 = (float)(COT_LOG2E * inv_eps);
+
+  // ---- load this CTA's rows of C (all n blocks) and G once (TMA bulk copies, one mbarrier)
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    s_flags = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && nrows > 0) {
+    const uint32_t row_bytes = (uint32_t)m * 4u;
+    mbar_arrive_expect_tx(bar, (uint32_t)nrows * (uint32_t)(n + 1) * row_bytes);
+    const uint64_t pol = policy_evict_first();
+    for (int i = 0; i < nrows; ++i) {
+      for (int k = 0; k < n; ++k)
+        bulk_g2s(Cs + ((size_t)i * n + k) * m, p.C + (((size_t)b * n + k) * m + r0 + i) * m, row_bytes, bar, pol);
+      bulk_g2s(Gs + (size_t)i * m, p.G + ((size_t)b * m + r0 + i) * m, row_bytes, bar, pol);
+    }
+  }
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    zs[j] = p.z_hat[b * m + j];
+    const double bj = p.beta[b * m + j];
+    bcol[2 * j] = bj;
+    bcol[2 * j + 1] = log(bj);
+  }
+  for (int i = threadIdx.x; i < nrows; i += blockDim.x) {
+    const double a = p.alpha[b * m + r0 + i];
+    rstat[4 * i + 2] = a;
+    rstat[4 * i + 3] = log(a);
+  }
+  if (nrows > 0) mbar_wait(bar, 0);
+  __syncthreads();
+
+  const int cols_per_cta = (m + kNCL - 1) / kNCL;
+  const int c0 = crank * cols_per_cta, c1 = min(m, c0 + cols_per_cta);
+  const int nrw = (nrows + nwarps - 1) / nwarps;            // rows per warp (1 for C5)
+  constexpr int MAXR = 2;
+  // k-sums of the warp's rows for the next epilogue, accumulated in two halves of the k range so that each
+  // half can cover one cluster-barrier latency
+  float sacc[MAXR][VPL][4], gcr[MAXR][VPL][4];
+  auto ksum_range = [&](int k_lo, int k_hi) {
+    for (int rr = 0; rr < nrw && rr < MAXR; ++rr) {
+      const int i = warp + rr * nwarps;
+      if (i >= nrows) break;
+      const float4* crow = reinterpret_cast<const float4*>(Cs + (size_t)i * n * m);
+      int k = k_lo;
+      for (; k + 4 <= k_hi; k += 4) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            const int jv = q * 32 + lane;
+            if (jv < mv) {
+              const float4 c = crow[(size_t)(k + kk) * mv + jv];
+              sacc[rr][q][0] += ex2(fmaf(-c.x, c2, gcr[rr][q][0]));
+              sacc[rr][q][1] += ex2(fmaf(-c.y, c2, gcr[rr][q][1]));
+              sacc[rr][q][2] += ex2(fmaf(-c.z, c2, gcr[rr][q][2]));
+              sacc[rr][q][3] += ex2(fmaf(-c.w, c2, gcr[rr][q][3]));
+            }
+          }
+      }
+      for (; k < k_hi; ++k)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const int jv = q * 32 + lane;
+          if (jv < mv) {
+            const float4 c = crow[(size_t)k * mv + jv];
+            sacc[rr][q][0] += ex2(fmaf(-c.x, c2, gcr[rr][q][0]));
+            sacc[rr][q][1] += ex2(fmaf(-c.y, c2, gcr[rr][q][1]));
+            sacc[rr][q][2] += ex2(fmaf(-c.z, c2, gcr[rr][q][2]));
+            sacc[rr][q][3] += ex2(fmaf(-c.w, c2, gcr[rr][q][3]));
+          }
+        }
+    }
+  };
+  for (int rr = 0; rr < MAXR; ++rr) {
+    const int i = warp + rr * nwarps;
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int jv = q * 32 + lane;
+      const float4 gv = (i < nrows && jv < mv) ? reinterpret_cast<const float4*>(Gs + (size_t)i * m)[jv]
+                                               : make_float4(0, 0, 0, 0);
+      gcr[rr][q][0] = gv.x * c2;
+      gcr[rr][q][1] = gv.y * c2;
+      gcr[rr][q][2] = gv.z * c2;
+      gcr[rr][q][3] = gv.w * c2;
+    }
+  }
+  auto zero_s = [&]() {
+#pragma unroll
+    for (int rr = 0; rr < MAXR; ++rr)
+#pragma unroll
+      for (int q = 0; q < VPL; ++q)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) sacc[rr][q][v] = 0.f;
+  };
+  const int khalf = n / 2;
+  zero_s();
+  ksum_range(0, n);                                         // k-sums of iteration 0
+  int t = 0;
+  bool stop = false;
+  for (; t < p.iters && !stop; ++t) {
+    // ================= epilogues of iteration t (z_hat of iteration t-1 is complete in the replica)
+    double P[VPL][4];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) P[q][v] = 0.0;
+    for (int rr = 0; rr < nrw && rr < MAXR; ++rr) {
+      const int i = warp + rr * nwarps;
+      if (i >= nrows) break;
+      double x[VPL][4];
+      double lmax = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int jv = q * 32 + lane;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          x[q][v] = jv < mv ? zs[4 * jv + v] - (double)Gs[(size_t)i * m + 4 * jv + v] * inv_eps
+                            : -INFINITY;
+          lmax = fmax(lmax, x[q][v]);
+        }
+      }
+      const double M = warp_max(lmax);
+      double tt[VPL][4];
+      double lsum = 0.0;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          tt[q][v] = (x[q][v] == -INFINITY) ? 0.0
+                                            : (double)sacc[rr][q][v] * (double)ex2((float)((x[q][v] - M) * COT_LOG2E));
+          lsum += tt[q][v];
+        }
+      const double r = warp_sum(lsum);
+      const double a = rstat[4 * i + 2];
+      if (lane == 0) {   // w_hat_i = log alpha_i - M_i - log r_i is formed once, after the last iteration
+        rstat[4 * i + 0] = M;
+        rstat[4 * i + 1] = r;
+      }
+      double rinv = (double)__frcp_rn((float)r);   // alpha_i / r_i: fast reciprocal + 2 Newton steps
+      rinv = rinv * fma(-r, rinv, 2.0);
+      rinv = rinv * fma(-r, rinv, 2.0);
+      const double rho = a * rinv;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) P[q][v] = fma(rho, tt[q][v], P[q][v]);
+    }
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int jv = q * 32 + lane;
+      if (jv < mv)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) wpart[(size_t)warp * m + 4 * jv + v] = P[q][v];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {   // CTA partial: warps in order
+      double acc = 0.0;
+      for (int w = 0; w < nwarps; ++w) acc += wpart[(size_t)w * m + j];
+      cpart[j] = acc;
+    }
+    // ================= B1: publish the CTA partial; stream the first half of the next k-sums meanwhile
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    const bool more = t + 1 < p.iters;
+    zero_s();
+    if (more) ksum_range(0, khalf);
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    // ================= column pass of this CTA's slice: one thread per (column, source CTA), the 8 values
+    //                   combined by a fixed xor tree (deterministic), q-update written to every replica
+    const bool need = (p.tol > 0.0 && (st.iters + 1) % p.check_every == 0) || t == p.iters - 1;
+    double dev = 0.0;
+    for (int base = 0; base < (c1 - c0) * kNCL; base += blockDim.x) {
+      const int idx = base + threadIdx.x;
+      const int jc = idx / kNCL, src = idx % kNCL;
+      const int j = c0 + jc;
+      const bool ok = jc < (c1 - c0);
+      double v = ok ? cluster.map_shared_rank(cpart, src)[j] : 0.0;
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      double zn = 0.0;
+      if (ok) {
+        const double bj = bcol[2 * j];
+        if (src == 0) {
+          dev += fabs(v - bj);
+          if (!(v >= 1e-28)) s_flags = 1;
+        }
+        zn = zs[j] + (bcol[2 * j + 1] - log(v));
+        cluster.map_shared_rank(zs, src)[j] = zn;   // lane `src` of the group writes replica `src`
+      }
+    }
+    if (need) {
+      dev = warp_sum(dev);
+      __shared__ double wdev[32];
+      if (lane == 0) wdev[warp] = dev;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double d = 0.0;
+        for (int w = 0; w < nwarps; ++w) d += wdev[w];
+        cluster.map_shared_rank(mon, 0)[crank] = d;
+      }
+    }
+    // ================= B2: the q-update is in every replica; stream the second half meanwhile
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    if (more) ksum_range(khalf, n);
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    st.iters += 1;
+    if (need) {
+      double rr = 0.0;
+      const double* m0 = cluster.map_shared_rank(mon, 0);
+      for (int cr = 0; cr < kNCL; ++cr) rr += m0[cr];
+      st.residual = rr * (double)n;
+    }
+    if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
+      st.active = 0;
+      st.converged = 1;
+      stop = true;
+    }
+  }
+  // ---- write back: w_hat of this CTA's rows (from the last epilogue), z_hat (CTA 0; replicas identical)
+  for (int i = threadIdx.x; i < nrows; i += blockDim.x)
+    if (t > 0) p.w_hat[b * m + r0 + i] = rstat[4 * i + 3] - rstat[4 * i + 0] - log(rstat[4 * i + 1]);
+  if (crank == 0) {
+    for (int j = threadIdx.x; j < m; j += blockDim.x) p.z_hat[b * m + j] = zs[j];
+  }
+  __syncthreads();
+  if (s_flags) atomicOr(&p.state[b].flags, (int)STATE_UNDERFLOW);
+  if (crank == 0 && threadIdx.x == 0) {
+    SolverState out = p.state[b];
+    out.iters = st.iters;
+    out.residual = st.residual;
+    out.active = st.active;
+    out.converged = st.converged;
+    p.state[b] = out;
+  }
+  cluster.sync();   // no CTA leaves while others may still read its shared memory
+}
+
+static size_t batch_smem_bytes(int n, int m, int RB, int nwarps) {
+  return (size_t)RB * n * m * 4 + (size_t)RB * m * 4 + (size_t)m * 8 + (size_t)nwarps * m * 8 + (size_t)m * 8 +
+         kNCL * 8 + (size_t)RB * 32 + (size_t)m * 16 + 16;
+}
+
+bool batch_cluster_eligible(const IterArgs& a) {
+  if (a.dtype != COT_F32 || a.m % 4 != 0 || a.m > 256 || a.m < kNCL || a.R != a.m || (a.flags & COT_FORCE_LDG))
+    return false;
+  const int RB = (int)((a.m + kNCL - 1) / kNCL);
+  if (RB > 32) return false;
+  return batch_smem_bytes((int)a.n, (int)a.m, RB, std::min(RB, 16)) <= 200 * 1024;
+}
+
+cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int iters, cudaStream_t s) {
+  BatchParams p;
+  p.C = static_cast<const float*>(a.C);
+  p.G = static_cast<const float*>(a.G);
+  p.alpha = a.alpha;
+  p.beta = a.beta;
+  p.w_hat = a.w_hat;
+  p.z_hat = a.z_hat;
+  p.eps = a.eps;
+  p.state = ws.state;
+  p.n = (int)a.n;
+  p.m = (int)a.m;
+  p.RB = (int)((a.m + kNCL - 1) / kNCL);
+  p.iters = iters;
+  p.tol = a.tol;
+  p.check_every = a.check_every > 0 ? a.check_every : 1;
+  const int nwarps = std::min(p.RB, 16);   // one warp per row (two rows per warp when m > 128)
+  const size_t smem = batch_smem_bytes(p.n, p.m, p.RB, nwarps);
+  void* fn = a.m <= 128 ? (void*)k_batch_cluster<1> : (void*)k_batch_cluster<2>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.B * kNCL));
+  cfg.blockDim = dim3((unsigned)(nwarps * 32));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kNCL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&p};
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+}  // namespace cot

@@ -287,3 +287,20 @@ def test_split_rows_cols_api_matches_iter():
     _compare(p, rep.cpu().numpy()[0], T.cpu().numpy(), w, z)
     it, _, _ = prob.state()
     assert it[0] == 25
+
+
+def test_cluster_path_batch_freeze_fp32():
+    """The cluster-resident path (fp32, m <= 256): per-problem freeze rule in a batch with mixed eps."""
+    p = synthetic.random_cyclic(seed=6, n=6, m=32, B=4, eps=0.1, dtype=np.float32)
+    p.eps = np.array([0.1, 0.05, 0.2, 0.08])
+    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps))
+    prob.init().iterate(4000, tol=1e-7, check_every=5)
+    T, rep = prob.plan(T_blocks=True)
+    it, conv, _ = prob.state()
+    for b in range(p.B):
+        q = p.single(b)
+        w, z, t, _ = oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, float(q.eps[0]), 4000, tol=1e-7, check_every=5,
+                                            form="kernel")
+        assert conv[b] == 1 and abs(int(it[b]) - t) <= 5
+        if it[b] == t:
+            _compare(q, rep.cpu().numpy()[b], T.cpu().numpy()[b], w, z)
