@@ -166,10 +166,12 @@ class Runner:
         self.ptr = dict(C=P(self.C), a=P(self.alpha), b=P(self.beta), e=P(self.eps), G=P(self.G), A=P(self.A),
                         w=P(self.w), z=P(self.z), ws=P(self.ws), Tb=P(self.Tb), Tf=P(self.Tfull), rep=P(self.rep))
         self.flags = int(os.environ.get("COT_BENCH_FLAGS", "0"))
+        self.pre = os.environ.get("COT_BENCH_MODE") == "precomputed"   # NEXT-1 line (separate metric)
+        self.S = torch.empty((self.B, 1, self.m, self.m), dtype=self.C.dtype, device=dev) if self.pre else None
         # the persistent TMA kernel runs all iterations in one launch (B == 1, fp32, m % 4 == 0)
         self.persistent = (self.B == 1 and self.dt == cot.COT_F32 and self.m % 4 == 0 and not (self.flags & 2))
-        self.launches_per_step = 1 + 1 + (1 if self.persistent else 2 * iters) + 3 + 1
-        self.bytes_iter = float(p.B) * (p.n + 1) * p.m * p.m * p.C.itemsize
+        self.launches_per_step = 1 + 1 + (1 if self.persistent else 2 * iters) + 3 + 1 + (1 if self.pre else 0)
+        self.bytes_iter = float(p.B) * ((2 if self.pre else p.n + 1) * p.m * p.m) * p.C.itemsize
 
     def _ck(self, code, fn):
         if code != 0:
@@ -185,8 +187,13 @@ class Runner:
             e0 = self.torch.cuda.Event(enable_timing=True)
             e1 = self.torch.cuda.Event(enable_timing=True)
             e0.record(self.stream)
-        self._ck(L.cerot_iter(q["a"], q["b"], q["C"], q["G"], B, n, m, dt, q["e"], self.iters, 0.0, 1, self.flags,
-                              q["w"], q["z"], q["ws"], wsn, s), "cerot_iter")
+        if self.pre:   # NEXT-1: S once, then O(m^2) iterations on (S, G)
+            self._ck(L.cerot_precompute(q["C"], q["G"], B, n, m, dt, q["e"], self.S.data_ptr(), s), "cerot_precompute")
+            self._ck(L.cerot_iter(q["a"], q["b"], self.S.data_ptr(), q["G"], B, 1, m, dt, q["e"], self.iters, 0.0, 1,
+                                  self.flags | 4, q["w"], q["z"], q["ws"], wsn, s), "cerot_iter")
+        else:
+            self._ck(L.cerot_iter(q["a"], q["b"], q["C"], q["G"], B, n, m, dt, q["e"], self.iters, 0.0, 1, self.flags,
+                                  q["w"], q["z"], q["ws"], wsn, s), "cerot_iter")
         if record:
             e1.record(self.stream)
             self.ev.append((e0, e1))
@@ -370,8 +377,11 @@ def run_ours(args, rank, world, local_rank):
               ("per iteration: k_iter_tma rows-only + k_colsum + ncclAllReduce + k_zupdate" if mode == "row_sharded"
                else "k_rows_ldg + k_cols (one launch pair per iteration)"))
     trf = _ncu_traffic_per_iter(args.workload) if world == 1 else None
+    metric = _metric()
+    if getattr(R, "pre", False):   # NEXT-1 is reported on its own line, never under the n*m^2 streaming metric
+        metric = "C-EROT precomputed-kernel mode (Alg. 2 as written): n*m^2-equivalent evals/s (NOT the streaming metric)"
     out = {
-        "metric": _metric(), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32" if p.C.dtype == np.float32 else "f64",
         "data": "synthetic (seeded; BASELINE.json recipe, random-rotation point clouds, no dataset)",

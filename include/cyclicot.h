@@ -58,6 +58,8 @@ typedef enum {
                                  z_hat is a warm start                                                  */
 #define COT_FORCE_LDG  0x2u   /* use the generic LDG row kernels even where the TMA (large problems)  */
                               /* or cluster-resident (small problems) kernels apply                    */
+#define COT_PRECOMPUTED 0x4u  /* NEXT-1: `C` is S from cerot_precompute ([B][1][m][m], pass n = 1); the  */
+                              /* row pass uses s_ij = S_ij instead of re-streaming the n blocks          */
 /* Diagnostic flags (results are NOT valid with them; used by scripts/ubench_iter.py only):          */
 #define COT_DIAG_NO_COMPUTE 0x100u  /* TMA kernel: consumers only acknowledge slots (pure HBM stream)    */
 #define COT_DIAG_NO_SYNC    0x200u  /* TMA kernel: skip the column pass and device-wide barriers        */
@@ -93,6 +95,12 @@ size_t cot_workspace_bytes(int64_t B, int64_t n, int64_t m, int dtype);
 /*   overwritten, not accumulated). Asynchronous; use cot_check_nonfinite to turn it into a status.   */
 int clot_aggregate(const void* C, int64_t B, int64_t n, int64_t m, int dtype,
                    void* G, int32_t* argmin, int32_t* d_nonfinite, void* stream);
+
+/* NEXT-1 (Alg. 2 line 1 as written): S[b][i][j] = sum_k exp((G_ij - C_ijk)/eps_b) in [1, n]       */
+/* (the cyclic Gibbs kernel K_ij = S_ij exp(-G_ij/eps), eq. def_Kij, kept G-shifted). Then       */
+/* cerot_iter(C = S, n = 1, flags | COT_PRECOMPUTED) runs O(m^2) iterations. Asynchronous.         */
+int cerot_precompute(const void* C, const void* G, int64_t B, int64_t n, int64_t m, int dtype, const double* eps,
+                     void* S, void* stream);
 
 /* Synchronises `stream`, reads *d_nonfinite and returns COT_E_NONFINITE if it is > 0, else COT_OK. */
 int cot_check_nonfinite(const int32_t* d_nonfinite, void* stream);

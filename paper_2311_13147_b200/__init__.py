@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libcyclicot.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "cyclicot.h")
 
 COT_F32, COT_F64 = 0, 1
-COT_COLD_START, COT_FORCE_LDG = 0x1, 0x2
+COT_COLD_START, COT_FORCE_LDG, COT_PRECOMPUTED = 0x1, 0x2, 0x4
 STATUS = {0: "COT_OK", 1: "COT_NOT_CONVERGED", -1: "COT_E_ARG", -2: "COT_E_NONFINITE", -3: "COT_E_MARGINAL",
           -4: "COT_E_CUDA", -5: "COT_E_NCCL", -6: "COT_E_WORKSPACE", -7: "COT_E_UNDERFLOW"}
 REPORT_FIELDS = ("objective", "reg_primal", "dual", "row_l1", "col_l1", "col_l2", "mass", "residual")
@@ -58,6 +58,7 @@ _SIGS = {
                                   _sz, _vp]),
     "cerot_solve": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _dbl, _i64, _i64, _u32, _vp,
                                    _vp, _vp, _vp, _sz, ctypes.POINTER(cot_report), _vp]),
+    "cerot_precompute": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp]),
     # row sharding (dist.py)
     "cot_workspace_bytes_sharded": (_sz, [_i64, _i64, _i64, ctypes.c_int]),
     "clot_aggregate_shard": (ctypes.c_int, [_vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp]),
@@ -203,6 +204,25 @@ class CerotProblem:
         _check(lib().cerot_iter(_ptr(self.alpha), _ptr(self.beta), _ptr(self.C), _ptr(self.G), self.B, self.n,
                                 self.m, self.dt, _ptr(self.eps), iters, tol, check_every, flags, _ptr(self.w_hat),
                                 _ptr(self.z_hat), _ptr(self.ws), self.ws.numel(), _stream(self.stream)), "cerot_iter")
+        return self
+
+    # ---- NEXT-1: Alg. 2 with the cyclic Gibbs kernel precomputed, O(m^2) per iteration
+    def precompute(self):
+        """S_ij = sum_k exp((G_ij - C_ijk)/eps) (cerot_precompute), kept on the device."""
+        import torch
+        shp = (self.B, 1, self.m, self.m) if self.batched else (1, self.m, self.m)
+        self.S = torch.empty(shp, dtype=self.C.dtype, device=self.C.device)
+        _check(lib().cerot_precompute(_ptr(self.C), _ptr(self.G), self.B, self.n, self.m, self.dt, _ptr(self.eps),
+                                      _ptr(self.S), _stream(self.stream)), "cerot_precompute")
+        return self
+
+    def iterate_precomputed(self, iters: int, tol: float = 0.0, check_every: int = 1, flags: int = 0):
+        if getattr(self, "S", None) is None:
+            self.precompute()
+        _check(lib().cerot_iter(_ptr(self.alpha), _ptr(self.beta), _ptr(self.S), _ptr(self.G), self.B, 1, self.m,
+                                self.dt, _ptr(self.eps), iters, tol, check_every, flags | COT_PRECOMPUTED,
+                                _ptr(self.w_hat), _ptr(self.z_hat), _ptr(self.ws), self.ws.numel(),
+                                _stream(self.stream)), "cerot_iter")
         return self
 
     def rows(self, parity: int, flags: int = 0):

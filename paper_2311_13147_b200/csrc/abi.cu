@@ -228,6 +228,15 @@ int clot_aggregate(const void* C, int64_t B, int64_t n, int64_t m, int dtype, vo
   return COT_OK;
 }
 
+int cerot_precompute(const void* C, const void* G, int64_t B, int64_t n, int64_t m, int dtype, const double* eps,
+                     void* S, void* stream) {
+  int st = check_shape(B, n, m, dtype);
+  if (st) return st;
+  if (!C || !G || !eps || !S) return arg_error("cerot_precompute: NULL argument");
+  COT_CHECK_CUDA(launch_precompute(C, G, B, n, m, dtype, eps, S, (cudaStream_t)stream));
+  return COT_OK;
+}
+
 int cot_check_nonfinite(const int32_t* d_nonfinite, void* stream) {
   if (!d_nonfinite) return arg_error("cot_check_nonfinite: NULL flag");
   int32_t h = 0;

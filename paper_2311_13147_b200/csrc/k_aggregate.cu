@@ -132,6 +132,71 @@ __global__ void __launch_bounds__(256) k_aggregate(const T* __restrict__ C, int6
   }
 }
 
+// NEXT-1 (Alg. 2 line 1, in the G-shifted form): S_ij = sum_k exp((G_ij - C_ijk)/eps) in [1, n],
+// i.e. K_ij = S_ij exp(-G_ij/eps) (eq. def_Kij) without over/underflow. One streaming pass.
+template <typename T, int V>
+__global__ void __launch_bounds__(256) k_precompute(const T* __restrict__ C, const T* __restrict__ G, int64_t B,
+                                                    int n, int64_t mm, const double* __restrict__ eps,
+                                                    T* __restrict__ S) {
+  using VT = typename Vec<T, V>::type;
+  const int64_t groups = B * mm / V;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = g * V;
+    const int64_t b = e / mm, ij = e - b * mm;
+    const VT* src = reinterpret_cast<const VT*>(C + b * n * mm + ij);
+    const int64_t kstride = mm / V;
+    const VT gv = reinterpret_cast<const VT*>(G)[g];
+    const double inv_eps = 1.0 / eps[b];
+    T gg[V], acc[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      gg[q] = lane<T, V>(gv, q);
+      acc[q] = T(0);
+    }
+    for (int k = 0; k < n; ++k) {
+      const VT v = __ldcs(src + (int64_t)k * kstride);
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        if constexpr (sizeof(T) == 4)
+          acc[q] += ex2((gg[q] - lane<T, V>(v, q)) * (float)(COT_LOG2E * inv_eps));
+        else
+          acc[q] += exp((gg[q] - lane<T, V>(v, q)) * inv_eps);
+      }
+    }
+    VT out;
+#pragma unroll
+    for (int q = 0; q < V; ++q) set_lane<T, V>(out, q, acc[q]);
+    reinterpret_cast<VT*>(S)[g] = out;
+  }
+}
+
+cudaError_t launch_precompute(const void* C, const void* G, int64_t B, int64_t n, int64_t m, int dtype,
+                              const double* eps, void* S, cudaStream_t s) {
+  const int64_t mm = m * m;
+  const int sms = device_sm_count();
+  auto grid_for = [&](int64_t groups) {
+    int64_t g = (groups + 255) / 256;
+    const int64_t cap = (int64_t)sms * 8;
+    return (int)(g < cap ? (g > 0 ? g : 1) : cap);
+  };
+  if (dtype == COT_F32) {
+    if (mm % 4 == 0)
+      k_precompute<float, 4><<<grid_for(B * mm / 4), 256, 0, s>>>((const float*)C, (const float*)G, B, (int)n, mm, eps,
+                                                                  (float*)S);
+    else
+      k_precompute<float, 1><<<grid_for(B * mm), 256, 0, s>>>((const float*)C, (const float*)G, B, (int)n, mm, eps,
+                                                              (float*)S);
+  } else {
+    if (mm % 2 == 0)
+      k_precompute<double, 2><<<grid_for(B * mm / 2), 256, 0, s>>>((const double*)C, (const double*)G, B, (int)n, mm,
+                                                                   eps, (double*)S);
+    else
+      k_precompute<double, 1><<<grid_for(B * mm), 256, 0, s>>>((const double*)C, (const double*)G, B, (int)n, mm, eps,
+                                                               (double*)S);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_aggregate(const void* C, int64_t B, int64_t n, int64_t m, int dtype, void* G, int32_t* A,
                              int32_t* nonfinite, cudaStream_t s, int64_t R) {
   const int64_t mm = (R < 0 ? m : R) * m;   // elements per block (R rows of m columns)

@@ -41,6 +41,7 @@ struct BatchParams {
   int iters;
   double tol;
   long long check_every;
+  int pre;               // precomputed mode (NEXT-1): C is S [B][1][m][m], s_ij = S_ij
 };
 
 template <int VPL>
@@ -114,6 +115,21 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
       const int i = warp + rr * nwarps;
       if (i >= nrows) break;
       const float4* crow = reinterpret_cast<const float4*>(Cs + (size_t)i * n * m);
+      if (p.pre) {   // NEXT-1: the row holds S_ij (n = 1); the k range is empty or [0, 1)
+        if (k_lo < k_hi)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            const int jv = q * 32 + lane;
+            if (jv < mv) {
+              const float4 c = crow[jv];
+              sacc[rr][q][0] = c.x;
+              sacc[rr][q][1] = c.y;
+              sacc[rr][q][2] = c.z;
+              sacc[rr][q][3] = c.w;
+            }
+          }
+        continue;
+      }
       int k = k_lo;
       for (; k + 4 <= k_hi; k += 4) {
 #pragma unroll
@@ -337,6 +353,7 @@ cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int ite
   p.iters = iters;
   p.tol = a.tol;
   p.check_every = a.check_every > 0 ? a.check_every : 1;
+  p.pre = (a.flags & COT_PRECOMPUTED) ? 1 : 0;
   const int nwarps = std::min(p.RB, 16);   // one warp per row (two rows per warp when m > 128)
   const size_t smem = batch_smem_bytes(p.n, p.m, p.RB, nwarps);
   void* fn = a.m <= 128 ? (void*)k_batch_cluster<1> : (void*)k_batch_cluster<2>;

@@ -51,6 +51,7 @@ struct RowParams {
   int64_t n, m, R, row_begin, rpu, upp, U;
   double* partials;      // [U][m]
   const SolverState* state;
+  int pre;               // precomputed mode: C is S_ij = sum_k exp((G_ij - C_ijk)/eps) (n = 1), s = S
 };
 
 __device__ __forceinline__ double blk_sum(double v, double* sh) {
@@ -117,6 +118,18 @@ __global__ void __launch_bounds__(256) k_rows_ldg(RowParams p) {
       }
       // ---- streamed k-sum: the n*m^2 Gibbs-kernel evaluations of this iteration
       int64_t k = 0;
+      if (p.pre) {   // NEXT-1 (Alg. 2 line 1 as written): s_ij was computed once by cerot_precompute
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          const int64_t jv = (int64_t)q * NT + threadIdx.x;
+          VT cvv = jv < mv ? __ldg(Crow + jv) : VT{};
+          T c[V];
+          VecL<T, V>::unpack(cvv, c);
+#pragma unroll
+          for (int v = 0; v < V; ++v) s[q][v] = c[v];
+        }
+        k = p.n;
+      }
       for (; k + KU <= p.n; k += KU) {
         VT cv[KU][CPT];
 #pragma unroll
@@ -343,6 +356,7 @@ cudaError_t launch_rows(const IterArgs& a, const Workspace& ws, const UnitPlan& 
   rp.U = up.U;
   rp.partials = ws.partials[parity];
   rp.state = ws.state;
+  rp.pre = (a.flags & COT_PRECOMPUTED) ? 1 : 0;
   if (a.dtype == COT_F32) {
     if (a.m % 4 == 0) return rows_dispatch<float, 4>(rp, up.grid, a.m, s);
     return rows_dispatch<float, 1>(rp, up.grid, a.m, s);

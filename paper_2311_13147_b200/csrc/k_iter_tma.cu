@@ -53,6 +53,7 @@ struct TmaParams {
   int nk, ne, qn;        // k-sum warps, epilogue warps, row-queue depth
   int evict_last_rows;   // rows [0, evict_last_rows) of every block are streamed with an L2 evict_last hint
   int diag;              // COT_DIAG_* bits (diagnostics only)
+  int pre;               // precomputed mode (NEXT-1): C is S [R][m] (n = 1) and s_ij = S_ij
   unsigned long long* trace;   // diagnostics: [grid][8] cycle counters, or nullptr
 };
 
@@ -419,7 +420,16 @@ __global__ void __launch_bounds__(448, 1) k_iter_tma(TmaParams p) {
       for (; k0 + KS <= n; k0 += KS) {
         mbar_wait(&full[slot], phase);
         const VT* sb = reinterpret_cast<const VT*>(ring + (size_t)slot * slot_floats);
-        if (!(p.diag & COT_DIAG_NO_COMPUTE)) {
+        if (p.pre) {   // NEXT-1: the slot holds S_ij (n = KS = 1)
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            const float4 c = sb[q * nkt + kt];
+            s[q][0] = c.x;
+            s[q][1] = c.y;
+            s[q][2] = c.z;
+            s[q][3] = c.w;
+          }
+        } else if (!(p.diag & COT_DIAG_NO_COMPUTE)) {
 #pragma unroll
           for (int q2 = 0; q2 < KS; ++q2) {
 #pragma unroll
@@ -737,6 +747,7 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
   p.bar = ws.grid_bar;
   p.evict_last_rows = 0;
   p.diag = (int)(a.flags & (COT_DIAG_NO_COMPUTE | COT_DIAG_NO_SYNC));
+  p.pre = (a.flags & COT_PRECOMPUTED) ? 1 : 0;
   if (const char* ev = getenv("COT_EVICT_LAST_ROWS")) p.evict_last_rows = atoi(ev);   // L2 residency experiment
   p.trace = nullptr;
   static unsigned long long* trace_buf = nullptr;   // diagnostics only (COT_TRACE=1)

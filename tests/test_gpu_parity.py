@@ -304,3 +304,33 @@ def test_cluster_path_batch_freeze_fp32():
         assert conv[b] == 1 and abs(int(it[b]) - t) <= 5
         if it[b] == t:
             _compare(q, rep.cpu().numpy()[b], T.cpu().numpy()[b], w, z)
+
+
+@pytest.mark.parametrize("maker,path", [(lambda: synthetic.c2_ring(eps_factor=1e-2), "cluster"),
+                                        (lambda: synthetic.c2_ring(eps_factor=1e-2), "ldg"),
+                                        (lambda: synthetic.c4_large(m=512, n=32), "tma"),
+                                        (lambda: synthetic.c1_tiny(), "ldg"),
+                                        (lambda: synthetic.c5_batched(B=3, first=11), "cluster")])
+def test_precomputed_mode_matches_alg2(maker, path):
+    """NEXT-1: Alg. 2 as written (K precomputed once; O(m^2) per iteration) against the oracle's
+    precomputed-K form, iterate for iterate; S itself against the oracle's log K (G-shifted)."""
+    p = maker()
+    iters = 150
+    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps)).init()
+    prob.precompute()
+    for b in range(p.B):
+        q = p.single(b)
+        Go, _ = oracle.aggregate(q.C)
+        logK = oracle.lse(-np.asarray(q.C, np.float64) / float(q.eps[0]), axis=0)
+        S_ref = np.exp(logK + Go.astype(np.float64) / float(q.eps[0]))     # S = K e^{G/eps} in [1, n]
+        S_g = prob.S.cpu().numpy().reshape(p.B, p.m, p.m)[b].astype(np.float64)
+        assert np.abs(S_g / S_ref - 1).max() < (1e-12 if q.C.dtype == np.float64 else 2e-6)
+    prob.iterate_precomputed(iters, flags=cot.COT_FORCE_LDG if path == "ldg" else 0)
+    T, rep = prob.plan(T_blocks=True)
+    T = T.cpu().numpy().reshape((p.B,) + p.C.shape[-3:])
+    rep = rep.cpu().numpy()
+    for b in range(p.B):
+        q = p.single(b)
+        w, z, _, _ = oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, float(q.eps[0]), iters, form="kernel")
+        fp64 = q.C.dtype == np.float64
+        _compare(q, rep[b], T[b], w, z, obj_rtol=1e-10 if fp64 else 1e-6, l1_tol=1e-10 if fp64 else 1e-5)
