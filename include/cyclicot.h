@@ -218,6 +218,21 @@ int cerot_plan_sharded(const double* alpha, const double* beta, const void* C_lo
                        const double* w_hat, const double* z_hat, void* T_local, double* d_report,
                        void* workspace, size_t ws_bytes, void* comm, void* stream);
 
+/* ---------------------------------------------------------------------------------------------- */
+/* NEXT-3: C-SROT, strongly convex regularised OT through the 2m-variable Fenchel dual        */
+/* (Theorem 2) by alternating maximisation: each sweep solves every w_i with z fixed, then     */
+/* every z_j with w fixed, by safeguarded Newton on the monotone derivative; the plan is      */
+/* T_ijk = (phi*)'(w_i + z_j - C_ijk). Regulariser COT_REG_SQUARED: phi(x) = x^2/(2 gamma)    */
+/* for x >= 0, (phi*)'(y) = gamma max(y, 0) (sparse plans). reg_param: DEVICE [B] gamma. w, z: DEVICE      */
+/* [B][m] fp64 in cost units (not eps-scaled); cold start z = 0 with COT_COLD_START. Stops when the       */
+/* monitor n*sum_j|c_j - beta_j| (plan after the w-step) <= tol, checked every check_every sweeps, or    */
+/* after max_sweeps. report: HOST [B]. Synchronises.                                                      */
+typedef enum { COT_REG_ENTROPIC = 0, COT_REG_SQUARED = 1 } cot_reg;
+int csrot_solve(const double* alpha, const double* beta, const void* C, int64_t B, int64_t n, int64_t m, int dtype,
+                int reg, const double* reg_param, double tol, int64_t max_sweeps, int64_t check_every,
+                uint32_t flags, double* w, double* z, void* T_blocks, void* workspace, size_t ws_bytes,
+                cot_report* report, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,3 +11,4 @@ DESIGN.md §3; no function here is "parity unpinned" except the Table 1/2 absolu
 from .core import *        # noqa: F401,F403
 from .lot import *         # noqa: F401,F403
 from .sinkhorn import *    # noqa: F401,F403
+from .srot import *        # noqa: F401,F403

@@ -58,6 +58,8 @@ _SIGS = {
                                   _sz, _vp]),
     "cerot_solve": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _dbl, _i64, _i64, _u32, _vp,
                                    _vp, _vp, _vp, _sz, ctypes.POINTER(cot_report), _vp]),
+    "csrot_solve": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp, _dbl, _i64, _i64,
+                                   _u32, _vp, _vp, _vp, _vp, _sz, ctypes.POINTER(cot_report), _vp]),
     "cerot_precompute": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp]),
     # row sharding (dist.py)
     "cot_workspace_bytes_sharded": (_sz, [_i64, _i64, _i64, ctypes.c_int]),
@@ -283,3 +285,32 @@ def cerot_solve(C, alpha, beta, eps, tol=0.0, max_iter=1000, check_every=1, T_bl
         d.update(iters=r.iters, converged=bool(r.converged), status=STATUS[r.status])
         out.append(d)
     return w_hat, z_hat, T, out
+
+
+COT_REG_SQUARED = 1
+
+
+def csrot_solve(C, alpha, beta, gamma, tol=0.0, max_sweeps=1000, check_every=1, T_blocks=False, stream=None):
+    """NEXT-3: C-SROT with the squared regulariser on the device. Returns (w, z, T or None,
+    [report dict]); w, z in cost units."""
+    import torch
+    B, n, m, batched = _shape(C)
+    dt = _dtype_code(C)
+    alpha = alpha.to(torch.float64).contiguous()
+    beta = beta.to(torch.float64).contiguous()
+    gam = torch.as_tensor(gamma, dtype=torch.float64, device=C.device).reshape(-1).expand(B).contiguous()
+    w = torch.zeros_like(alpha)
+    z = torch.zeros_like(beta)
+    ws = workspace(B, n, m, dt, C.device)
+    T = torch.empty_like(C) if T_blocks else None
+    reps = (cot_report * B)()
+    code = lib().csrot_solve(_ptr(alpha), _ptr(beta), _ptr(C), B, n, m, dt, COT_REG_SQUARED, _ptr(gam), tol,
+                             max_sweeps, check_every, COT_COLD_START, _ptr(w), _ptr(z), _ptr(T), _ptr(ws), ws.numel(),
+                             reps, _stream(stream))
+    _check(code, "csrot_solve", ok=(0, 1))
+    out = []
+    for r in reps:
+        d = {f: getattr(r, f) for f in REPORT_FIELDS}
+        d.update(iters=r.iters, converged=bool(r.converged), status=STATUS[r.status])
+        out.append(d)
+    return w, z, T, out

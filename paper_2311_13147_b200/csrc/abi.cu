@@ -70,6 +70,7 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, i
   w.c_local = reinterpret_cast<double*>(take((size_t)(B * m) * 8));
   w.c_global = reinterpret_cast<double*>(take((size_t)(B * m) * 8));
   w.plan_buf = reinterpret_cast<double*>(take((size_t)(B * (kPlanBufHead + m)) * 8));
+  w.rowscal = reinterpret_cast<double*>(take((size_t)(B * m * 4) * 8));
   w.A = reinterpret_cast<int32_t*>(take((size_t)(B * R * m) * 4));
   w.G = take((size_t)(B * R * m) * esz);
   if (ws) *ws = w;
@@ -419,6 +420,67 @@ int cerot_solve(const double* alpha, const double* beta, const void* C, int64_t 
   }
   st = plan_and_report(a, ws, T_blocks, ws.report, nullptr, s);
   if (st) return st;
+  std::vector<double> rep((size_t)B * kReportDoubles);
+  COT_CHECK_CUDA(cudaMemcpyAsync(rep.data(), ws.report, rep.size() * 8, cudaMemcpyDeviceToHost, s));
+  st = cerot_state(workspace, B, m, n, dtype, it.data(), conv.data(), res.data(), stream);
+  if (st) return st;
+  bool all_conv = true;
+  for (int64_t b = 0; b < B; ++b) {
+    cot_report& r = report[b];
+    const double* d = rep.data() + b * kReportDoubles;
+    r.objective = d[0];
+    r.reg_primal = d[1];
+    r.dual = d[2];
+    r.row_l1 = d[3];
+    r.col_l1 = d[4];
+    r.col_l2 = d[5];
+    r.mass = d[6];
+    r.residual = d[7];
+    r.iters = it[(size_t)b];
+    r.converged = conv[(size_t)b];
+    r.status = (tol > 0.0 && !conv[(size_t)b]) ? COT_NOT_CONVERGED : COT_OK;
+    all_conv = all_conv && (r.status == COT_OK);
+  }
+  return all_conv ? COT_OK : COT_NOT_CONVERGED;
+}
+
+// ------------------------------------------------------------------------------------- NEXT-3: C-SROT
+int csrot_solve(const double* alpha, const double* beta, const void* C, int64_t B, int64_t n, int64_t m, int dtype,
+                int reg, const double* reg_param, double tol, int64_t max_sweeps, int64_t check_every, uint32_t flags,
+                double* w, double* z, void* T_blocks, void* workspace, size_t ws_bytes, cot_report* report,
+                void* stream) {
+  int st = check_shape(B, n, m, dtype);
+  if (st) return st;
+  if (reg != COT_REG_SQUARED) return arg_error("csrot_solve: only COT_REG_SQUARED here (entropic: cerot_solve)");
+  if (!alpha || !beta || !C || !reg_param || !w || !z || !report) return arg_error("csrot_solve: NULL argument");
+  if (max_sweeps < 0 || tol < 0) return arg_error("csrot_solve: max_sweeps >= 0 and tol >= 0 required");
+  Workspace ws;
+  st = check_ws(workspace, ws_bytes, B, n, m, m, dtype, &ws);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (check_every < 1) check_every = 1;
+  COT_CHECK_CUDA(launch_aggregate(C, B, n, m, dtype, ws.G, ws.A, ws.nonfinite, s));   // finiteness check
+  st = cot_check_nonfinite(ws.nonfinite, stream);
+  if (st) return st;
+  COT_CHECK_CUDA(launch_init(alpha, beta, B, m, flags, z, ws, s));
+  const IterArgs a = make_args(alpha, beta, C, nullptr, B, n, m, dtype, nullptr, tol, check_every, flags, w, z);
+  std::vector<int64_t> it((size_t)B);
+  std::vector<int32_t> conv((size_t)B);
+  std::vector<double> res((size_t)B);
+  int64_t done = 0;
+  while (done < max_sweeps) {
+    const int64_t chunk = std::min<int64_t>(check_every, max_sweeps - done);
+    for (int64_t t = 0; t < chunk; ++t) COT_CHECK_CUDA(launch_srot_sweep(a, reg_param, ws, s));
+    done += chunk;
+    if (tol > 0.0) {
+      st = cerot_state(workspace, B, m, n, dtype, it.data(), conv.data(), res.data(), stream);
+      if (st) return st;
+      bool all = true;
+      for (int64_t b = 0; b < B && all; ++b) all = conv[(size_t)b] != 0;
+      if (all) break;
+    }
+  }
+  COT_CHECK_CUDA(launch_srot_plan(a, reg_param, ws, T_blocks, ws.report, s));
   std::vector<double> rep((size_t)B * kReportDoubles);
   COT_CHECK_CUDA(cudaMemcpyAsync(rep.data(), ws.report, rep.size() * 8, cudaMemcpyDeviceToHost, s));
   st = cerot_state(workspace, B, m, n, dtype, it.data(), conv.data(), res.data(), stream);

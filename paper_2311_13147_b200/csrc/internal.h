@@ -47,6 +47,7 @@ struct Workspace {
   double* c_local;         // [B][m] column sums over the held rows (sharded path)
   double* c_global;        // [B][m] column sums after the cross-GPU reduction
   double* plan_buf;        // [B][kPlanBufHead + m] local plan reductions (allreduced in place)
+  double* rowscal;         // [B][m][4] per-row plan scalars of the C-SROT report
 };
 // Lays the workspace out from `base` (may be NULL to only size it). Returns the byte count. R = rows held
 // per problem (m unless row-sharded).
@@ -97,6 +98,10 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
                             cudaStream_t s);
 // Plan pass over the held rows: T blocks (optional) + unit partials in the workspace (no finalisation).
 cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& up, void* T_blocks, cudaStream_t s);
+// NEXT-3 C-SROT (squared regulariser): one alternating-maximisation sweep (w-step, z-step + monitor), plan.
+cudaError_t launch_srot_sweep(const IterArgs& a, const double* gam, const Workspace& ws, cudaStream_t s);
+cudaError_t launch_srot_plan(const IterArgs& a, const double* gam, const Workspace& ws, void* T_blocks,
+                             double* report, cudaStream_t s);
 cudaError_t launch_colsum(const Workspace& ws, const UnitPlan& up, int64_t B, int64_t m, int parity, double* c,
                           cudaStream_t s);
 cudaError_t launch_zupdate(const double* c, const double* beta, int64_t B, int64_t m, int64_t n, double tol,
