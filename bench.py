@@ -244,8 +244,12 @@ class ShardedRunner:
         self.p, self.iters, self.stream = p, iters, stream
         self.B, self.n, self.m = 1, p.n, p.m
         self.row_begin, self.R = cdist.row_partition(p.m, world, rank)
+        # fused (default): the exchange inside the persistent kernel over peer-mapped buffers (cerot_iter_fused);
+        # COT_SHARD_IMPL=nccl: the baseline, one ncclAllReduce + 3 launches per iteration (cerot_iter_sharded)
+        self.fused = os.environ.get("COT_SHARD_IMPL", "fused") == "fused"
         with stdout_to_stderr():
             self.comm = cdist.NcclComm()
+            self.xchg = cdist.PeerExchange(p.m) if self.fused else None
         Cl = np.ascontiguousarray(p.C[:, self.row_begin:self.row_begin + self.R, :])
         self.Cl_host = Cl
         self.sh = cdist.ShardedCerot(torch.as_tensor(Cl, device=dev), torch.as_tensor(p.alpha, device=dev),
@@ -257,8 +261,8 @@ class ShardedRunner:
         self.rep = torch.empty(8, dtype=torch.float64, device=dev)
         self.nf = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ev = []
-        self.persistent = False
-        self.launches_per_step = 1 + 1 + 3 * iters + 3 + 1
+        self.persistent = self.fused
+        self.launches_per_step = 1 + 1 + (1 if self.fused else 3 * iters) + 3 + 1
         self.bytes_iter = float(p.n + 1) * self.R * p.m * p.C.itemsize
         q = lambda t: t.data_ptr()
         self.q = dict(C=q(self.sh.C), G=q(self.sh.G), A=q(self.sh.argmin), a=q(self.sh.alpha), b=q(self.sh.beta),
@@ -279,9 +283,14 @@ class ShardedRunner:
             e0 = self.torch.cuda.Event(enable_timing=True)
             e1 = self.torch.cuda.Event(enable_timing=True)
             e0.record(self.stream)
-        self._ck(L.cerot_iter_sharded(q["a"], q["b"], q["C"], q["G"], n, m, self.row_begin, R, dt, q["e"], self.iters,
-                                      0.0, 1, 0, q["w"], q["z"], q["ws"], wsn, self.comm.handle, s),
-                 "cerot_iter_sharded")
+        if self.fused:
+            self._ck(L.cerot_iter_fused(q["a"], q["b"], q["C"], q["G"], n, m, self.row_begin, R, dt, q["e"],
+                                        self.iters, 0.0, 1, 0, q["w"], q["z"], q["ws"], wsn, self.xchg.world,
+                                        self.xchg.rank, self.xchg.xbufs, s), "cerot_iter_fused")
+        else:
+            self._ck(L.cerot_iter_sharded(q["a"], q["b"], q["C"], q["G"], n, m, self.row_begin, R, dt, q["e"],
+                                          self.iters, 0.0, 1, 0, q["w"], q["z"], q["ws"], wsn, self.comm.handle, s),
+                     "cerot_iter_sharded")
         if record:
             e1.record(self.stream)
             self.ev.append((e0, e1))
@@ -373,9 +382,13 @@ def run_ours(args, rank, world, local_rank):
     per_launch_ms = it_mean if R.persistent else it_mean / iters
     achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
     dom_share = it_mean / ms_step
-    kernel = ("k_iter_tma (persistent: all iterations in one launch)" if R.persistent else
-              ("per iteration: k_iter_tma rows-only + k_colsum + ncclAllReduce + k_zupdate" if mode == "row_sharded"
-               else "k_rows_ldg + k_cols (one launch pair per iteration)"))
+    if mode == "row_sharded":
+        kernel = ("k_iter_tma fused (persistent, all iterations in one launch per rank; column sums exchanged "
+                  "in-kernel through peer-mapped LL lines)" if R.fused else
+                  "per iteration: k_iter_tma rows-only + k_colsum + ncclAllReduce + k_zupdate")
+    else:
+        kernel = ("k_iter_tma (persistent: all iterations in one launch)" if R.persistent else
+                  "k_rows_ldg + k_cols (one launch pair per iteration)")
     trf = _ncu_traffic_per_iter(args.workload) if world == 1 else None
     metric = _metric()
     if getattr(R, "pre", False):   # NEXT-1 is reported on its own line, never under the n*m^2 streaming metric
@@ -392,7 +405,10 @@ def run_ours(args, rank, world, local_rank):
                    "l2": f"inputs ({p.C.nbytes * (world if mode == 'row_sharded' else 1) / 1e6:.0f} MB of cost) "
                          f"larger than L2 (126 MB) at N=1: no flush",
                    "parallelism": {"single": "rows over the SMs of one GPU",
-                                   "row_sharded": f"rows over {world} GPUs, 1 ncclAllReduce (m fp64) per iteration",
+                                   "row_sharded": (f"rows over {world} GPUs, in-kernel exchange of the m column sums "
+                                                   f"per iteration over NVLink peer memory" if getattr(R, "fused", False)
+                                                   else f"rows over {world} GPUs, 1 ncclAllReduce (m fp64) per "
+                                                        f"iteration"),
                                    "problem_sharded": f"problems over {world} GPUs, no collective"}[mode]},
         "roofline": {"bound": "hbm", "kernel": kernel,
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -411,6 +427,8 @@ def run_ours(args, rank, world, local_rank):
         out["cpu_baseline"] = cpu_baseline(p, args)
     out["clocks"] = clk.summary()
     if mode == "row_sharded":
+        if R.xchg is not None:
+            R.xchg.close()
         R.comm.close()
     return out
 

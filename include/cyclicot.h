@@ -50,7 +50,8 @@ typedef enum {
   COT_E_CUDA = -4,         /* a CUDA runtime error (message in cot_last_error)                         */
   COT_E_NCCL = -5,         /* an NCCL error in the sharded path                                        */
   COT_E_WORKSPACE = -6,    /* ws_bytes < cot_workspace_bytes(...) or misaligned workspace              */
-  COT_E_UNDERFLOW = -7     /* a column sum fell below 1e-28 in the fp32 path (eps too small)*/
+  COT_E_UNDERFLOW = -7,    /* a column sum fell below 1e-28 in the fp32 path (eps too small)*/
+  COT_E_PEER = -8          /* fused multi-GPU path: a peer rank's exchange line did not arrive in 20 s */
 } cot_status;
 
 /* Flags for cerot_* */
@@ -217,6 +218,47 @@ int cerot_plan_sharded(const double* alpha, const double* beta, const void* C_lo
                        int64_t n, int64_t m, int64_t row_begin, int64_t R, int dtype, const double* eps,
                        const double* w_hat, const double* z_hat, void* T_local, double* d_report,
                        void* workspace, size_t ws_bytes, void* comm, void* stream);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* Fused row sharding: the same partition and arithmetic as cerot_iter_sharded, but the    */
+/* exchange step runs INSIDE the persistent iteration kernel (one cooperative launch per rank for all     */
+/* `iters` iterations): after the local row pass of iteration t (Alg. 2 line 4), CTA b of every    */
+/* rank writes its rank's column sums of column slice b straight into every rank's exchange buffer over  */
+/* NVLink (peer-mapped CUDA IPC memory; 16-byte LL lines carrying the iteration's generation, no fence), */
+/* then reads all ranks' lines of slice b from its own buffer and sums them in rank order, so c_j and the */
+/* q-update (Alg. 2 line 5) are bitwise identical on every rank. No NCCL call and no host          */
+/* round trip per iteration. Requirements: fp32 C, m % 4 == 0, m <= 1024, nranks <= COT_MAX_RANKS, a     */
+/* balanced contiguous row partition (R = floor or ceil of m / nranks), every rank launching the same     */
+/* `iters` (a peer that never arrives makes the call's state report COT_E_PEER after 20 s).              */
+#define COT_MAX_RANKS 8
+/* Bytes of one rank's exchange buffer: a 256-byte header (the iteration epoch) + [2][nranks][m] lines.  */
+size_t cot_xchg_bytes(int64_t m, int nranks);
+/* Allocates and zeroes this rank's exchange buffer (cudaMalloc on the current device; the library owns  */
+/* it until cot_xchg_free) and, if ipc_handle != NULL, writes its 64-byte cudaIpcMemHandle (HOST) for the */
+/* other ranks.                                                                                           */
+int cot_xchg_alloc(int64_t m, int nranks, void** xbuf, void* ipc_handle);
+/* Maps another rank's exchange buffer (64-byte handle from its cot_xchg_alloc) into this process with    */
+/* peer access; release with cot_xchg_close. Never call it on this rank's own handle.                     */
+int cot_xchg_open(const void* ipc_handle, void** peer_xbuf);
+int cot_xchg_close(void* peer_xbuf);
+int cot_xchg_free(void* xbuf);
+/* `iters` fused iterations of this rank. xbufs: HOST array [nranks] of DEVICE pointers, rank q's         */
+/* exchange buffer as addressed by this process (xbufs[rank] = own buffer). Other arguments and the       */
+/* state / potentials as cerot_iter_sharded; cerot_init first (per rank). Asynchronous.                  */
+int cerot_iter_fused(const double* alpha, const double* beta, const void* C_local, const void* G_local,
+                     int64_t n, int64_t m, int64_t row_begin, int64_t R, int dtype, const double* eps,
+                     int64_t iters, double tol, int64_t check_every, uint32_t flags, double* w_hat,
+                     double* z_hat, void* workspace, size_t ws_bytes, int nranks, int rank, void* const* xbufs,
+                     void* stream);
+/* Emulation on ONE GPU (the recipe for testing a multi-rank protocol without the GPUs): all `nranks`    */
+/* ranks' fused iterations in ONE cooperative launch, each virtual rank on 1/nranks of the SMs with its   */
+/* own shard, workspace, potentials and exchange buffer (all on this device). Every per-rank argument is  */
+/* a HOST array [nranks]; alpha, beta, eps are shared.                                                   */
+int cerot_iter_fused_emulated(int nranks, const double* alpha, const double* beta, const void* const* C_local,
+                              const void* const* G_local, int64_t n, int64_t m, const int64_t* row_begin,
+                              const int64_t* R, int dtype, const double* eps, int64_t iters, double tol,
+                              int64_t check_every, uint32_t flags, double* const* w_hat, double* const* z_hat,
+                              void* const* workspace, const size_t* ws_bytes, void* const* xbufs, void* stream);
 
 /* ---------------------------------------------------------------------------------------------- */
 /* NEXT-3: C-SROT, strongly convex regularised OT through the 2m-variable Fenchel dual        */

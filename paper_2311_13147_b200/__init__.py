@@ -21,7 +21,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "cyclicot.h")
 COT_F32, COT_F64 = 0, 1
 COT_COLD_START, COT_FORCE_LDG, COT_PRECOMPUTED = 0x1, 0x2, 0x4
 STATUS = {0: "COT_OK", 1: "COT_NOT_CONVERGED", -1: "COT_E_ARG", -2: "COT_E_NONFINITE", -3: "COT_E_MARGINAL",
-          -4: "COT_E_CUDA", -5: "COT_E_NCCL", -6: "COT_E_WORKSPACE", -7: "COT_E_UNDERFLOW"}
+          -4: "COT_E_CUDA", -5: "COT_E_NCCL", -6: "COT_E_WORKSPACE", -7: "COT_E_UNDERFLOW", -8: "COT_E_PEER"}
 REPORT_FIELDS = ("objective", "reg_primal", "dual", "row_l1", "col_l1", "col_l2", "mass", "residual")
 
 
@@ -75,6 +75,21 @@ _SIGS = {
                                           _i64, _u32, _vp, _vp, _vp, _sz, _vp, _vp]),
     "cerot_plan_sharded": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp,
                                           _vp, _vp, _vp, _sz, _vp, _vp]),
+    # fused row sharding (in-kernel peer exchange; dist.py)
+    "cot_xchg_bytes": (_sz, [_i64, ctypes.c_int]),
+    "cot_xchg_alloc": (ctypes.c_int, [_i64, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), _vp]),
+    "cot_xchg_open": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_void_p)]),
+    "cot_xchg_close": (ctypes.c_int, [_vp]),
+    "cot_xchg_free": (ctypes.c_int, [_vp]),
+    "cerot_iter_fused": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl,
+                                        _i64, _u32, _vp, _vp, _vp, _sz, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_void_p), _vp]),
+    "cerot_iter_fused_emulated": (ctypes.c_int, [ctypes.c_int, _vp, _vp, ctypes.POINTER(ctypes.c_void_p),
+                                                 ctypes.POINTER(ctypes.c_void_p), _i64, _i64, ctypes.POINTER(_i64),
+                                                 ctypes.POINTER(_i64), ctypes.c_int, _vp, _i64, _dbl, _i64, _u32,
+                                                 ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                                                 ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_sz),
+                                                 ctypes.POINTER(ctypes.c_void_p), _vp]),
 }
 
 

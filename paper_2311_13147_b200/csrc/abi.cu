@@ -64,6 +64,16 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, i
   w.nonfinite = reinterpret_cast<int32_t*>(take(4));
   w.report = reinterpret_cast<double*>(take((size_t)B * kReportDoubles * 8));
   w.resid_part = reinterpret_cast<double*>(take((size_t)std::max<int64_t>(B * ntiles, sm_count) * 8));
+  if (B == 1) {   // LL lines of the persistent kernel
+    const size_t o0 = off;
+    w.lepoch = reinterpret_cast<unsigned long long*>(take(256));
+    w.zlines = reinterpret_cast<uint4*>(take((size_t)m * 16));
+    w.rlines = reinterpret_cast<uint4*>(take((size_t)2 * sm_count * 16));
+    w.plines = reinterpret_cast<uint4*>(take((size_t)2 * sm_count * m * 16));
+    w.lcap = sm_count;
+    w.ll_base = base ? static_cast<char*>(base) + o0 : nullptr;
+    w.ll_bytes = off - o0;
+  }
   w.plan_scal = reinterpret_cast<double*>(take((size_t)up.U * kPlanScalars * 8));
   w.partials[0] = reinterpret_cast<double*>(take((size_t)(up.U * m) * 8));
   w.partials[1] = reinterpret_cast<double*>(take((size_t)(up.U * m) * 8));
@@ -271,6 +281,11 @@ int cerot_init(const double* alpha, const double* beta, int64_t B, int64_t m, ui
     return COT_E_WORKSPACE;
   }
   carve_workspace(workspace, B, 1, m, m, COT_F32, device_sm_count(), &ws);
+  if (ws.ll_base && static_cast<char*>(ws.ll_base) + ws.ll_bytes > static_cast<char*>(workspace) + ws_bytes) {
+    set_error("workspace too small");
+    return COT_E_WORKSPACE;
+  }
+  if (ws.ll_base) COT_CHECK_CUDA(cudaMemsetAsync(ws.ll_base, 0, ws.ll_bytes, (cudaStream_t)stream));
   COT_CHECK_CUDA(launch_init(alpha, beta, B, m, flags, z_hat, ws, (cudaStream_t)stream));
   return COT_OK;
 }
@@ -356,6 +371,10 @@ int cerot_state(const void* workspace, int64_t B, int64_t m, int64_t n, int dtyp
   if (flags & STATE_UNDERFLOW) {
     set_error("a column sum fell below 1e-28 (fp32 underflow; eps too small for this cost scale)");
     return COT_E_UNDERFLOW;
+  }
+  if (flags & STATE_PEER_TIMEOUT) {
+    set_error("fused multi-GPU path: a peer rank's exchange line did not arrive within 20 s");
+    return COT_E_PEER;
   }
   return COT_OK;
 }
@@ -628,6 +647,118 @@ int cerot_iter_sharded(const double* alpha, const double* beta, const void* C_lo
     }
     COT_CHECK_CUDA(launch_zupdate(c, beta, 1, m, n, tol, check_every, z_hat, ws, s));
   }
+  return COT_OK;
+}
+
+// ------------------------------------------------------------------------------ fused row sharding
+size_t cot_xchg_bytes(int64_t m, int nranks) {
+  if (m < 1 || nranks < 1 || nranks > kMaxRanks) return 0;
+  return kXchgHeader + (size_t)2 * nranks * m * sizeof(uint4);
+}
+
+int cot_xchg_alloc(int64_t m, int nranks, void** xbuf, void* ipc_handle) {
+  const size_t bytes = cot_xchg_bytes(m, nranks);
+  if (!bytes || !xbuf) return arg_error("cot_xchg_alloc: need m >= 1, 1 <= nranks <= COT_MAX_RANKS, xbuf");
+  void* p = nullptr;
+  COT_CHECK_CUDA(cudaMalloc(&p, bytes));
+  cudaError_t e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && ipc_handle) {
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    e = cudaIpcGetMemHandle(&h, p);
+    if (e == cudaSuccess) memcpy(ipc_handle, &h, sizeof(h));
+  }
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    set_error(std::string("cot_xchg_alloc: ") + cudaGetErrorString(e));
+    return COT_E_CUDA;
+  }
+  *xbuf = p;
+  return COT_OK;
+}
+
+int cot_xchg_open(const void* ipc_handle, void** peer_xbuf) {
+  if (!ipc_handle || !peer_xbuf) return arg_error("cot_xchg_open: NULL argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  COT_CHECK_CUDA(cudaIpcOpenMemHandle(peer_xbuf, h, cudaIpcMemLazyEnablePeerAccess));
+  return COT_OK;
+}
+
+int cot_xchg_close(void* peer_xbuf) {
+  if (!peer_xbuf) return COT_OK;
+  COT_CHECK_CUDA(cudaIpcCloseMemHandle(peer_xbuf));
+  return COT_OK;
+}
+
+int cot_xchg_free(void* xbuf) {
+  if (!xbuf) return COT_OK;
+  COT_CHECK_CUDA(cudaFree(xbuf));
+  return COT_OK;
+}
+
+static int fused_rank_args(const double* alpha, const double* beta, const void* C_local, const void* G_local,
+                           int64_t n, int64_t m, int64_t row_begin, int64_t R, int dtype, const double* eps,
+                           double tol, int64_t check_every, uint32_t flags, double* w_hat, double* z_hat,
+                           void* workspace, size_t ws_bytes, int nranks, int rank, void* const* xbufs,
+                           FusedRank* fr) {
+  int st = check_shape(1, n, m, dtype);
+  if (st) return st;
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+    return arg_error("fused sharding: need 1 <= nranks <= COT_MAX_RANKS and 0 <= rank < nranks");
+  if (R < 1 || row_begin < 0 || row_begin + R > m) return arg_error("fused sharding: bad row range");
+  if (R != m / nranks && R != (m + nranks - 1) / nranks)
+    return arg_error("fused sharding: R must be floor or ceil of m / nranks (balanced partition)");
+  if (!alpha || !beta || !C_local || !G_local || !eps || !w_hat || !z_hat || !xbufs)
+    return arg_error("fused sharding: NULL argument");
+  for (int q = 0; q < nranks; ++q)
+    if (!xbufs[q]) return arg_error("fused sharding: NULL exchange buffer");
+  if (tol < 0) return arg_error("fused sharding: tol >= 0 required");
+  st = check_ws(workspace, ws_bytes, 1, n, m, R, dtype, &fr->ws);
+  if (st) return st;
+  fr->a = make_args(alpha, beta, C_local, G_local, 1, n, m, dtype, eps, tol, check_every, flags, w_hat, z_hat,
+                    row_begin, R);
+  if (!tma_eligible(fr->a))
+    return arg_error("fused sharding needs fp32 costs, m % 4 == 0 and m <= 1024 (else cerot_iter_sharded)");
+  for (int q = 0; q < kMaxRanks; ++q)
+    fr->xpeer[q] = q < nranks ? reinterpret_cast<uint4*>(static_cast<char*>(xbufs[q]) + kXchgHeader) : nullptr;
+  fr->xepoch = static_cast<unsigned long long*>(xbufs[rank]);
+  fr->rank = rank;
+  return COT_OK;
+}
+
+int cerot_iter_fused(const double* alpha, const double* beta, const void* C_local, const void* G_local, int64_t n,
+                     int64_t m, int64_t row_begin, int64_t R, int dtype, const double* eps, int64_t iters, double tol,
+                     int64_t check_every, uint32_t flags, double* w_hat, double* z_hat, void* workspace,
+                     size_t ws_bytes, int nranks, int rank, void* const* xbufs, void* stream) {
+  if (iters < 0) return arg_error("cerot_iter_fused: iters >= 0 required");
+  FusedRank fr;
+  int st = fused_rank_args(alpha, beta, C_local, G_local, n, m, row_begin, R, dtype, eps, tol, check_every, flags,
+                           w_hat, z_hat, workspace, ws_bytes, nranks, rank, xbufs, &fr);
+  if (st) return st;
+  if (iters == 0) return COT_OK;
+  COT_CHECK_CUDA(launch_iter_tma_fused(&fr, 1, nranks, false, (int)iters, (cudaStream_t)stream));
+  return COT_OK;
+}
+
+int cerot_iter_fused_emulated(int nranks, const double* alpha, const double* beta, const void* const* C_local,
+                              const void* const* G_local, int64_t n, int64_t m, const int64_t* row_begin,
+                              const int64_t* R, int dtype, const double* eps, int64_t iters, double tol,
+                              int64_t check_every, uint32_t flags, double* const* w_hat, double* const* z_hat,
+                              void* const* workspace, const size_t* ws_bytes, void* const* xbufs, void* stream) {
+  if (iters < 0) return arg_error("cerot_iter_fused_emulated: iters >= 0 required");
+  if (nranks < 1 || nranks > kMaxRanks) return arg_error("cerot_iter_fused_emulated: 1 <= nranks <= COT_MAX_RANKS");
+  if (!C_local || !G_local || !row_begin || !R || !w_hat || !z_hat || !workspace || !ws_bytes || !xbufs)
+    return arg_error("cerot_iter_fused_emulated: NULL array");
+  FusedRank fr[kMaxRanks];
+  for (int v = 0; v < nranks; ++v) {
+    int st = fused_rank_args(alpha, beta, C_local[v], G_local[v], n, m, row_begin[v], R[v], dtype, eps, tol,
+                             check_every, flags, w_hat[v], z_hat[v], workspace[v], ws_bytes[v], nranks, v, xbufs, &fr[v]);
+    if (st) return st;
+  }
+  if (iters == 0) return COT_OK;
+  COT_CHECK_CUDA(launch_iter_tma_fused(fr, nranks, nranks, true, (int)iters, (cudaStream_t)stream));
   return COT_OK;
 }
 

@@ -18,7 +18,10 @@ struct SolverState {
   int flags;         // bit 0: marginal validation failed; bit 1: column underflow
   int pad;
 };
-enum { STATE_BAD_MARGINAL = 1, STATE_UNDERFLOW = 2 };
+enum { STATE_BAD_MARGINAL = 1, STATE_UNDERFLOW = 2, STATE_PEER_TIMEOUT = 4 };
+
+constexpr int kMaxRanks = 8;   // fused multi-GPU exchange: ranks of one row partition (one 8-GPU node)
+constexpr size_t kXchgHeader = 256;   // exchange buffer: epoch counter, then the LL lines
 
 // Rows of each problem are cut into units of `rpu` consecutive rows; units are the work items of the
 // row kernels (K-ITER, K-PLAN) and each unit writes one fp64 column-partial row. `upp` units per
@@ -48,6 +51,15 @@ struct Workspace {
   double* c_global;        // [B][m] column sums after the cross-GPU reduction
   double* plan_buf;        // [B][kPlanBufHead + m] local plan reductions (allreduced in place)
   double* rowscal;         // [B][m][4] per-row plan scalars of the C-SROT report
+  // LL-line region of the persistent kernel (B == 1 only; zeroed by cerot_init; offsets depend on B, m and
+  // the SM count only, so cerot_init finds it without n, R or the dtype)
+  void* ll_base;
+  size_t ll_bytes;
+  unsigned long long* lepoch;   // [1]
+  uint4* zlines;                // [m]
+  uint4* rlines;                // [2][lcap]
+  uint4* plines;                // [2][lcap][m]
+  int lcap;                     // = SM count
 };
 // Lays the workspace out from `base` (may be NULL to only size it). Returns the byte count. R = rows held
 // per problem (m unless row-sharded).
@@ -96,6 +108,17 @@ cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int ite
 // into ws.partials[parity] when rows_only.
 cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, bool rows_only, int parity,
                             cudaStream_t s);
+// Fused multi-GPU row sharding: the persistent kernel of one rank (or, emulated, of all ranks in one
+// cooperative grid on one GPU) with the column-sum exchange done in-kernel through peer-mapped LL lines.
+struct FusedRank {
+  IterArgs a;                          // this rank's shard (row_begin, R)
+  Workspace ws;
+  uint4* xpeer[kMaxRanks];             // every rank's line array, as addressed by this rank
+  unsigned long long* xepoch;          // this rank's epoch counter
+  int rank;
+};
+int fused_column_slices(int64_t m, int nranks, int sms);
+cudaError_t launch_iter_tma_fused(const FusedRank* r, int nv, int nranks, bool emulate, int iters, cudaStream_t s);
 // Plan pass over the held rows: T blocks (optional) + unit partials in the workspace (no finalisation).
 cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& up, void* T_blocks, cudaStream_t s);
 // NEXT-3 C-SROT (squared regulariser): one alternating-maximisation sweep (w-step, z-step + monitor), plan.

@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 namespace cot {
@@ -46,15 +47,25 @@ struct TmaParams {
   int rows_only;
   double tol;
   long long check_every;
-  double* partials;      // [U][m]
-  double* resid_part;    // [gridDim.x]
+  double* partials;      // [U][m] (rows_only: the plain fp64 column partials of cerot_rows)
   SolverState* state;    // [1]
-  unsigned* bar;         // [4]: two device-wide barriers {arrival count, generation}
+  // device-wide steps through LL lines (workspace; zeroed by cerot_init): generation g = lepoch + iteration
+  uint4* plines;         // [2][lcap][m] column partials of each unit
+  uint4* zlines;         // [m] z_hat after the q-update
+  uint4* rlines;         // [2][lcap] monitor partial of each column slice
+  unsigned long long* lepoch;   // iterations run on this workspace since cerot_init
+  int lcap;              // unit capacity of the line arrays (>= U)
+  int gsh;               // 1: this CTA's rows of G are staged in shared memory
   int nk, ne, qn;        // k-sum warps, epilogue warps, row-queue depth
   int evict_last_rows;   // rows [0, evict_last_rows) of every block are streamed with an L2 evict_last hint
   int diag;              // COT_DIAG_* bits (diagnostics only)
   int pre;               // precomputed mode (NEXT-1): C is S [R][m] (n = 1) and s_ij = S_ij
   unsigned long long* trace;   // diagnostics: [grid][8] cycle counters, or nullptr
+  // fused multi-GPU mode (nranks > 0): the column sums of each slice are exchanged through LL lines
+  int nranks, rank;      // ranks of the row partition, this rank
+  int ncs;               // column slices (identical on every rank)
+  uint4* xpeer[kMaxRanks];          // rank q's line array [2][nranks][m], mapped into this rank's address space
+  unsigned long long* xepoch;       // this rank's exchange epoch (iterations exchanged so far)
 };
 
 __device__ __forceinline__ void cbar(int nthreads) {   // consumer-only named barrier
@@ -85,37 +96,56 @@ __device__ __forceinline__ unsigned lds_acquire(const unsigned* p) {
 __device__ __forceinline__ void sts_release(unsigned* p, unsigned v) {
   asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
-// Hand-off barrier between the consumer warps (arrive, non-blocking) and the sync warp (sync).
-__device__ __forceinline__ void handoff_arrive(int nthreads) {
-  asm volatile("bar.arrive 2, %0;" ::"r"(nthreads) : "memory");
+// LL lines of the fused multi-GPU exchange: 16-byte volatile stores / loads on (possibly peer-mapped)
+// global memory; each 8-byte half {32-bit payload, 32-bit generation} is written and read as one unit.
+__device__ __forceinline__ void st_line(uint4* p, uint4 v) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
 }
-__device__ __forceinline__ void handoff_sync(int nthreads) {
-  asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+__device__ __forceinline__ uint4 ld_line(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr unsigned long long kPeerTimeoutNs = 20000000000ull;   // 20 s without a peer's line: give up
+constexpr int kColScratch = 256 + kMaxRanks * 8;   // doubles: column-pass groups, then the rank exchange
+constexpr int kRankScratch = 256;
 
-// Device-wide barrier among the consumer warps of all CTAs, split into arrive / wait so that independent
-// work can run in between. bar = {arrival count, generation}. Ordering uses release/acquire atomics at gpu
-// scope (the CTA barrier before the arrival makes it cumulative over the CTA's writes); no fence.sc, which
-// would also stall this SM's in-flight TMA traffic.
-__device__ __forceinline__ unsigned grid_arrive(unsigned* bar, int nct, unsigned* gen_sh) {
-  cbar(nct);
-  if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire(bar + 1);
-    const unsigned arrived = atom_add_acq_rel(bar, 1u);
-    if (arrived == gridDim.x - 1) {
-      st_relaxed(bar, 0u);
-      red_add_release(bar + 1, 1u);
-    }
-    *gen_sh = gen;
-  }
-  cbar(nct);
-  return *gen_sh;
+__device__ __forceinline__ uint4 ll_pack(double v, unsigned g) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return make_uint4((unsigned)b, g, (unsigned)(b >> 32), g);
 }
-__device__ __forceinline__ void grid_wait(unsigned* bar, unsigned gen, int nct) {
-  if (threadIdx.x == 0) {
-    while (ld_acquire(bar + 1) == gen) __nanosleep(20);
+__device__ __forceinline__ bool ll_ready(const uint4& l, unsigned g) { return l.y == g && l.w == g; }
+__device__ __forceinline__ double ll_value(const uint4& l) {
+  return __longlong_as_double((long long)(((unsigned long long)l.z << 32) | l.x));
+}
+// Spin until the line carries generation g; false after kPeerTimeoutNs (v is then garbage).
+__device__ __forceinline__ bool poll_line(const uint4* a, unsigned g, double& v) {
+  uint4 l = ld_line(a);
+  if (ll_ready(l, g)) {
+    v = ll_value(l);
+    return true;
   }
-  cbar(nct);
+  const unsigned long long t0 = gtimer();
+  while (true) {
+    l = ld_line(a);
+    if (ll_ready(l, g)) {
+      v = ll_value(l);
+      return true;
+    }
+    if (gtimer() - t0 > kPeerTimeoutNs) {
+      v = 0.0;
+      return false;
+    }
+  }
 }
 
 // Two-cbar block reduction for rare uses (monitor partial).
@@ -172,6 +202,86 @@ __device__ __forceinline__ double exp_split(double d) {
   return (double)ex2(f) * __longlong_as_double(e << 52);
 }
 
+// s * e^d for d in fp64 (|d| < ~700) and s in fp32: 2^round(d log2e) built exactly in the exponent bits,
+// times s * 2^frac (|frac| <= 1/2) in fp32 with MUFU.EX2, so the rounding of the argument costs < 3e-8
+// relative regardless of |d|. Three conversions per call; the round uses the 1.5*2^52 trick (no F2I).
+__device__ __forceinline__ double exp_scaled(double d, float s) {
+  // below 2^-1022 the term is negligible; above 2^1000 the caller's range check redoes the row exactly
+  const double a = fmin(fmax(d * COT_LOG2E, -1022.0), 1000.0);
+  const double big = a + 6755399441055744.0;
+  const int ai = __double2loint(big);
+  const float f = (float)(a - (big - 6755399441055744.0));
+  return (double)(s * ex2(f)) * __hiloint2double((ai + 1023) << 20, 0);
+}
+
+// One-barrier block reductions of N values over the epilogue warps (<= 8 warps; double-buffered scratch).
+template <int N>
+__device__ __forceinline__ void cblk_sumN(double* v, double* red2, int& buf, int nct, int wbase) {
+  const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) - wbase;
+  double* r = red2 + buf * 64;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const double x = warp_sum(v[k]);
+    if (lane == 0) r[k * 8 + wid] = x;
+  }
+  cbar(nct);
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double x = r[k * 8];
+    for (int w = 1; w < (nct >> 5); ++w) x += r[k * 8 + w];
+    v[k] = x;
+  }
+  buf ^= 1;
+}
+template <int N>
+__device__ __forceinline__ void cblk_maxN(double* v, double* red2, int& buf, int nct, int wbase) {
+  const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) - wbase;
+  double* r = red2 + buf * 64;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const double x = warp_max(v[k]);
+    if (lane == 0) r[k * 8 + wid] = x;
+  }
+  cbar(nct);
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double x = r[k * 8];
+    for (int w = 1; w < (nct >> 5); ++w) x = fmax(x, r[k * 8 + w]);
+    v[k] = x;
+  }
+  buf ^= 1;
+}
+
+// One-barrier block reduction of two rows' (max, sum) over the epilogue warps (double-buffered scratch).
+__device__ __forceinline__ void cblk_maxsum2(double* mx, double* sm, double* red2, int& buf, int nct, int wbase) {
+  const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) - wbase;
+  double a0 = warp_max(mx[0]), a1 = warp_max(mx[1]);
+  double b0 = warp_sum(sm[0]), b1 = warp_sum(sm[1]);
+  double* r = red2 + buf * 64;
+  if (lane == 0) {
+    r[wid] = a0;
+    r[8 + wid] = a1;
+    r[16 + wid] = b0;
+    r[24 + wid] = b1;
+  }
+  cbar(nct);
+  a0 = r[0];
+  a1 = r[8];
+  b0 = r[16];
+  b1 = r[24];
+  for (int w = 1; w < (nct >> 5); ++w) {
+    a0 = fmax(a0, r[w]);
+    a1 = fmax(a1, r[8 + w]);
+    b0 += r[16 + w];
+    b1 += r[24 + w];
+  }
+  mx[0] = a0;
+  mx[1] = a1;
+  sm[0] = b0;
+  sm[1] = b1;
+  buf ^= 1;
+}
+
 template <int VEC>
 struct VecF;
 template <>
@@ -188,32 +298,37 @@ struct VecF<4> {
 };
 
 template <int CPT, int EPT, int KS>
-__global__ void __launch_bounds__(448, 1) k_iter_tma(TmaParams p) {
+__device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid, const int nblk) {
   constexpr int VEC = 4;
+  constexpr int RS = 6;                       // rowstat stride: next reference, Mref, r, log alpha, alpha, -
+  constexpr int RB = EPT == 1 ? 4 : 2;        // rows per epilogue batch
   using VT = float4;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = p.nk, ne = p.ne;             // k-sum warps, epilogue warps; then producer, sync warps
+  const int nk = p.nk, ne = p.ne;             // k-sum warps, epilogue warps, then the producer warp
   const int nkt = nk * 32, net = ne * 32;
-  const int wprod = nk + ne, wsync = nk + ne + 1;
+  const int wprod = nk + ne;
   const int m = p.m, mv = m / VEC;
   const int n = p.n, R = p.R;
-  const int U = p.U, rpu = p.rpu, QN = p.qn;
+  const int rpu = p.rpu, QN = p.qn;
   const size_t slot_floats = (size_t)KS * m;
   // ---- shared memory layout
   float* ring = reinterpret_cast<float*>(smem);
   float* queue = reinterpret_cast<float*>(smem + (size_t)p.nslot * slot_floats * 4 + 1024);   // [QN][m]
-  double* rowstat = reinterpret_cast<double*>(queue + (size_t)QN * m);   // [rpu][4]: M', M, r, log alpha
-  uint64_t* full = reinterpret_cast<uint64_t*>(rowstat + (size_t)rpu * 4);
+  double* gsh = reinterpret_cast<double*>(queue + (size_t)QN * m);      // [rpu][m] -G/eps in fp64 if p.gsh
+  double* rowstat = gsh + (p.gsh ? (size_t)rpu * m : 0);                 // [rpu][RS]
+  double* xs = rowstat + (size_t)rpu * RS;                               // [kColScratch] column-pass scratch
+  uint64_t* full = reinterpret_cast<uint64_t*>(xs + kColScratch);
   uint64_t* empty = full + p.nslot;
   uint64_t* qfull = empty + p.nslot;
   uint64_t* qempty = qfull + QN;
   unsigned* ctl = reinterpret_cast<unsigned*>(qempty + QN);
-  // ctl: [0] TMA slots issued [1] producer done [2] stop producer [4] z generation (completed q-updates)
-  //      [5] halt (frozen) [6] rows produced by the k-sum warps [7] k-sum warps done
-  //      [8] k-sum broadcast [9] epilogue broadcast
+  // ctl: [0] TMA slots issued [1] producer done [2] stop producer [5] halt
+  //      [6] rows produced by the k-sum warps [7] k-sum warps done [8] k-sum broadcast
   double* red2 = reinterpret_cast<double*>(ctl + 16);   // [2][64]
 
+  const int u = bid;                        // one unit of rows per CTA (the launcher sets nblk == U)
+  const int i0 = u * rpu, i1 = min(R, i0 + rpu), nrows = i1 - i0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nslot; ++s) {
       mbar_init(&full[s], 1);
@@ -226,12 +341,18 @@ __global__ void __launch_bounds__(448, 1) k_iter_tma(TmaParams p) {
     for (int c = 0; c < 16; ++c) ctl[c] = 0;
     fence_mbar_init();
   }
+  const double inv_eps = 1.0 / p.eps[0];
+  if (p.gsh) {   // this CTA's rows of -G/eps in fp64, read by the epilogue warps every iteration
+    const VT* src = reinterpret_cast<const VT*>(p.G + (size_t)i0 * m);
+    for (int idx = threadIdx.x; idx < nrows * mv; idx += blockDim.x) {
+      const float4 g4 = __ldg(src + idx);
+      reinterpret_cast<double2*>(gsh)[2 * idx] = make_double2(-(double)g4.x * inv_eps, -(double)g4.y * inv_eps);
+      reinterpret_cast<double2*>(gsh)[2 * idx + 1] = make_double2(-(double)g4.z * inv_eps, -(double)g4.w * inv_eps);
+    }
+  }
   __syncthreads();
 
-  const int u = blockIdx.x;                 // one unit of rows per CTA (the launcher sets grid == U)
-  const int i0 = u * rpu, i1 = min(R, i0 + rpu), nrows = i1 - i0;
   const bool active0 = p.state[0].active != 0;
-  const double inv_eps = 1.0 / p.eps[0];
 
   if (warp == wprod) {
     // ===================================================================== producer (one lane)
@@ -267,8 +388,8 @@ __global__ void __launch_bounds__(448, 1) k_iter_tma(TmaParams p) {
       }
     producer_done:
       if (p.trace) {
-        p.trace[blockIdx.x * 8 + 0] = prod_wait;
-        p.trace[blockIdx.x * 8 + 1] = clock64() - tp0;
+        p.trace[bid * 8 + 0] = prod_wait;
+        p.trace[bid * 8 + 1] = clock64() - tp0;
       }
     }
     if (lane == 0) {
@@ -276,96 +397,6 @@ __global__ void __launch_bounds__(448, 1) k_iter_tma(TmaParams p) {
       *(volatile unsigned*)&ctl[1] = 1u;
     }
     __syncwarp();
-  } else if (warp == wsync) {
-    // ===================================================================== sync warp
-    // Per iteration t: wait until the epilogue warps published the CTA's column partial of t; B1; column
-    // pass of this CTA's slice; B2; monitor / freeze rule; publish z generation t+1 (or halt).
-    SolverState st = p.state[0];
-    const long long iters0 = st.iters;
-    const bool sync = !p.rows_only && !(p.diag & COT_DIAG_NO_SYNC);
-    const int cols_per_cta = (m + gridDim.x - 1) / gridDim.x;
-    const int col0 = blockIdx.x * cols_per_cta;
-    const int col1 = min(m, col0 + cols_per_cta);
-    if (!p.rows_only && active0) {
-      for (int t = 0; t < p.iters; ++t) {
-        handoff_sync(net + 32);               // epilogue warps published partial t (and w_hat of t)
-        if (!sync) {
-          st.iters += 1;
-          if (lane == 0) sts_release(&ctl[4], (unsigned)(t + 1));
-          continue;
-        }
-        // ---- B1: every CTA's partial of iteration t is published
-        if (lane == 0) {
-          const unsigned gen = ld_acquire(p.bar + 1);
-          if (atom_add_acq_rel(p.bar, 1u) == gridDim.x - 1) {
-            st_relaxed(p.bar, 0u);
-            red_add_release(p.bar + 1, 1u);
-          }
-          while (ld_acquire(p.bar + 1) == gen) __nanosleep(20);
-        }
-        __syncwarp();
-        // ---- column pass: c_j = sum_u P_uj (fixed order: lane-strided units, then the warp_sum tree)
-        const long long itg = iters0 + t + 1;
-        const bool need_resid = (p.tol > 0.0 && itg % p.check_every == 0) || t == p.iters - 1;
-        double dev = 0.0;
-        for (int cb = col0; cb < col1; cb += 8) {
-          double acc[8];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-          for (int u2 = lane; u2 < U; u2 += 32) {
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              if (cb + c < col1) acc[c] += __ldcg(p.partials + (size_t)u2 * m + cb + c);
-          }
-#pragma unroll
-          for (int c = 0; c < 8; ++c) acc[c] = warp_sum(acc[c]);
-          const int c = lane;
-          if (c < 8 && cb + c < col1) {
-            double cj = acc[0];
-#pragma unroll
-            for (int q = 1; q < 8; ++q) cj = (c == q) ? acc[q] : cj;
-            const int j = cb + c;
-            const double bj = p.beta[j];
-            dev += fabs(cj - bj);
-            if (!(cj >= 1e-28)) atomicOr(&p.state[0].flags, (int)STATE_UNDERFLOW);
-            p.z_hat[j] = __ldcg(p.z_hat + j) + (log(bj) - log(cj));
-          }
-        }
-        dev = warp_sum(dev);
-        // ---- B2: every q-update of iteration t is written
-        if (lane == 0) {
-          if (need_resid) p.resid_part[blockIdx.x] = dev;
-          const unsigned gen = ld_acquire(p.bar + 3);
-          if (atom_add_acq_rel(p.bar + 2, 1u) == gridDim.x - 1) {
-            st_relaxed(p.bar + 2, 0u);
-            red_add_release(p.bar + 3, 1u);
-          }
-          while (ld_acquire(p.bar + 3) == gen) __nanosleep(20);
-        }
-        __syncwarp();
-        st.iters += 1;
-        if (need_resid) {   // every CTA sums the monitor partials in the same order
-          double r = 0.0;
-          for (int b2 = lane; b2 < (int)gridDim.x; b2 += 32) r += __ldcg(p.resid_part + b2);
-          st.residual = warp_sum(r) * (double)n;
-        }
-        if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
-          st.active = 0;
-          st.converged = 1;
-          if (lane == 0) sts_release(&ctl[5], 1u);   // halt: iteration t+1 is discarded
-          break;
-        }
-        if (lane == 0) sts_release(&ctl[4], (unsigned)(t + 1));
-      }
-      if (blockIdx.x == 0 && lane == 0) {
-        SolverState out = p.state[0];
-        out.iters = st.iters;
-        out.residual = st.residual;
-        out.active = st.active;
-        out.converged = st.converged;
-        p.state[0] = out;
-      }
-    }
   } else if (warp < nk) {
     // ===================================================================== k-sum warps
     // s_ij = sum_k exp2((G_ij - C_ijk) log2e/eps) for every row, streamed from the TMA ring into the row
@@ -480,7 +511,7 @@ __global__ void __launch_bounds__(448, 1) k_iter_tma(TmaParams p) {
       ++produced;
       if (kt == 0) *(volatile unsigned*)&ctl[6] = produced;
     }
-    if (p.trace && kt == 0) p.trace[blockIdx.x * 8 + 3] = c_ksum;
+    if (p.trace && kt == 0) p.trace[bid * 8 + 3] = c_ksum;
     asm volatile("bar.sync 3, %0;" ::"r"(nkt) : "memory");
     if (kt == 0) {
       __threadfence_block();
@@ -501,172 +532,353 @@ __global__ void __launch_bounds__(448, 1) k_iter_tma(TmaParams p) {
     }
   } else {
     // ===================================================================== epilogue warps
-    // Per row (in order): wait for its k-sums in the queue and, at the first row of an iteration, for the
-    // previous q-update; then the fp64 epilogue: x_ij = z_hat_j - G_ij/eps, r_i = sum_j s_ij exp(x_ij - M'_i)
-    // and M_i = max_j x_ij in ONE block reduction against the previous row maximum M'_i (exact exponent
-    // split), w_hat_i = log alpha_i - M'_i - log r_i (lazily, once per iteration), P_j += (alpha_i/r_i) t_ij.
+    // Per iteration: (1) the row epilogues (in order): wait for the row's k-sums in the queue, then
+    //   x_ij = z_hat_j - G_ij/eps, r_i = sum_j s_ij exp(x_ij - M'_i) and M_i = max_j x_ij in ONE block
+    //   reduction against the previous row maximum M'_i (exact exponent split), w_hat_i, and the column
+    //   partial P_j += (alpha_i/r_i) t_ij;
+    // (2) the device-wide steps, with no grid barrier: the CTA's partial goes out as LL lines (each fp64 value
+    //   with the iteration's generation in both 8-byte halves), the owner CTA of each column slice polls the
+    //   slice's lines of every unit and sums them in unit order (deterministic), [fused multi-GPU: exchanges
+    //   the slice's sums with the other ranks the same way], applies the q-update and publishes z_hat of the
+    //   slice as LL lines; every CTA then polls the z lines it needs for the next iteration. The monitor is a
+    //   line per CTA, summed in CTA order by every CTA (identical freeze decisions).
     const int et = threadIdx.x - nkt;
-    const int ewarp = warp - nk;
+    const bool fused = p.nranks > 0;
+    const bool sync = !p.rows_only && !(p.diag & COT_DIAG_NO_SYNC);
+    const int ncs = fused ? p.ncs : nblk;
+    const int cpc = (m + ncs - 1) / ncs;
+    const int col0 = bid < ncs ? bid * cpc : m;
+    const int col1 = min(m, col0 + cpc);
+    const int ngrp = net >> 3;                // column pass: thread = (unit group, column of an 8-column chunk)
+    const unsigned long long lep0 = sync ? *(volatile const unsigned long long*)p.lepoch : 0ull;
+    const unsigned long long xep0 = fused ? *(volatile const unsigned long long*)p.xepoch : 0ull;
     uint32_t qs = 0, qph = 0;
     unsigned consumed = 0;
     int rbuf = 0;
-    long long c_epi = 0, c_wait = 0;
+    long long c_epi = 0, c_wait = 0, c_cmp = 0, c_red = 0, c_col = 0;
+    bool timeout = false;
+    const bool have_ref = p.state[0].iters > 0;   // w_hat holds the previous iteration's p-update
     for (int r = et; r < nrows; r += net) {
       const double a = p.alpha[p.row_begin + i0 + r];
-      rowstat[r * 4 + 0] = __longlong_as_double(0x7ff8000000000000LL);   // no previous maximum yet
-      rowstat[r * 4 + 3] = log(a);
+      const double la = log(a);
+      // shift reference = the row's log-sum-exp of the previous iteration, log alpha_i - w_hat_i (NaN: none)
+      rowstat[r * RS + 0] = have_ref ? la - p.w_hat[p.row_begin + i0 + r] : __longlong_as_double(0x7ff8000000000000LL);
+      rowstat[r * RS + 3] = la;
+      rowstat[r * RS + 4] = a;
     }
     asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+    SolverState st = p.state[0];
+    const long long iters0 = st.iters;
     double z[EPT][VEC], P[EPT][VEC];
-    auto load_z = [&]() {
-#pragma unroll
-      for (int q = 0; q < EPT; ++q) {
-        const int jv = q * net + et;
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) z[q][v] = jv < mv ? __ldcg(p.z_hat + VEC * jv + v) : 0.0;
-      }
-    };
 #pragma unroll
     for (int q = 0; q < EPT; ++q)
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
-    bool halted = false;
-    if (active0) load_z();
-    for (int t = 0; active0 && t < p.iters && !halted; ++t) {
-      if (t > 0) {   // z generation >= t: the q-update of iteration t-1 is visible
-        const long long tw0 = p.trace ? clock64() : 0;
-        if (et == 0) {
-          unsigned zg = lds_acquire(&ctl[4]), h = lds_acquire(&ctl[5]);
-          while (zg < (unsigned)t && !h) {
-            __nanosleep(32);
-            zg = lds_acquire(&ctl[4]);
-            h = lds_acquire(&ctl[5]);
-          }
-          ctl[9] = h ? 1u : 0u;
-        }
-        asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
-        halted = ctl[9] != 0;
-        asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
-        if (p.trace) c_wait += clock64() - tw0;
-        if (halted) break;
-        load_z();
+      for (int v = 0; v < VEC; ++v) {
+        const int jv = q * net + et;
+        z[q][v] = jv < mv ? __ldcg(p.z_hat + VEC * jv + v) : 0.0;
+        P[q][v] = 0.0;
       }
-      for (int r = 0; r < nrows; ++r) {
-        // G row (read-only) first, so its latency overlaps the queue wait
-        float g[EPT][VEC];
+    auto need_resid = [&](int t) {
+      const long long itg = iters0 + t + 1;
+      return (p.tol > 0.0 && itg % p.check_every == 0) || t == p.iters - 1;
+    };
+    // monitor of the iteration that produced generation g: sum of the slice owners' lines in CTA order
+    auto read_resid = [&](unsigned g) {
+      const uint4* rl = p.rlines + (size_t)(g & 1u) * p.lcap;
+      double v = 0.0;
+      for (int b = et; b < ncs; b += net) {
+        double x;
+        timeout |= !poll_line(rl + b, g, x);
+        v += x;
+      }
+      return cblk_sum1(v, red2, rbuf, net, nk);
+    };
+    int done = 0;   // iterations completed (q-update applied) in this launch
+    bool halted = false;
+    for (int t = 0; active0 && t < p.iters; ++t) {
+      if (t > 0 && sync) {
+        // ---- z_hat of generation g (the q-update of iteration t-1) and, if due, its monitor
+        const long long tw0 = p.trace ? clock64() : 0;
+        const unsigned g = (unsigned)(lep0 + t);
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
           const int jv = q * net + et;
-          const float4 gv = jv < mv ? __ldg(reinterpret_cast<const VT*>(p.G + (size_t)(i0 + r) * m) + jv)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-          g[q][0] = gv.x;
-          g[q][1] = gv.y;
-          g[q][2] = gv.z;
-          g[q][3] = gv.w;
-        }
-        mbar_wait(&qfull[qs], qph);
-        const long long te0 = p.trace ? clock64() : 0;
-        float s[EPT][VEC];
-        const VT* qrow = reinterpret_cast<const VT*>(queue + (size_t)qs * m);
+          if (jv < mv) {
 #pragma unroll
-        for (int q = 0; q < EPT; ++q) {
-          const int jv = q * net + et;
-          const float4 sv = jv < mv ? qrow[jv] : make_float4(0.f, 0.f, 0.f, 0.f);
-          s[q][0] = sv.x;
-          s[q][1] = sv.y;
-          s[q][2] = sv.z;
-          s[q][3] = sv.w;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&qempty[qs]);
-        ++consumed;
-        if (++qs == (uint32_t)QN) {
-          qs = 0;
-          qph ^= 1u;
-        }
-        // ---- the row epilogue
-        double x[EPT][VEC];
-        double lmax = -INFINITY;
-#pragma unroll
-        for (int q = 0; q < EPT; ++q) {
-          const bool ok = q * net + et < mv;
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            x[q][v] = ok ? z[q][v] - (double)g[q][v] * inv_eps : -INFINITY;
-            lmax = fmax(lmax, x[q][v]);
+            for (int v = 0; v < VEC; ++v) timeout |= !poll_line(p.zlines + VEC * jv + v, g, z[q][v]);
           }
         }
-        double Mref = rowstat[r * 4 + 0];
-        double tt[EPT][VEC];
-        double Mtrue, rsum;
-        bool exact = !(Mref == Mref);          // no previous maximum: two-pass
-        if (!exact) {
-          double lsum = 0.0;
+        if (need_resid(t - 1)) st.residual = read_resid(g) * (double)n;
+        if (p.trace) c_wait += clock64() - tw0;
+        if (fused && (__ldcg(&p.state[0].flags) & STATE_PEER_TIMEOUT)) halted = true;
+        if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
+          st.active = 0;
+          st.converged = 1;
+          halted = true;
+        }
+        if (halted) {
+          st.active = 0;
+          if (et == 0) sts_release(&ctl[5], 1u);   // stop the k-sum warps (their rows are drained below)
+          break;
+        }
+      }
+      // rows in batches of RB: one block reduction (the RB row sums) per batch; the batch's k-sums are read
+      // straight from the queue slots (released after the batch) and -G/eps from shared memory
+      for (int r0 = 0; r0 < nrows; r0 += RB) {
+        const int nb = min(RB, nrows - r0);
+        uint32_t qsb[RB];
+        {
+          uint32_t q2 = qs, ph2 = qph;
+#pragma unroll
+          for (int b = 0; b < RB; ++b) {
+            qsb[b] = q2;
+            if (b < nb) {
+              mbar_wait(&qfull[q2], ph2);
+              if (++q2 == (uint32_t)QN) {
+                q2 = 0;
+                ph2 ^= 1u;
+              }
+            }
+          }
+        }
+        const long long te0 = p.trace ? clock64() : 0;
+        // element (b, q, v): s_ij from the queue, x_ij = z_j - G_ij/eps
+        auto sval = [&](int b, int q, int v) -> float { return queue[(size_t)qsb[b] * m + VEC * (q * net + et) + v]; };
+        auto xval = [&](int b, int q, int v) -> double {
+          const int j = VEC * (q * net + et) + v;
+          return z[q][v] + (p.gsh ? gsh[(size_t)(r0 + b) * m + j] : -(double)__ldg(p.G + (size_t)(i0 + r0 + b) * m + j) * inv_eps);
+        };
+        // ---- the row epilogues: t_ij = s_ij exp(x_ij - Mref_i) with Mref_i the row's log-sum-exp of the
+        // previous iteration (so x - Mref <= ~log(n m) unless z jumped); r_i = sum_j t_ij in one block
+        // reduction for the batch. A batch with a row sum outside [1e-280, 1e280] (no reference yet, or a jump
+        // of the potentials) is redone in the exact two-pass form (maximum first).
+        double Mref[RB], sm[RB], tt[RB][EPT][VEC];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) {
+          Mref[b] = b < nb ? rowstat[(r0 + b) * RS + 0] : 0.0;
+          sm[b] = 0.0;
+        }
+        const bool stale = Mref[0] == Mref[0];      // the CTA's rows get their references together
+#pragma unroll
+        for (int b = 0; b < RB; ++b)
+#pragma unroll
+          for (int q = 0; q < EPT; ++q) {
+            const bool ok = q * net + et < mv && b < nb && stale;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              tt[b][q][v] = ok ? exp_scaled(xval(b, q, v) - Mref[b], sval(b, q, v)) : 0.0;
+              sm[b] += tt[b][q][v];
+            }
+          }
+        const long long te1 = p.trace ? clock64() : 0;
+        cblk_sumN<RB>(sm, red2, rbuf, net, nk);
+        if (p.trace) {
+          c_cmp += te1 - te0;
+          c_red += clock64() - te1;
+        }
+        bool redo = false;
+#pragma unroll
+        for (int b = 0; b < RB; ++b) redo |= b < nb && !(sm[b] >= 1e-280 && sm[b] <= 1e280);
+        if (redo) {   // block-uniform (sm is the block total): exact two-pass for the whole batch
+          double mx[RB];
+#pragma unroll
+          for (int b = 0; b < RB; ++b) {
+            mx[b] = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < EPT; ++q)
+#pragma unroll
+              for (int v = 0; v < VEC; ++v)
+                if (q * net + et < mv && b < nb) mx[b] = fmax(mx[b], xval(b, q, v));
+          }
+          cblk_maxN<RB>(mx, red2, rbuf, net, nk);
+#pragma unroll
+          for (int b = 0; b < RB; ++b) {
+            Mref[b] = b < nb ? mx[b] : 0.0;
+            sm[b] = 0.0;
+#pragma unroll
+            for (int q = 0; q < EPT; ++q) {
+              const bool ok = q * net + et < mv && b < nb;
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) {
+                tt[b][q][v] = ok ? exp_scaled(xval(b, q, v) - Mref[b], sval(b, q, v)) : 0.0;
+                sm[b] += tt[b][q][v];
+              }
+            }
+          }
+          cblk_sumN<RB>(sm, red2, rbuf, net, nk);
+        }
+        // release the batch's queue slots
+        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < RB; ++b) {
+          if (b >= nb) break;
+          if (lane == 0) mbar_arrive(&qempty[qs]);
+          ++consumed;
+          if (++qs == (uint32_t)QN) {
+            qs = 0;
+            qph ^= 1u;
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < RB; ++b) {
+          if (b >= nb) break;
+          const int r = r0 + b;
+          const double rsum = sm[b];
+          double rinv = (double)__frcp_rn((float)rsum);   // alpha_i / r_i: fast reciprocal + 2 Newton steps
+          rinv = rinv * fma(-rsum, rinv, 2.0);
+          rinv = rinv * fma(-rsum, rinv, 2.0);
+          const double rho = rowstat[r * RS + 4] * rinv;
+          if (et == 0) {
+            rowstat[r * RS + 1] = Mref[b];           // shift used for r_i
+            rowstat[r * RS + 2] = rsum;
+          }
 #pragma unroll
           for (int q = 0; q < EPT; ++q)
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) {
-              tt[q][v] = (x[q][v] == -INFINITY) ? 0.0 : (double)s[q][v] * exp_split(x[q][v] - Mref);
-              lsum += tt[q][v];
-            }
-          Mtrue = lmax;
-          rsum = lsum;
-          cblk_maxsum(Mtrue, rsum, red2, rbuf, net, nk);
-          exact = !(fabs(Mtrue - Mref) < 500.0);   // shifted sum out of the safe fp64 range: redo exactly
-        } else {
-          Mtrue = cblk_max1(lmax, red2, rbuf, net, nk);
+            for (int v = 0; v < VEC; ++v) P[q][v] = fma(rho, tt[b][q][v], P[q][v]);
         }
-        if (exact) {
-          Mref = Mtrue;
-          double lsum = 0.0;
+        if (p.trace) c_epi += clock64() - te0;
+      }
+      // ---- w_hat of this CTA's rows (parallel logs)
+      asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+      for (int r = et; r < nrows; r += net) {   // LSE_i = Mref_i + log r_i: w_hat_i and the next reference
+        const double lse = rowstat[r * RS + 1] + log(rowstat[r * RS + 2]);
+        p.w_hat[p.row_begin + i0 + r] = rowstat[r * RS + 3] - lse;
+        rowstat[r * RS + 0] = lse;
+      }
+      if (p.rows_only) {   // cerot_rows: the plain fp64 partial, no device-wide step
 #pragma unroll
-          for (int q = 0; q < EPT; ++q)
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) {
-              tt[q][v] = (x[q][v] == -INFINITY) ? 0.0 : (double)s[q][v] * exp_split(x[q][v] - Mref);
-              lsum += tt[q][v];
-            }
-          rsum = cblk_sum1(lsum, red2, rbuf, net, nk);
+        for (int q = 0; q < EPT; ++q) {
+          const int jv = q * net + et;
+          if (jv < mv)
+            reinterpret_cast<double4*>(p.partials + (size_t)u * m)[jv] = make_double4(P[q][0], P[q][1], P[q][2], P[q][3]);
         }
-        double rinv = (double)__frcp_rn((float)rsum);   // alpha_i / r_i: fast reciprocal + 2 Newton steps
-        rinv = rinv * fma(-rsum, rinv, 2.0);
-        rinv = rinv * fma(-rsum, rinv, 2.0);
-        const double rho = p.alpha[p.row_begin + i0 + r] * rinv;
-        if (et == 0) {
-          rowstat[r * 4 + 0] = Mtrue;           // reference for the next iteration
-          rowstat[r * 4 + 1] = Mref;            // shift used for r_i
-          rowstat[r * 4 + 2] = rsum;
-        }
+        done = 1;
+        break;
+      }
+      if (!sync) {   // diagnostics (COT_DIAG_NO_SYNC): no column pass, z_hat unchanged
 #pragma unroll
         for (int q = 0; q < EPT; ++q)
 #pragma unroll
-          for (int v = 0; v < VEC; ++v) P[q][v] = fma(rho, tt[q][v], P[q][v]);
-        if (p.trace) c_epi += clock64() - te0;
+          for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
+        st.iters += 1;
+        ++done;
+        continue;
       }
-      // ---- publish iteration t: w_hat of this CTA's rows (parallel logs) and the column partial
-      asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
-      for (int r = et; r < nrows; r += net)
-        p.w_hat[p.row_begin + i0 + r] = rowstat[r * 4 + 3] - rowstat[r * 4 + 1] - log(rowstat[r * 4 + 2]);
+      // ---- publish the column partial of iteration t as LL lines of generation g1
+      const unsigned g1 = (unsigned)(lep0 + t + 1);
+      {
+        uint4* pl = p.plines + ((size_t)(g1 & 1u) * p.lcap + u) * m;
 #pragma unroll
-      for (int q = 0; q < EPT; ++q) {
-        const int jv = q * net + et;
-        if (jv < mv)
-          reinterpret_cast<double4*>(p.partials + (size_t)u * m)[jv] =
-              make_double4(P[q][0], P[q][1], P[q][2], P[q][3]);
+        for (int q = 0; q < EPT; ++q) {
+          const int jv = q * net + et;
+          if (jv < mv) {
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
+            for (int v = 0; v < VEC; ++v) st_line(pl + VEC * jv + v, ll_pack(P[q][v], g1));
+          }
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
+        }
       }
-      if (p.rows_only) break;
-      handoff_arrive(net + 32);               // to the sync warp (orders these writes before its B1)
+      // ---- column pass of this CTA's slice: c_j = sum_u P_uj in unit order; q-update; z lines
+      const long long tc0 = p.trace ? clock64() : 0;
+      double dev = 0.0;
+      const uint4* plr = p.plines + (size_t)(g1 & 1u) * p.lcap * m;
+      for (int cb = col0; cb < col1; cb += 8) {
+        const int c = et & 7, grp = et >> 3;
+        const bool colok = cb + c < col1;
+        double acc = 0.0;
+        for (int ub = grp; ub < nblk; ub += 8 * ngrp) {   // 8 lines in flight per thread, unit order kept
+          uint4 l[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int u2 = ub + k * ngrp;
+            l[k] = (colok && u2 < nblk) ? ld_line(plr + (size_t)u2 * m + cb + c) : make_uint4(0u, g1, 0u, g1);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int u2 = ub + k * ngrp;
+            double v = ll_value(l[k]);
+            if (colok && u2 < nblk && !ll_ready(l[k], g1)) timeout |= !poll_line(plr + (size_t)u2 * m + cb + c, g1, v);
+            acc += v;
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");   // previous chunk's readers of xs are done
+        xs[grp * 8 + c] = acc;
+        asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+        double cj = 0.0;
+        if (et < 8) {
+          for (int g2 = 0; g2 < ngrp; ++g2) cj += xs[g2 * 8 + et];
+        }
+        if (fused) {
+          // ---- the exchange step across GPUs: this rank's slice sums -> every rank's x-lines (NVLink peer
+          // stores), then all ranks' lines of the slice from this rank's buffer, summed in rank order
+          const int nr = p.nranks;
+          const unsigned xg = (unsigned)(xep0 + t + 1);
+          const int par = (int)(xg & 1u);
+          if (et < 8 && cb + et < col1) {
+            const uint4 line = ll_pack(cj, xg);
+            for (int q = 0; q < nr; ++q) st_line(p.xpeer[q] + ((size_t)(par * nr + p.rank)) * m + cb + et, line);
+          }
+          for (int q = et >> 3; q < nr && colok; q += ngrp) {
+            double v;
+            timeout |= !poll_line(p.xpeer[p.rank] + ((size_t)(par * nr + q)) * m + cb + c, xg, v);
+            xs[kRankScratch + q * 8 + c] = v;
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+          if (et < 8) {
+            cj = 0.0;
+            for (int q2 = 0; q2 < nr; ++q2) cj += xs[kRankScratch + q2 * 8 + et];
+          }
+        }
+        if (et < 8 && cb + et < col1) {
+          const int j = cb + et;
+          const double bj = p.beta[j];
+          dev += fabs(cj - bj);
+          if (!(cj >= 1e-28)) atomicOr(&p.state[0].flags, (int)STATE_UNDERFLOW);
+          const double zj = __ldcg(p.z_hat + j) + (log(bj) - log(cj));
+          p.z_hat[j] = zj;
+          st_line(p.zlines + j, ll_pack(zj, g1));
+        }
+      }
+      if (timeout) atomicOr(&p.state[0].flags, (int)STATE_PEER_TIMEOUT);
+      if (p.trace) c_col += clock64() - tc0;
+      if (need_resid(t)) {
+        dev = cblk_sum1(dev, red2, rbuf, net, nk);
+        if (et == 0 && bid < ncs) st_line(p.rlines + (size_t)(g1 & 1u) * p.lcap + bid, ll_pack(dev, g1));
+      }
+      st.iters += 1;
+      ++done;
     }
+    if (sync && active0 && !halted && done > 0) {   // monitor + freeze rule of the last iteration
+      const unsigned g = (unsigned)(lep0 + done);
+      st.residual = read_resid(g) * (double)n;
+      if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
+        st.active = 0;
+        st.converged = 1;
+      }
+    }
+    if (bid == 0 && et == 0 && active0 && !p.rows_only) {
+      SolverState out = p.state[0];
+      out.iters = st.iters;
+      out.residual = st.residual;
+      out.active = st.active;
+      out.converged = st.converged;
+      p.state[0] = out;
+      if (sync) *(volatile unsigned long long*)p.lepoch = lep0 + (unsigned long long)done;
+      if (fused) *(volatile unsigned long long*)p.xepoch = xep0 + (unsigned long long)done;
+    }
+    if (timeout) atomicOr(&p.state[0].flags, (int)STATE_PEER_TIMEOUT);
     if (p.trace && et == 0) {
-      p.trace[blockIdx.x * 8 + 4] = c_epi;
-      p.trace[blockIdx.x * 8 + 5] = c_wait;
+      p.trace[bid * 8 + 4] = c_epi;
+      p.trace[bid * 8 + 5] = c_wait;
+      p.trace[bid * 8 + 2] = c_cmp;
+      p.trace[bid * 8 + 6] = c_red;
+      p.trace[bid * 8 + 7] = c_col;
     }
     // ---- drain the queue after a halt: consume every row the k-sum warps still produce
-    (void)ewarp;
     while (true) {
-      const unsigned done = lds_volatile(&ctl[7]);
+      const unsigned kdone = lds_volatile(&ctl[7]);
       __threadfence_block();
       const unsigned prod = lds_volatile(&ctl[6]);
       if (consumed < prod) {
@@ -678,7 +890,7 @@ __global__ void __launch_bounds__(448, 1) k_iter_tma(TmaParams p) {
           qs = 0;
           qph ^= 1u;
         }
-      } else if (done) {
+      } else if (kdone) {
         if (consumed >= lds_volatile(&ctl[6])) break;
       }
     }
@@ -686,15 +898,45 @@ __global__ void __launch_bounds__(448, 1) k_iter_tma(TmaParams p) {
   __syncthreads();
 }
 
+// ------------------------------------------------------------------------------------------ kernels
+template <int CPT, int EPT, int KS>
+__global__ void __launch_bounds__(416, 1) k_iter_tma(const __grid_constant__ TmaParams p) {
+  iter_tma_body<CPT, EPT, KS>(p, blockIdx.x, gridDim.x);
+}
+
+// Emulated multi-rank launch (one GPU): virtual rank v runs on CTAs [base[v], base[v+1]) with its own
+// shard, workspace and exchange lines -- the same body and the same exchange protocol as the per-GPU
+// launch, in ONE cooperative grid so that the ranks' spins on each other's lines are co-resident.
+struct TmaMulti {
+  TmaParams rp[kMaxRanks];
+  int base[kMaxRanks + 1];
+  int nv;
+};
+template <int CPT, int EPT, int KS>
+__global__ void __launch_bounds__(416, 1) k_iter_tma_emu(const __grid_constant__ TmaMulti pm) {
+  int v = 0;
+  while (v + 1 < pm.nv && (int)blockIdx.x >= pm.base[v + 1]) ++v;
+  iter_tma_body<CPT, EPT, KS>(pm.rp[v], (int)blockIdx.x - pm.base[v], pm.base[v + 1] - pm.base[v]);
+}
+
 // ------------------------------------------------------------------------------------------ launcher
 bool tma_eligible(const IterArgs& a) {
   return a.dtype == COT_F32 && a.B == 1 && a.m % 4 == 0 && a.m <= 1024 && !(a.flags & COT_FORCE_LDG);
 }
 
-cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, bool rows_only, int parity,
-                            cudaStream_t s) {
-  const int sms = device_sm_count();
-  TmaParams p;
+namespace {
+struct TmaCfg {
+  int cpt, ept, KS, threads, grid;
+  size_t smem;
+  void* fn;       // k_iter_tma instance
+  void* fn_emu;   // k_iter_tma_emu instance
+};
+
+// Parameters + launch configuration of the persistent kernel for one (shard of a) problem on `sms` SMs.
+cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool rows_only, int parity, int sms,
+                       TmaParams* pp, TmaCfg* cfg) {
+  TmaParams& p = *pp;
+  memset(&p, 0, sizeof(p));
   p.C = static_cast<const float*>(a.C);
   p.G = static_cast<const float*>(a.G);
   p.alpha = a.alpha;
@@ -711,73 +953,109 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
   p.U = (int)up.U;
   // ---- warp roles: k-sum warps (4 columns x CPT per thread, <= 8 warps), epilogue warps (4 x EPT)
   const int m = (int)a.m, mv = m / 4;
+  // Warp roles (13 warps at m = 1024, 128 registers): a long k-sum per row (n >= 16: the HBM-bound stream)
+  // gets 8 k-sum warps and 4 epilogue warps (2 float4 each); a short one (latency-bound: the epilogue and
+  // the device-wide steps dominate) gets 4 k-sum warps (2 float4 each) and 8 epilogue warps.
+  const bool long_ksum = getenv("COT_LONG_KSUM") ? atoi(getenv("COT_LONG_KSUM")) != 0 : a.n >= 16;
+  const int kmax = long_ksum ? 8 : 4;
   int cpt = 1;
-  while ((mv + 32 * cpt - 1) / (32 * cpt) > 8) cpt *= 2;
+  while ((mv + 32 * cpt - 1) / (32 * cpt) > kmax) cpt *= 2;
   p.nk = (mv + 32 * cpt - 1) / (32 * cpt);
-  p.ne = std::max(std::max(1, p.nk / 2), (mv + 63) / 64);   // <= 2 float4 per epilogue thread
+  p.ne = std::max(1, std::min(long_ksum ? 4 : 8, (mv + 31) / 32));
   if (const char* ev = getenv("COT_NE")) p.ne = std::max(1, std::min(8, atoi(ev)));   // tuning experiments
   int ept = 1;
   while ((mv + 32 * p.ne - 1) / (32 * p.ne) > ept) ept *= 2;
-  if (cpt > 1 || ept > 2) return cudaErrorInvalidValue;
+  if (cpt > 2 || ept > 2 || (cpt == 2 && ept == 2)) return cudaErrorInvalidValue;
   // ---- TMA ring and row queue
   const int row_bytes = m * 4;
   int KS = 1;
-  int ks_bytes = 65536;
+  int ks_bytes = 32768;   // 32 KB slots: >= 4 in flight per SM at m = 1024 (measured best on C4)
   if (const char* ev = getenv("COT_SLOT_BYTES")) ks_bytes = atoi(ev);   // tuning experiments
   while (KS * 2 <= 16 && KS * 2 * row_bytes <= ks_bytes && KS * 2 <= (int)a.n) KS *= 2;
   p.KS = KS;
   const size_t slot_bytes = (size_t)p.KS * row_bytes;
   p.qn = std::max(1, std::min(p.rpu, 8));
   if (const char* ev = getenv("COT_QN")) p.qn = std::max(1, atoi(ev));
-  const size_t queue_bytes = (size_t)p.qn * row_bytes + (size_t)p.rpu * 4 * 8;
+  p.qn = std::max(p.qn, std::min(p.rpu, 4));   // the epilogue holds up to one batch (<= 4 rows) of queue slots
+  const size_t gsh_bytes = (size_t)p.rpu * m * 8;   // -G/eps in fp64
+  p.gsh = gsh_bytes <= 64 * 1024 && !getenv("COT_NO_GSH");
+  const size_t queue_bytes = (size_t)p.qn * row_bytes + (p.gsh ? gsh_bytes : 0) + (size_t)p.rpu * 6 * 8 +
+                             (size_t)kColScratch * 8;
   const size_t budget = 220 * 1024;
   if (queue_bytes + 2 * slot_bytes + 4096 > budget) return cudaErrorInvalidConfiguration;
   p.nslot = (int)std::max<size_t>(2, std::min<size_t>(64, (budget - queue_bytes - 4096) / slot_bytes));
   // ring + 1 KiB pad (branch-free over-reads past the last column stay in-bounds) + row queue + row
   // statistics + barriers + control + reduction scratch
-  const size_t smem = (size_t)p.nslot * slot_bytes + 1024 + queue_bytes + ((size_t)p.nslot + p.qn) * 16 + 64 +
-                      128 * 8 + 64;
+  cfg->smem = (size_t)p.nslot * slot_bytes + 1024 + queue_bytes + ((size_t)p.nslot + p.qn) * 16 + 64 + 128 * 8 + 64;
   p.iters = rows_only ? 1 : iters;
   p.rows_only = rows_only ? 1 : 0;
   p.tol = a.tol;
   p.check_every = a.check_every > 0 ? a.check_every : 1;
-  p.partials = ws.partials[rows_only ? (parity & 1) : 0];
-  p.resid_part = ws.resid_part;
+  p.partials = ws.partials[parity & 1];
   p.state = ws.state;
-  p.bar = ws.grid_bar;
+  p.plines = ws.plines;
+  p.zlines = ws.zlines;
+  p.rlines = ws.rlines;
+  p.lepoch = ws.lepoch;
+  p.lcap = ws.lcap;
+  if (!rows_only && (!ws.plines || up.U > ws.lcap)) return cudaErrorInvalidValue;
   p.evict_last_rows = 0;
   p.diag = (int)(a.flags & (COT_DIAG_NO_COMPUTE | COT_DIAG_NO_SYNC));
   p.pre = (a.flags & COT_PRECOMPUTED) ? 1 : 0;
   if (const char* ev = getenv("COT_EVICT_LAST_ROWS")) p.evict_last_rows = atoi(ev);   // L2 residency experiment
   p.trace = nullptr;
+  p.nranks = 0;
+  cfg->threads = (p.nk + p.ne + 1) * 32;
+  cfg->grid = (int)up.U;
+  cfg->cpt = cpt;
+  cfg->ept = ept;
+  cfg->KS = KS;
+  cfg->fn = cfg->fn_emu = nullptr;
+#define COT_PICK(C_, E_, K_)                     \
+  if (cpt == C_ && ept == E_ && KS == K_) {      \
+    cfg->fn = (void*)k_iter_tma<C_, E_, K_>;     \
+    cfg->fn_emu = (void*)k_iter_tma_emu<C_, E_, K_>; \
+  }
+#define COT_PICK_K(C_, E_) \
+  COT_PICK(C_, E_, 1) COT_PICK(C_, E_, 2) COT_PICK(C_, E_, 4) COT_PICK(C_, E_, 8) COT_PICK(C_, E_, 16)
+  COT_PICK_K(1, 1) COT_PICK_K(1, 2) COT_PICK_K(2, 1)
+#undef COT_PICK_K
+#undef COT_PICK
+  if (!cfg->fn) return cudaErrorInvalidValue;
+  return cudaSuccess;
+}
+
+cudaError_t check_occupancy(void* fn, int threads, size_t smem, int grid, int sms) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  if (grid > occ * sms) return cudaErrorInvalidConfiguration;   // one unit per co-resident CTA
+  return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, bool rows_only, int parity,
+                            cudaStream_t s) {
+  const int sms = device_sm_count();
+  TmaParams p;
+  TmaCfg cfg;
+  cudaError_t e = tma_config(a, ws, iters, rows_only, parity, sms, &p, &cfg);
+  if (e != cudaSuccess) return e;
   static unsigned long long* trace_buf = nullptr;   // diagnostics only (COT_TRACE=1)
   if (getenv("COT_TRACE")) {
     if (!trace_buf) cudaMalloc(&trace_buf, 4096 * 8 * sizeof(unsigned long long));
     cudaMemsetAsync(trace_buf, 0, 4096 * 8 * sizeof(unsigned long long), s);
     p.trace = trace_buf;
   }
-  const int threads = (p.nk + p.ne + 2) * 32;
-  cudaError_t e;
-  void* fn = nullptr;
-#define COT_PICK(C_, E_, K_) \
-  if (cpt == C_ && ept == E_ && KS == K_) fn = (void*)k_iter_tma<C_, E_, K_>;
-#define COT_PICK_K(C_, E_) \
-  COT_PICK(C_, E_, 1) COT_PICK(C_, E_, 2) COT_PICK(C_, E_, 4) COT_PICK(C_, E_, 8) COT_PICK(C_, E_, 16)
-  COT_PICK_K(1, 1) COT_PICK_K(1, 2)
-#undef COT_PICK_K
-#undef COT_PICK
-  if (!fn) return cudaErrorInvalidValue;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = check_occupancy(cfg.fn, cfg.threads, cfg.smem, cfg.grid, sms);
   if (e != cudaSuccess) return e;
-  int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
-  if (e != cudaSuccess) return e;
-  if (occ < 1) return cudaErrorInvalidConfiguration;
-  if (up.U > (int64_t)occ * sms) return cudaErrorInvalidConfiguration;   // one unit per co-resident CTA
-  const int grid = (int)up.U;
+  const int grid = cfg.grid;
   void* args[] = {&p};
-  if (rows_only) return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, s);
-  e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, s);
+  if (rows_only) return cudaLaunchKernel(cfg.fn, dim3(grid), dim3(cfg.threads), args, cfg.smem, s);
+  e = cudaLaunchCooperativeKernel(cfg.fn, dim3(grid), dim3(cfg.threads), args, cfg.smem, s);
   if (e == cudaSuccess && p.trace) {   // diagnostics: print cycle breakdown (averaged over CTAs)
     std::vector<unsigned long long> h((size_t)grid * 8);
     cudaStreamSynchronize(s);
@@ -791,11 +1069,65 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
     const double it = iters > 0 ? iters : 1;
     fprintf(stderr,
             "[cot trace] iters=%d per-iter cycles (mean/max over CTAs): prod_wait %.0f/%.0f prod_total %.0f/%.0f "
-            "ksum %.0f/%.0f epi_busy %.0f/%.0f epi_wait_z %.0f/%.0f\n",
+            "ksum %.0f/%.0f epi_busy %.0f/%.0f epi_wait_z %.0f/%.0f [epi: compute %.0f reduce %.0f; colpass %.0f]\n",
             iters, acc[0] / it, mx[0] / it, acc[1] / it, mx[1] / it, acc[3] / it, mx[3] / it, acc[4] / it,
-            mx[4] / it, acc[5] / it, mx[5] / it);
+            mx[4] / it, acc[5] / it, mx[5] / it, acc[2] / it, acc[6] / it, acc[7] / it);
   }
   return e;
+}
+
+int fused_column_slices(int64_t m, int nranks, int sms) {
+  // the smallest unit count of a balanced row partition (rows per rank = floor or ceil of m / nranks)
+  const int64_t lo = m / nranks, hi = (m + nranks - 1) / nranks;
+  int64_t ncs = unit_plan(1, hi, sms).U;
+  if (lo >= 1) ncs = std::min<int64_t>(ncs, unit_plan(1, lo, sms).U);
+  return (int)ncs;
+}
+
+cudaError_t launch_iter_tma_fused(const FusedRank* r, int nv, int nranks, bool emulate, int iters, cudaStream_t s) {
+  if (nv < 1 || nv > kMaxRanks || nranks < 1 || nranks > kMaxRanks || (emulate && nv != nranks) ||
+      (!emulate && nv != 1))
+    return cudaErrorInvalidValue;
+  const int sms_dev = device_sm_count();
+  const int sms = emulate ? sms_dev / nranks : sms_dev;   // emulation: each virtual rank gets 1/nranks of the SMs
+  if (sms < 1) return cudaErrorInvalidConfiguration;
+  TmaMulti pm;
+  memset(&pm, 0, sizeof(pm));
+  TmaCfg cfg0;
+  int ncs = emulate ? 1 << 30 : fused_column_slices(r[0].a.m, nranks, sms);
+  size_t smem = 0;
+  pm.nv = nv;
+  pm.base[0] = 0;
+  for (int v = 0; v < nv; ++v) {
+    TmaCfg cfg;
+    cudaError_t e = tma_config(r[v].a, r[v].ws, iters, false, 0, sms, &pm.rp[v], &cfg);
+    if (e != cudaSuccess) return e;
+    if (v == 0) cfg0 = cfg;
+    if (cfg.fn != cfg0.fn || cfg.threads != cfg0.threads) return cudaErrorInvalidValue;   // same instance
+    smem = std::max(smem, cfg.smem);
+    pm.base[v + 1] = pm.base[v] + cfg.grid;
+    if (emulate) ncs = std::min(ncs, cfg.grid);
+    else if (cfg.grid < ncs) return cudaErrorInvalidValue;   // the caller's rows are not a balanced partition
+    TmaParams& p = pm.rp[v];
+    p.nranks = nranks;
+    p.rank = r[v].rank;
+    for (int q = 0; q < nranks; ++q) p.xpeer[q] = r[v].xpeer[q];
+    p.xepoch = r[v].xepoch;
+    // a shard whose cost rows fit comfortably in L2 is kept there across iterations
+    if (!emulate && (double)(r[v].a.n + 1) * r[v].a.R * r[v].a.m * 4.0 <= 80e6) p.evict_last_rows = (int)r[v].a.R;
+  }
+  for (int v = 0; v < nv; ++v) pm.rp[v].ncs = ncs;
+  const int grid = pm.base[nv];
+  if (!emulate) {
+    cudaError_t e = check_occupancy(cfg0.fn, cfg0.threads, smem, grid, sms_dev);
+    if (e != cudaSuccess) return e;
+    void* args[] = {&pm.rp[0]};
+    return cudaLaunchCooperativeKernel(cfg0.fn, dim3(grid), dim3(cfg0.threads), args, smem, s);
+  }
+  cudaError_t e = check_occupancy(cfg0.fn_emu, cfg0.threads, smem, grid, sms_dev);
+  if (e != cudaSuccess) return e;
+  void* args[] = {&pm};
+  return cudaLaunchCooperativeKernel(cfg0.fn_emu, dim3(grid), dim3(cfg0.threads), args, smem, s);
 }
 
 }  // namespace cot

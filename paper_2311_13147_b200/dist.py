@@ -9,6 +9,13 @@
 
 The communicator is bootstrapped through torch.distributed: rank 0 creates the 128-byte ncclUniqueId with
 cot_nccl_unique_id, it is broadcast as a uint8 tensor, and every rank calls cot_comm_init.
+
+* Fused row sharding (the default multi-GPU path of bench.py): the same partition and arithmetic, but the
+  exchange step runs inside the persistent iteration kernel (cerot_iter_fused): each rank's column sums are
+  written straight into every rank's exchange buffer over NVLink (CUDA IPC peer mappings set up once by
+  `PeerExchange`; the 64-byte handles travel through torch.distributed) and summed in rank order on every
+  rank. `emulate_fused` runs all ranks' fused iterations as one cooperative launch on one GPU (the test
+  harness of the protocol when fewer GPUs than ranks are available).
 """
 from __future__ import annotations
 
@@ -19,7 +26,8 @@ import numpy as np
 
 from . import (COT_COLD_START, REPORT_FIELDS, _check, _dtype_code, _ptr, _stream, lib)
 
-__all__ = ["row_partition", "problem_partition", "broadcast_bytes", "NcclComm", "ShardedCerot"]
+__all__ = ["row_partition", "problem_partition", "broadcast_bytes", "allgather_bytes", "NcclComm",
+           "PeerExchange", "ShardedCerot", "emulate_fused"]
 
 
 def row_partition(m: int, world: int, rank: int) -> Tuple[int, int]:
@@ -47,6 +55,55 @@ def broadcast_bytes(payload: Optional[bytes], nbytes: int, src: int = 0, group=N
         t.copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
     dist.broadcast(t, src=src, group=group)
     return bytes(t.cpu().numpy().tobytes())
+
+
+def allgather_bytes(payload: bytes, group=None, device=None) -> list:
+    """Every rank's `payload` (same length on every rank), in rank order (gloo or nccl)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = torch.frombuffer(bytearray(payload), dtype=torch.uint8).to(device or "cpu")
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    return [bytes(o.cpu().numpy().tobytes()) for o in out]
+
+
+class PeerExchange:
+    """This rank's exchange buffer of the fused path plus every other rank's, mapped with CUDA IPC.
+
+    xbufs is the HOST array of device pointers cerot_iter_fused takes: entry q = rank q's buffer as
+    addressed by this process (entry `rank` = the local buffer). Collective: every rank constructs it."""
+
+    def __init__(self, m: int, group=None):
+        import torch
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.local = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        _check(lib().cot_xchg_alloc(m, self.world, ctypes.byref(self.local), handle), "cot_xchg_alloc")
+        self.opened = []
+        ptrs = [None] * self.world
+        ptrs[self.rank] = self.local.value
+        if self.world > 1:
+            dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else None
+            handles = allgather_bytes(handle.raw, group, dev)
+            for q, h in enumerate(handles):
+                if q == self.rank:
+                    continue
+                pq = ctypes.c_void_p()
+                _check(lib().cot_xchg_open(ctypes.create_string_buffer(h, 64), ctypes.byref(pq)), "cot_xchg_open")
+                self.opened.append(pq)
+                ptrs[q] = pq.value
+        self.xbufs = (ctypes.c_void_p * self.world)(*ptrs)
+
+    def close(self):
+        for pq in self.opened:
+            lib().cot_xchg_close(pq)
+        self.opened = []
+        if self.local:
+            lib().cot_xchg_free(self.local)
+            self.local = ctypes.c_void_p()
 
 
 class NcclComm:
@@ -123,6 +180,15 @@ class ShardedCerot:
                                         self._comm, _stream(self.stream)), "cerot_iter_sharded")
         return self
 
+    def iterate_fused(self, xchg: "PeerExchange", iters: int, tol: float = 0.0, check_every: int = 1,
+                      flags: int = 0):
+        """`iters` iterations with the exchange inside the persistent kernel (cerot_iter_fused)."""
+        _check(lib().cerot_iter_fused(_ptr(self.alpha), _ptr(self.beta), _ptr(self.C), _ptr(self.G), self.n, self.m,
+                                      self.row_begin, self.R, self.dt, _ptr(self.eps), iters, tol, check_every, flags,
+                                      _ptr(self.w_hat), _ptr(self.z_hat), _ptr(self.ws), self.ws.numel(), xchg.world,
+                                      xchg.rank, xchg.xbufs, _stream(self.stream)), "cerot_iter_fused")
+        return self
+
     # the two halves, for callers that reduce the column sums themselves (emulation, tests)
     def rows(self, flags: int = 0):
         _check(lib().cerot_rows_shard(_ptr(self.alpha), _ptr(self.C), _ptr(self.G), self.n, self.m, self.row_begin,
@@ -162,6 +228,39 @@ class ShardedCerot:
         _check(lib().cerot_state(_ptr(self.ws), 1, self.m, self.n, self.dt, it, cv, rs, _stream(self.stream)),
                "cerot_state")
         return int(it[0]), int(cv[0]), float(rs[0])
+
+
+def emulate_fused(shards, iters: int, tol: float = 0.0, check_every: int = 1, flags: int = 0, xbufs=None,
+                  stream=None):
+    """All ranks' fused iterations in ONE cooperative launch on one GPU (cerot_iter_fused_emulated).
+
+    shards: list of ShardedCerot (rank order, one device, balanced partition). xbufs: per-rank exchange
+    buffers from cot_xchg_alloc (allocated here when None; returned so that later calls reuse them -- the
+    epoch inside each buffer must keep advancing)."""
+    V = len(shards)
+    L = lib()
+    if xbufs is None:
+        xbufs = []
+        for _ in range(V):
+            b = ctypes.c_void_p()
+            _check(L.cot_xchg_alloc(shards[0].m, V, ctypes.byref(b), None), "cot_xchg_alloc")
+            xbufs.append(b.value)
+    P = ctypes.c_void_p
+    arr = lambda xs: (P * V)(*xs)
+    s0 = shards[0]
+    _check(L.cerot_iter_fused_emulated(
+        V, _ptr(s0.alpha), _ptr(s0.beta), arr([_ptr(s.C) for s in shards]), arr([_ptr(s.G) for s in shards]),
+        s0.n, s0.m, (ctypes.c_int64 * V)(*[s.row_begin for s in shards]), (ctypes.c_int64 * V)(*[s.R for s in shards]),
+        s0.dt, _ptr(s0.eps), iters, tol, check_every, flags, arr([_ptr(s.w_hat) for s in shards]),
+        arr([_ptr(s.z_hat) for s in shards]), arr([_ptr(s.ws) for s in shards]),
+        (ctypes.c_size_t * V)(*[s.ws.numel() for s in shards]), arr(xbufs), _stream(stream)),
+        "cerot_iter_fused_emulated")
+    return xbufs
+
+
+def free_xbufs(xbufs):
+    for b in xbufs or []:
+        lib().cot_xchg_free(b)
 
 
 def report_dict(rep) -> dict:

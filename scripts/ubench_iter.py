@@ -10,7 +10,7 @@ import torch
 import paper_2311_13147_b200 as cot
 import synthetic
 
-p = synthetic.c4_large()
+p = synthetic.c3_image() if os.environ.get("WL") == "C3" else synthetic.c4_large(m=int(os.environ.get("M", "1024")), n=int(os.environ.get("N", "64")))
 dev = torch.device("cuda:0")
 C = torch.as_tensor(p.C, device=dev)
 prob = cot.CerotProblem(C, torch.as_tensor(p.alpha, device=dev), torch.as_tensor(p.beta, device=dev), p.eps)
