@@ -100,7 +100,7 @@ cudaError_t launch_init(const double* alpha, const double* beta, int64_t B, int6
 cudaError_t launch_rows(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int parity, cudaStream_t s);
 // Column pass (deterministic reduction + q-update + monitor) reading ws.partials[parity].
 cudaError_t launch_cols(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int parity, cudaStream_t s);
-bool tma_eligible(const IterArgs& a);
+bool tma_eligible(const IterArgs& a, int sms = 0);   // sms: SMs the launch may use (0: all)
 // Cluster-resident small problems (fp32, m <= 256, m % 4 == 0): `iters` full iterations of every problem.
 bool batch_cluster_eligible(const IterArgs& a);
 cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int iters, cudaStream_t s);

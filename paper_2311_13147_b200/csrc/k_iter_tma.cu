@@ -202,34 +202,54 @@ __device__ __forceinline__ double exp_split(double d) {
   return (double)ex2(f) * __longlong_as_double(e << 52);
 }
 
-// s * e^d for d in fp64 (|d| < ~700) and s in fp32: 2^round(d log2e) built exactly in the exponent bits,
-// times s * 2^frac (|frac| <= 1/2) in fp32 with MUFU.EX2, so the rounding of the argument costs < 3e-8
-// relative regardless of |d|. Three conversions per call; the round uses the 1.5*2^52 trick (no F2I).
+// s * e^d for d in fp64 and s in fp32: 2^round(d log2e) built exactly in the exponent bits (the round by the
+// 1.5*2^52 trick, valid for |d| < 1e15), times s * 2^frac (|frac| <= 1/2) in fp32 with MUFU.EX2, so the
+// rounding of the argument costs < 3e-8 relative regardless of |d|. The exponent is clamped to
+// [-1022, 1000]: terms below 2^-1022 come out ~1e-308 (negligible), terms above 2^1000 make the caller's
+// row-sum range check redo the row exactly. Two conversions, no branch.
 __device__ __forceinline__ double exp_scaled(double d, float s) {
-  // below 2^-1022 the term is negligible; above 2^1000 the caller's range check redoes the row exactly
-  const double a = fmin(fmax(d * COT_LOG2E, -1022.0), 1000.0);
+  const double a = d * COT_LOG2E;
   const double big = a + 6755399441055744.0;
-  const int ai = __double2loint(big);
+  const int ai = min(max(__double2loint(big), -1022), 1000);
   const float f = (float)(a - (big - 6755399441055744.0));
   return (double)(s * ex2(f)) * __hiloint2double((ai + 1023) << 20, 0);
 }
 
 // One-barrier block reductions of N values over the epilogue warps (<= 8 warps; double-buffered scratch).
+// The sums use a transposed butterfly: at the first levels each lane keeps half of its values and sends the
+// other half, so N = 4 rows cost 6 double shuffles per warp instead of 20 (fixed order: deterministic).
 template <int N>
 __device__ __forceinline__ void cblk_sumN(double* v, double* red2, int& buf, int nct, int wbase) {
+  static_assert(N == 2 || N == 4, "row batches of 2 or 4");
   const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) - wbase;
   double* r = red2 + buf * 64;
+  int row;
+  double k;
+  if (N == 4) {
+    const bool hi = lane & 16;
+    const double s0 = __shfl_xor_sync(0xffffffffu, hi ? v[0] : v[2], 16);
+    const double s1 = __shfl_xor_sync(0xffffffffu, hi ? v[1] : v[3], 16);
+    const double k0 = (hi ? v[2] : v[0]) + s0, k1 = (hi ? v[3] : v[1]) + s1;   // rows 2hi, 2hi+1
+    const bool h8 = lane & 8;
+    k = (h8 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+    row = (hi ? 2 : 0) + (h8 ? 1 : 0);
 #pragma unroll
-  for (int k = 0; k < N; ++k) {
-    const double x = warp_sum(v[k]);
-    if (lane == 0) r[k * 8 + wid] = x;
+    for (int o = 4; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    if ((lane & 7) == 0) r[row * 8 + wid] = k;
+  } else {
+    const bool hi = lane & 16;
+    k = (hi ? v[1] : v[0]) + __shfl_xor_sync(0xffffffffu, hi ? v[0] : v[1], 16);
+    row = hi ? 1 : 0;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    if ((lane & 15) == 0) r[row * 8 + wid] = k;
   }
   cbar(nct);
 #pragma unroll
-  for (int k = 0; k < N; ++k) {
-    double x = r[k * 8];
-    for (int w = 1; w < (nct >> 5); ++w) x += r[k * 8 + w];
-    v[k] = x;
+  for (int q = 0; q < N; ++q) {
+    double x = r[q * 8];
+    for (int w = 1; w < (nct >> 5); ++w) x += r[q * 8 + w];
+    v[q] = x;
   }
   buf ^= 1;
 }
@@ -642,34 +662,45 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
           }
         }
         const long long te0 = p.trace ? clock64() : 0;
-        // element (b, q, v): s_ij from the queue, x_ij = z_j - G_ij/eps
-        auto sval = [&](int b, int q, int v) -> float { return queue[(size_t)qsb[b] * m + VEC * (q * net + et) + v]; };
-        auto xval = [&](int b, int q, int v) -> double {
-          const int j = VEC * (q * net + et) + v;
-          return z[q][v] + (p.gsh ? gsh[(size_t)(r0 + b) * m + j] : -(double)__ldg(p.G + (size_t)(i0 + r0 + b) * m + j) * inv_eps);
-        };
-        // ---- the row epilogues: t_ij = s_ij exp(x_ij - Mref_i) with Mref_i the row's log-sum-exp of the
-        // previous iteration (so x - Mref <= ~log(n m) unless z jumped); r_i = sum_j t_ij in one block
-        // reduction for the batch. A batch with a row sum outside [1e-280, 1e280] (no reference yet, or a jump
-        // of the potentials) is redone in the exact two-pass form (maximum first).
+#pragma unroll
+        for (int b = 1; b < RB; ++b)
+          if (b >= nb) qsb[b] = qsb[0];          // branch-free: unused rows read a valid slot, masked below
+        // ---- the row epilogues: t_ij = s_ij exp(x_ij - Mref_i), x_ij = z_j - G_ij/eps, with Mref_i the row's
+        // log-sum-exp of the previous iteration (so x - Mref <= ~log(n m) unless z jumped); r_i = sum_j t_ij
+        // in one block reduction for the batch. A batch with a row sum outside [1e-280, 1e280] (no reference
+        // yet, or a jump of the potentials) is redone in the exact two-pass form (maximum first).
         double Mref[RB], sm[RB], tt[RB][EPT][VEC];
 #pragma unroll
         for (int b = 0; b < RB; ++b) {
-          Mref[b] = b < nb ? rowstat[(r0 + b) * RS + 0] : 0.0;
+          Mref[b] = rowstat[(r0 + (b < nb ? b : 0)) * RS + 0];
           sm[b] = 0.0;
         }
         const bool stale = Mref[0] == Mref[0];      // the CTA's rows get their references together
+        auto batch_terms = [&](bool use) {
 #pragma unroll
-        for (int b = 0; b < RB; ++b)
+          for (int b = 0; b < RB; ++b) {
+            const int rb = r0 + (b < nb ? b : 0);
 #pragma unroll
-          for (int q = 0; q < EPT; ++q) {
-            const bool ok = q * net + et < mv && b < nb && stale;
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) {
-              tt[b][q][v] = ok ? exp_scaled(xval(b, q, v) - Mref[b], sval(b, q, v)) : 0.0;
-              sm[b] += tt[b][q][v];
+            for (int q = 0; q < EPT; ++q) {
+              const int jv = q * net + et;
+              const bool ok = use && jv < mv && b < nb;
+              const int jc = jv < mv ? jv : 0;
+              const float4 s4 = reinterpret_cast<const VT*>(queue + (size_t)qsb[b] * m)[jc];
+              const double2* g2 = reinterpret_cast<const double2*>(gsh + (size_t)rb * m) + 2 * jc;
+              const double2 ga = g2[0], gb = g2[1];
+              const double t0 = exp_scaled(z[q][0] + ga.x - Mref[b], s4.x);
+              const double t1 = exp_scaled(z[q][1] + ga.y - Mref[b], s4.y);
+              const double t2 = exp_scaled(z[q][2] + gb.x - Mref[b], s4.z);
+              const double t3 = exp_scaled(z[q][3] + gb.y - Mref[b], s4.w);
+              tt[b][q][0] = ok ? t0 : 0.0;
+              tt[b][q][1] = ok ? t1 : 0.0;
+              tt[b][q][2] = ok ? t2 : 0.0;
+              tt[b][q][3] = ok ? t3 : 0.0;
+              sm[b] += (tt[b][q][0] + tt[b][q][1]) + (tt[b][q][2] + tt[b][q][3]);
             }
           }
+        };
+        batch_terms(stale);
         const long long te1 = p.trace ? clock64() : 0;
         cblk_sumN<RB>(sm, red2, rbuf, net, nk);
         if (p.trace) {
@@ -684,27 +715,22 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
 #pragma unroll
           for (int b = 0; b < RB; ++b) {
             mx[b] = -INFINITY;
+            const int rb = r0 + (b < nb ? b : 0);
 #pragma unroll
             for (int q = 0; q < EPT; ++q)
 #pragma unroll
-              for (int v = 0; v < VEC; ++v)
-                if (q * net + et < mv && b < nb) mx[b] = fmax(mx[b], xval(b, q, v));
+              for (int v = 0; v < VEC; ++v) {
+                const int jv = q * net + et;
+                if (jv < mv && b < nb) mx[b] = fmax(mx[b], z[q][v] + gsh[(size_t)rb * m + VEC * jv + v]);
+              }
           }
           cblk_maxN<RB>(mx, red2, rbuf, net, nk);
 #pragma unroll
           for (int b = 0; b < RB; ++b) {
             Mref[b] = b < nb ? mx[b] : 0.0;
             sm[b] = 0.0;
-#pragma unroll
-            for (int q = 0; q < EPT; ++q) {
-              const bool ok = q * net + et < mv && b < nb;
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) {
-                tt[b][q][v] = ok ? exp_scaled(xval(b, q, v) - Mref[b], sval(b, q, v)) : 0.0;
-                sm[b] += tt[b][q][v];
-              }
-            }
           }
+          batch_terms(true);
           cblk_sumN<RB>(sm, red2, rbuf, net, nk);
         }
         // release the batch's queue slots
@@ -920,8 +946,11 @@ __global__ void __launch_bounds__(416, 1) k_iter_tma_emu(const __grid_constant__
 }
 
 // ------------------------------------------------------------------------------------------ launcher
-bool tma_eligible(const IterArgs& a) {
-  return a.dtype == COT_F32 && a.B == 1 && a.m % 4 == 0 && a.m <= 1024 && !(a.flags & COT_FORCE_LDG);
+bool tma_eligible(const IterArgs& a, int sms) {
+  if (sms <= 0) sms = device_sm_count();
+  const int64_t rpu = unit_plan(1, a.R, sms).rpu;   // -G/eps of a CTA's rows (fp64) is staged in <= 64 KB
+  return a.dtype == COT_F32 && a.B == 1 && a.m % 4 == 0 && a.m <= 1024 && rpu * a.m * 8 <= 65536 &&
+         !(a.flags & COT_FORCE_LDG);
 }
 
 namespace {
@@ -978,7 +1007,8 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
   if (const char* ev = getenv("COT_QN")) p.qn = std::max(1, atoi(ev));
   p.qn = std::max(p.qn, std::min(p.rpu, 4));   // the epilogue holds up to one batch (<= 4 rows) of queue slots
   const size_t gsh_bytes = (size_t)p.rpu * m * 8;   // -G/eps in fp64
-  p.gsh = gsh_bytes <= 64 * 1024 && !getenv("COT_NO_GSH");
+  p.gsh = 1;
+  if (gsh_bytes > 64 * 1024) return cudaErrorInvalidConfiguration;   // see tma_eligible
   const size_t queue_bytes = (size_t)p.qn * row_bytes + (p.gsh ? gsh_bytes : 0) + (size_t)p.rpu * 6 * 8 +
                              (size_t)kColScratch * 8;
   const size_t budget = 220 * 1024;

@@ -93,3 +93,49 @@ def test_row_sharded_decomposition_gloo():
         assert np.abs(zh * eps - z).max() < 1e-12       # z replicated and equal to the unsharded iterate
         assert np.abs(wh * eps - w).max() < 1e-12       # union of the held rows' w = the unsharded w
     assert np.array_equal(out[0][0], out[1][0])         # bitwise identical q-updates on both ranks
+
+
+def _worker_fused(rank, world, port, out):
+    """Host logic of the fused path (cerot_iter_fused): the 64-byte IPC handles travel with allgather_bytes;
+    each rank's column sums reach every rank (the kernel's peer stores; all_gather here) and are summed in
+    RANK ORDER on every rank, so the q-updates are bitwise identical although the data are split unevenly."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        handles = cdist.allgather_bytes(bytes([rank]) * 64)
+        assert handles == [bytes([q]) * 64 for q in range(world)]
+        p = synthetic.random_cyclic(seed=7, n=4, m=20, eps=0.05)
+        eps = float(p.eps[0])
+        C = p.C.astype(np.float64)
+        b0, R = cdist.row_partition(p.m, world, rank)
+        assert R in (p.m // world, -(-p.m // world))       # the balanced partition cerot_iter_fused requires
+        rows = slice(b0, b0 + R)
+        zh = np.zeros(p.m)
+        for _ in range(20):
+            X = zh[None, None, :] - C[:, rows, :] / eps
+            mx = X.max(axis=(0, 2))
+            wh_loc = np.log(p.alpha[rows]) - mx - np.log(np.exp(X - mx[None, :, None]).sum(axis=(0, 2)))
+            c_loc = torch.from_numpy(np.exp(wh_loc[None, :, None] + X).sum(axis=(0, 1)))
+            lines = [torch.empty_like(c_loc) for _ in range(world)]
+            dist.all_gather(lines, c_loc)                       # every rank's lines of every slice
+            c = np.zeros(p.m)
+            for q in range(world):                              # rank order, as the kernel sums them
+                c = c + lines[q].numpy()
+            zh = zh + np.log(p.beta) - np.log(c)
+        out[rank] = zh
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_exchange_rank_order_gloo():
+    world = 3
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_fused, args=(world, port, out), nprocs=world, join=True)
+    p = synthetic.random_cyclic(seed=7, n=4, m=20, eps=0.05)
+    _, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 20)
+    for r in range(world):
+        assert np.array_equal(out[r], out[0])                  # bitwise identical on every rank
+    assert np.abs(out[0] * float(p.eps[0]) - z).max() < 1e-12
