@@ -228,7 +228,8 @@ int cerot_plan_sharded(const double* alpha, const double* beta, const void* C_lo
 /* then reads all ranks' lines of slice b from its own buffer and sums them in rank order, so c_j and the */
 /* q-update (Alg. 2 line 5) are bitwise identical on every rank. No NCCL call and no host          */
 /* round trip per iteration. Requirements: fp32 C, m % 4 == 0, m <= 1024, nranks <= COT_MAX_RANKS, a     */
-/* balanced contiguous row partition (R = floor or ceil of m / nranks), every rank launching the same     */
+/* balanced contiguous row partition (R = floor or ceil of m / nranks; any R when nranks == 1, which runs */
+/* one shard alone with the exchange to itself), every rank launching the same                          */
 /* `iters` (a peer that never arrives makes the call's state report COT_E_PEER after 20 s).              */
 #define COT_MAX_RANKS 8
 /* Bytes of one rank's exchange buffer: a 256-byte header (the iteration epoch) + [2][nranks][m] lines.  */

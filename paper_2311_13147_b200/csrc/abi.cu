@@ -708,7 +708,7 @@ static int fused_rank_args(const double* alpha, const double* beta, const void* 
   if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
     return arg_error("fused sharding: need 1 <= nranks <= COT_MAX_RANKS and 0 <= rank < nranks");
   if (R < 1 || row_begin < 0 || row_begin + R > m) return arg_error("fused sharding: bad row range");
-  if (R != m / nranks && R != (m + nranks - 1) / nranks)
+  if (nranks > 1 && R != m / nranks && R != (m + nranks - 1) / nranks)
     return arg_error("fused sharding: R must be floor or ceil of m / nranks (balanced partition)");
   if (!alpha || !beta || !C_local || !G_local || !eps || !w_hat || !z_hat || !xbufs)
     return arg_error("fused sharding: NULL argument");

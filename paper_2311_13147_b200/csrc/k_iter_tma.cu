@@ -408,8 +408,8 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       }
     producer_done:
       if (p.trace) {
-        p.trace[bid * 8 + 0] = prod_wait;
-        p.trace[bid * 8 + 1] = clock64() - tp0;
+        p.trace[bid * 16 + 0] = prod_wait;
+        p.trace[bid * 16 + 1] = clock64() - tp0;
       }
     }
     if (lane == 0) {
@@ -426,7 +426,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
     const float c2 = (float)(COT_LOG2E * inv_eps);
     uint32_t slot = 0, phase = 0, qs = 0, qph = 0;
     unsigned consumed = 0, produced = 0;
-    long long c_ksum = 0;
+    long long c_ksum = 0, c_kqw = 0;
     VT gnext[CPT];
     auto load_g = [&](int row) {
 #pragma unroll
@@ -515,7 +515,9 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       }
       if (p.trace) c_ksum += clock64() - tk0;
       // ---- hand the row's k-sums to the epilogue warps through the queue
+      const long long tqe = p.trace ? clock64() : 0;
       mbar_wait(&qempty[qs], qph ^ 1u);
+      if (p.trace) c_kqw += clock64() - tqe;
       VT* qrow = reinterpret_cast<VT*>(queue + (size_t)qs * m);
 #pragma unroll
       for (int q = 0; q < CPT; ++q) {
@@ -531,7 +533,10 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       ++produced;
       if (kt == 0) *(volatile unsigned*)&ctl[6] = produced;
     }
-    if (p.trace && kt == 0) p.trace[bid * 8 + 3] = c_ksum;
+    if (p.trace && kt == 0) {
+      p.trace[bid * 16 + 3] = c_ksum;
+      p.trace[bid * 16 + 9] = c_kqw;
+    }
     asm volatile("bar.sync 3, %0;" ::"r"(nkt) : "memory");
     if (kt == 0) {
       __threadfence_block();
@@ -575,7 +580,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
     uint32_t qs = 0, qph = 0;
     unsigned consumed = 0;
     int rbuf = 0;
-    long long c_epi = 0, c_wait = 0, c_cmp = 0, c_red = 0, c_col = 0;
+    long long c_epi = 0, c_wait = 0, c_cmp = 0, c_red = 0, c_col = 0, c_qw = 0, c_cp1 = 0, c_pub = 0;
     bool timeout = false;
     const bool have_ref = p.state[0].iters > 0;   // w_hat holds the previous iteration's p-update
     for (int r = et; r < nrows; r += net) {
@@ -613,6 +618,8 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       }
       return cblk_sum1(v, red2, rbuf, net, nk);
     };
+    // log beta_j of the first 8 columns of this CTA's slice (the usual whole slice), once per launch
+    const double lbeta0 = (sync && et < 8 && col0 + et < col1) ? log(p.beta[col0 + et]) : 0.0;   // no beta: rows_only
     int done = 0;   // iterations completed (q-update applied) in this launch
     bool halted = false;
     for (int t = 0; active0 && t < p.iters; ++t) {
@@ -649,6 +656,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         uint32_t qsb[RB];
         {
           uint32_t q2 = qs, ph2 = qph;
+          const long long tq0 = p.trace ? clock64() : 0;
 #pragma unroll
           for (int b = 0; b < RB; ++b) {
             qsb[b] = q2;
@@ -660,6 +668,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
               }
             }
           }
+          if (p.trace) c_qw += clock64() - tq0;
         }
         const long long te0 = p.trace ? clock64() : 0;
 #pragma unroll
@@ -679,6 +688,13 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         auto batch_terms = [&](bool use) {
 #pragma unroll
           for (int b = 0; b < RB; ++b) {
+            if (b >= nb) {   // CTA-uniform: short batches (e.g. one row per CTA) skip the unused rows
+#pragma unroll
+              for (int q = 0; q < EPT; ++q)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) tt[b][q][v] = 0.0;
+              continue;
+            }
             const int rb = r0 + (b < nb ? b : 0);
 #pragma unroll
             for (int q = 0; q < EPT; ++q) {
@@ -791,6 +807,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         ++done;
         continue;
       }
+      const long long tp0 = p.trace ? clock64() : 0;
       // ---- publish the column partial of iteration t as LL lines of generation g1
       const unsigned g1 = (unsigned)(lep0 + t + 1);
       {
@@ -808,6 +825,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       }
       // ---- column pass of this CTA's slice: c_j = sum_u P_uj in unit order; q-update; z lines
       const long long tc0 = p.trace ? clock64() : 0;
+      if (p.trace) c_pub += tc0 - tp0;
       double dev = 0.0;
       const uint4* plr = p.plines + (size_t)(g1 & 1u) * p.lcap * m;
       for (int cb = col0; cb < col1; cb += 8) {
@@ -829,12 +847,16 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
             acc += v;
           }
         }
+        if (p.trace) c_cp1 += clock64() - tc0;
+        // groups of a warp (lanes c, c+8, c+16, c+24) by two shuffle levels, then the warps in order
+        acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
         asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");   // previous chunk's readers of xs are done
-        xs[grp * 8 + c] = acc;
+        if (lane < 8) xs[(grp >> 2) * 8 + c] = acc;
         asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
         double cj = 0.0;
         if (et < 8) {
-          for (int g2 = 0; g2 < ngrp; ++g2) cj += xs[g2 * 8 + et];
+          for (int w2 = 0; w2 < (ngrp >> 2); ++w2) cj += xs[w2 * 8 + et];
         }
         if (fused) {
           // ---- the exchange step across GPUs: this rank's slice sums -> every rank's x-lines (NVLink peer
@@ -862,7 +884,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
           const double bj = p.beta[j];
           dev += fabs(cj - bj);
           if (!(cj >= 1e-28)) atomicOr(&p.state[0].flags, (int)STATE_UNDERFLOW);
-          const double zj = __ldcg(p.z_hat + j) + (log(bj) - log(cj));
+          const double zj = __ldcg(p.z_hat + j) + ((cb == col0 ? lbeta0 : log(bj)) - log(cj));
           p.z_hat[j] = zj;
           st_line(p.zlines + j, ll_pack(zj, g1));
         }
@@ -896,11 +918,14 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
     }
     if (timeout) atomicOr(&p.state[0].flags, (int)STATE_PEER_TIMEOUT);
     if (p.trace && et == 0) {
-      p.trace[bid * 8 + 4] = c_epi;
-      p.trace[bid * 8 + 5] = c_wait;
-      p.trace[bid * 8 + 2] = c_cmp;
-      p.trace[bid * 8 + 6] = c_red;
-      p.trace[bid * 8 + 7] = c_col;
+      p.trace[bid * 16 + 4] = c_epi;
+      p.trace[bid * 16 + 5] = c_wait;
+      p.trace[bid * 16 + 2] = c_cmp;
+      p.trace[bid * 16 + 6] = c_red;
+      p.trace[bid * 16 + 7] = c_col;
+      p.trace[bid * 16 + 8] = c_qw;
+      p.trace[bid * 16 + 10] = c_cp1;
+      p.trace[bid * 16 + 11] = c_pub;
     }
     // ---- drain the queue after a halt: consume every row the k-sum warps still produce
     while (true) {
@@ -985,7 +1010,8 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
   // Warp roles (13 warps at m = 1024, 128 registers): a long k-sum per row (n >= 16: the HBM-bound stream)
   // gets 8 k-sum warps and 4 epilogue warps (2 float4 each); a short one (latency-bound: the epilogue and
   // the device-wide steps dominate) gets 4 k-sum warps (2 float4 each) and 8 epilogue warps.
-  const bool long_ksum = getenv("COT_LONG_KSUM") ? atoi(getenv("COT_LONG_KSUM")) != 0 : a.n >= 16;
+  const bool long_ksum =
+      getenv("COT_LONG_KSUM") ? atoi(getenv("COT_LONG_KSUM")) != 0 : a.n * unit_plan(1, a.R, sms).rpu >= 128;
   const int kmax = long_ksum ? 8 : 4;
   int cpt = 1;
   while ((mv + 32 * cpt - 1) / (32 * cpt) > kmax) cpt *= 2;
@@ -1067,6 +1093,36 @@ cudaError_t check_occupancy(void* fn, int threads, size_t smem, int grid, int sm
 }
 }  // namespace
 
+namespace {
+// Diagnostics (COT_TRACE=1): per-CTA cycle counters of one persistent launch, printed as means / maxima.
+unsigned long long* trace_begin(cudaStream_t s) {
+  static unsigned long long* trace_buf = nullptr;
+  if (!getenv("COT_TRACE")) return nullptr;
+  if (!trace_buf) cudaMalloc(&trace_buf, 4096 * 16 * sizeof(unsigned long long));
+  cudaMemsetAsync(trace_buf, 0, 4096 * 16 * sizeof(unsigned long long), s);
+  return trace_buf;
+}
+void trace_end(const unsigned long long* trace, int grid, int iters, cudaStream_t s) {
+  std::vector<unsigned long long> h((size_t)grid * 16);
+  cudaStreamSynchronize(s);
+  cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
+  double acc[16] = {0}, mx[16] = {0};
+  for (int b = 0; b < grid; ++b)
+    for (int k = 0; k < 16; ++k) {
+      acc[k] += (double)h[(size_t)b * 16 + k] / grid;
+      mx[k] = std::max(mx[k], (double)h[(size_t)b * 16 + k]);
+    }
+  const double it = iters > 0 ? iters : 1;
+  fprintf(stderr,
+          "[cot trace] iters=%d per-iter cycles (mean/max over CTAs): prod_wait %.0f/%.0f prod_total %.0f/%.0f "
+          "ksum %.0f/%.0f epi_busy %.0f/%.0f epi_wait_z %.0f/%.0f [epi: compute %.0f reduce %.0f; colpass %.0f; "
+          "queue wait %.0f/%.0f; ksum queue wait %.0f; colpass poll %.0f; publish %.0f]\n",
+          iters, acc[0] / it, mx[0] / it, acc[1] / it, mx[1] / it, acc[3] / it, mx[3] / it, acc[4] / it,
+          mx[4] / it, acc[5] / it, mx[5] / it, acc[2] / it, acc[6] / it, acc[7] / it, acc[8] / it, mx[8] / it,
+          acc[9] / it, acc[10] / it, acc[11] / it);
+}
+}  // namespace
+
 cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, bool rows_only, int parity,
                             cudaStream_t s) {
   const int sms = device_sm_count();
@@ -1074,35 +1130,14 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
   TmaCfg cfg;
   cudaError_t e = tma_config(a, ws, iters, rows_only, parity, sms, &p, &cfg);
   if (e != cudaSuccess) return e;
-  static unsigned long long* trace_buf = nullptr;   // diagnostics only (COT_TRACE=1)
-  if (getenv("COT_TRACE")) {
-    if (!trace_buf) cudaMalloc(&trace_buf, 4096 * 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(trace_buf, 0, 4096 * 8 * sizeof(unsigned long long), s);
-    p.trace = trace_buf;
-  }
+  p.trace = trace_begin(s);
   e = check_occupancy(cfg.fn, cfg.threads, cfg.smem, cfg.grid, sms);
   if (e != cudaSuccess) return e;
   const int grid = cfg.grid;
   void* args[] = {&p};
   if (rows_only) return cudaLaunchKernel(cfg.fn, dim3(grid), dim3(cfg.threads), args, cfg.smem, s);
   e = cudaLaunchCooperativeKernel(cfg.fn, dim3(grid), dim3(cfg.threads), args, cfg.smem, s);
-  if (e == cudaSuccess && p.trace) {   // diagnostics: print cycle breakdown (averaged over CTAs)
-    std::vector<unsigned long long> h((size_t)grid * 8);
-    cudaStreamSynchronize(s);
-    cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost);
-    double acc[8] = {0}, mx[8] = {0};
-    for (int b = 0; b < grid; ++b)
-      for (int k = 0; k < 8; ++k) {
-        acc[k] += (double)h[(size_t)b * 8 + k] / grid;
-        mx[k] = std::max(mx[k], (double)h[(size_t)b * 8 + k]);
-      }
-    const double it = iters > 0 ? iters : 1;
-    fprintf(stderr,
-            "[cot trace] iters=%d per-iter cycles (mean/max over CTAs): prod_wait %.0f/%.0f prod_total %.0f/%.0f "
-            "ksum %.0f/%.0f epi_busy %.0f/%.0f epi_wait_z %.0f/%.0f [epi: compute %.0f reduce %.0f; colpass %.0f]\n",
-            iters, acc[0] / it, mx[0] / it, acc[1] / it, mx[1] / it, acc[3] / it, mx[3] / it, acc[4] / it,
-            mx[4] / it, acc[5] / it, mx[5] / it, acc[2] / it, acc[6] / it, acc[7] / it);
-  }
+  if (e == cudaSuccess && p.trace) trace_end(p.trace, grid, iters, s);
   return e;
 }
 
@@ -1124,7 +1159,8 @@ cudaError_t launch_iter_tma_fused(const FusedRank* r, int nv, int nranks, bool e
   TmaMulti pm;
   memset(&pm, 0, sizeof(pm));
   TmaCfg cfg0;
-  int ncs = emulate ? 1 << 30 : fused_column_slices(r[0].a.m, nranks, sms);
+  // column slices: identical on every rank (nranks == 1: any row range, the slices of this launch)
+  int ncs = emulate || nranks == 1 ? 1 << 30 : fused_column_slices(r[0].a.m, nranks, sms);
   size_t smem = 0;
   pm.nv = nv;
   pm.base[0] = 0;
@@ -1136,7 +1172,7 @@ cudaError_t launch_iter_tma_fused(const FusedRank* r, int nv, int nranks, bool e
     if (cfg.fn != cfg0.fn || cfg.threads != cfg0.threads) return cudaErrorInvalidValue;   // same instance
     smem = std::max(smem, cfg.smem);
     pm.base[v + 1] = pm.base[v] + cfg.grid;
-    if (emulate) ncs = std::min(ncs, cfg.grid);
+    if (emulate || nranks == 1) ncs = std::min(ncs, cfg.grid);
     else if (cfg.grid < ncs) return cudaErrorInvalidValue;   // the caller's rows are not a balanced partition
     TmaParams& p = pm.rp[v];
     p.nranks = nranks;
@@ -1151,8 +1187,11 @@ cudaError_t launch_iter_tma_fused(const FusedRank* r, int nv, int nranks, bool e
   if (!emulate) {
     cudaError_t e = check_occupancy(cfg0.fn, cfg0.threads, smem, grid, sms_dev);
     if (e != cudaSuccess) return e;
+    pm.rp[0].trace = trace_begin(s);
     void* args[] = {&pm.rp[0]};
-    return cudaLaunchCooperativeKernel(cfg0.fn, dim3(grid), dim3(cfg0.threads), args, smem, s);
+    e = cudaLaunchCooperativeKernel(cfg0.fn, dim3(grid), dim3(cfg0.threads), args, smem, s);
+    if (e == cudaSuccess && pm.rp[0].trace) trace_end(pm.rp[0].trace, grid, iters, s);
+    return e;
   }
   cudaError_t e = check_occupancy(cfg0.fn_emu, cfg0.threads, smem, grid, sms_dev);
   if (e != cudaSuccess) return e;

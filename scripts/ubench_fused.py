@@ -36,10 +36,24 @@ def main():
     ap.add_argument("--n", type=int, default=64)
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--ranks", default="1,2,4,8")
+    ap.add_argument("--shard-alone", type=int, default=0,
+                    help="G > 0: run rank 0's shard of a G-way row partition ALONE on this GPU (cerot_iter_fused, "
+                         "nranks = 1, exchange with itself): the per-GPU work and local sync of a G-GPU run, "
+                         "without the NVLink latency")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     p = synthetic.c4_large(m=a.m, n=a.n)
     D = lambda x: torch.as_tensor(np.ascontiguousarray(x), device=dev)
+    if a.shard_alone:
+        G = a.shard_alone
+        b0, R = cdist.row_partition(p.m, G, 0)
+        sh = cdist.ShardedCerot(D(p.C[:, b0:b0 + R, :]), D(p.alpha), D(p.beta), float(p.eps[0]), b0, p.m)
+        x = cdist.PeerExchange(p.m)
+        ms = timed(lambda: sh.init().iterate_fused(x, a.iters))
+        print(json.dumps({"mode": f"shard_alone_1_of_{G}", "rows": R, "m": a.m, "n": a.n,
+                          "us_per_iter": ms * 1e3 / a.iters}))
+        x.close()
+        return
     prob = cot.CerotProblem(D(p.C), D(p.alpha), D(p.beta), p.eps)
     ms = timed(lambda: prob.init().iterate(a.iters))
     print(json.dumps({"mode": "unsharded", "m": a.m, "n": a.n, "us_per_iter": ms * 1e3 / a.iters}))
