@@ -262,6 +262,17 @@ int cerot_iter_fused_emulated(int nranks, const double* alpha, const double* bet
                               void* const* workspace, const size_t* ws_bytes, void* const* xbufs, void* stream);
 
 /* ---------------------------------------------------------------------------------------------- */
+/* NEXT-4: the small LOT of Theorem 1 (eq. small_problem_CLOT; Alg. 1 line 2), the paper's     */
+/* serial step, on the HOST: min <G, S> s.t. S 1 = alpha, S^T 1 = beta, S >= 0 by the primal network     */
+/* simplex method with exact integer flows (masses scaled to 2^50) and the       */
+/* strongly feasible pivot rule. All pointers HOST, row-major fp64: alpha, beta [m] (> 0, equal sums to  */
+/* 1e-6 relative), G [m][m] finite; outputs S [m][m] (a vertex: <= 2m-1 non-zeros), *value = <G, S>, and  */
+/* (optional, may be NULL) dual potentials u, v [m] with u_i + v_j <= G_ij, equality where S_ij > 0, and  */
+/* the pivot count. Synchronous, single-threaded, no device work; thread-safe on distinct buffers.        */
+int clot_small_lot(const double* alpha, const double* beta, const double* G, int64_t m, double* S,
+                   double* value, double* u, double* v, int64_t* pivots);
+
+/* ---------------------------------------------------------------------------------------------- */
 /* NEXT-3: C-SROT, strongly convex regularised OT through the 2m-variable Fenchel dual        */
 /* (Theorem 2) by alternating maximisation: each sweep solves every w_i with z fixed, then     */
 /* every z_j with w fixed, by safeguarded Newton on the monotone derivative; the plan is      */

@@ -18,6 +18,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -42,6 +45,7 @@ struct BatchParams {
   double tol;
   long long check_every;
   int pre;               // precomputed mode (NEXT-1): C is S [B][1][m][m], s_ij = S_ij
+  unsigned long long* trace;   // diagnostics (COT_TRACE=1): [grid][8] cycle counters, or nullptr
 };
 
 template <int VPL>
@@ -186,7 +190,9 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
   ksum_range(0, n);                                         // k-sums of iteration 0
   int t = 0;
   bool stop = false;
+  long long tr[6] = {0, 0, 0, 0, 0, 0};
   for (; t < p.iters && !stop; ++t) {
+    const long long c0t = p.trace ? clock64() : 0;
     // ================= epilogues of iteration t (z_hat of iteration t-1 is complete in the replica)
     double P[VPL][4];
 #pragma unroll
@@ -241,6 +247,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
 #pragma unroll
         for (int v = 0; v < 4; ++v) wpart[(size_t)warp * m + 4 * jv + v] = P[q][v];
     }
+    const long long c1t = p.trace ? clock64() : 0;
     __syncthreads();
     for (int j = threadIdx.x; j < m; j += blockDim.x) {   // CTA partial: warps in order
       double acc = 0.0;
@@ -248,11 +255,14 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
       cpart[j] = acc;
     }
     // ================= B1: publish the CTA partial; stream the first half of the next k-sums meanwhile
+    const long long c2t = p.trace ? clock64() : 0;
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     const bool more = t + 1 < p.iters;
     zero_s();
     if (more) ksum_range(0, khalf);
+    const long long c3t = p.trace ? clock64() : 0;
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const long long c4t = p.trace ? clock64() : 0;
     // ================= column pass of this CTA's slice: one thread per (column, source CTA), the 8 values
     //                   combined by a fixed xor tree (deterministic), q-update written to every replica
     const bool need = (p.tol > 0.0 && (st.iters + 1) % p.check_every == 0) || t == p.iters - 1;
@@ -289,9 +299,20 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
       }
     }
     // ================= B2: the q-update is in every replica; stream the second half meanwhile
+    const long long c5t = p.trace ? clock64() : 0;
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     if (more) ksum_range(khalf, n);
+    const long long c6t = p.trace ? clock64() : 0;
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (p.trace) {
+      const long long c7t = clock64();
+      tr[0] += c1t - c0t;   // epilogues
+      tr[1] += c2t - c1t;   // CTA partial
+      tr[2] += c3t - c2t;   // first k-sum half
+      tr[3] += c4t - c3t;   // B1 wait
+      tr[4] += (c5t - c4t) + (c7t - c6t);   // column pass + B2 wait
+      tr[5] += c6t - c5t;   // second k-sum half
+    }
     st.iters += 1;
     if (need) {
       double rr = 0.0;
@@ -321,6 +342,8 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
     out.converged = st.converged;
     p.state[b] = out;
   }
+  if (p.trace && threadIdx.x == 0 && b < 256)
+    for (int k = 0; k < 6; ++k) p.trace[(size_t)blockIdx.x * 8 + k] = tr[k];
   cluster.sync();   // no CTA leaves while others may still read its shared memory
 }
 
@@ -371,8 +394,27 @@ cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int ite
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  static unsigned long long* trace_buf = nullptr;   // diagnostics only (COT_TRACE=1)
+  p.trace = nullptr;
+  if (getenv("COT_TRACE")) {
+    if (!trace_buf) cudaMalloc(&trace_buf, 256 * kNCL * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace_buf, 0, 256 * kNCL * 8 * sizeof(unsigned long long), s);
+    p.trace = trace_buf;
+  }
   void* args[] = {&p};
-  return cudaLaunchKernelExC(&cfg, fn, args);
+  e = cudaLaunchKernelExC(&cfg, fn, args);
+  if (e == cudaSuccess && p.trace) {
+    const int ctas = (int)std::min<int64_t>(a.B, 256) * kNCL;
+    std::vector<unsigned long long> h((size_t)ctas * 8);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    double acc[6] = {0};
+    for (int c = 0; c < ctas; ++c)
+      for (int k = 0; k < 6; ++k) acc[k] += (double)h[(size_t)c * 8 + k] / ctas / std::max(iters, 1);
+    fprintf(stderr, "[cot batch trace] per-iter cycles: epilogue %.0f cta_partial %.0f ksum1 %.0f B1_wait %.0f "
+            "colpass+B2_wait %.0f ksum2 %.0f\n", acc[0], acc[1], acc[2], acc[3], acc[4], acc[5]);
+  }
+  return e;
 }
 
 }  // namespace cot

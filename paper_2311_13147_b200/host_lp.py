@@ -1,5 +1,6 @@
 """The small LOT of Theorem 1 (eq. small_problem_CLOT): Alg. 1 line 2, the paper's serial step,
-run host-side and outside the hot path (BASELINE.json north_star). HiGHS (scipy) is the LP library used.
+run host-side and outside the hot path (BASELINE.json north_star). The solver is libcyclicot's host C++
+primal network simplex (clot_small_lot, NEXT-4; the algorithm the paper names).
 
 clot_solve() chains the device kernels around it: clot_aggregate (GPU) -> G to host -> LP -> S* to device
 -> clot_expand (GPU). The LP is the only host computation; nothing here is part of the timed hot path.
@@ -7,24 +8,30 @@ clot_solve() chains the device kernels around it: clot_aggregate (GPU) -> G to h
 from __future__ import annotations
 
 import numpy as np
-import scipy.optimize
-import scipy.sparse
 
 from . import clot_aggregate, clot_expand
 
 
-def small_lot(alpha: np.ndarray, beta: np.ndarray, G: np.ndarray):
-    """min <G, S> s.t. S 1 = alpha, S^T 1 = beta, S >= 0 (HiGHS). Returns (value, S) in fp64."""
-    m = G.shape[0]
-    rows = scipy.sparse.kron(scipy.sparse.eye(m), np.ones((1, m)))
-    cols = scipy.sparse.kron(np.ones((1, m)), scipy.sparse.eye(m))
-    A_eq = scipy.sparse.vstack([rows, cols]).tocsr()
-    res = scipy.optimize.linprog(np.asarray(G, np.float64).ravel(), A_eq=A_eq,
-                                 b_eq=np.concatenate([alpha, beta]), bounds=(0, None), method="highs")
-    if res.status != 0:
-        raise RuntimeError(f"small LOT failed: {res.message}")
-    S = np.maximum(res.x.reshape(m, m), 0.0)
-    return float(np.asarray(G, np.float64).ravel() @ res.x), S
+def small_lot(alpha: np.ndarray, beta: np.ndarray, G: np.ndarray, duals: bool = False):
+    """min <G, S> s.t. S 1 = alpha, S^T 1 = beta, S >= 0 by the network simplex (clot_small_lot, host C++).
+    Returns (value, S) in fp64, plus (u, v, pivots) when duals=True."""
+    import ctypes
+    from . import _check, lib
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    b = np.ascontiguousarray(beta, dtype=np.float64)
+    Gc = np.ascontiguousarray(G, dtype=np.float64)
+    m = Gc.shape[0]
+    S = np.zeros((m, m))
+    u = np.zeros(m)
+    v = np.zeros(m)
+    val = ctypes.c_double()
+    piv = ctypes.c_int64()
+    P = lambda x: x.ctypes.data_as(ctypes.c_void_p)
+    _check(lib().clot_small_lot(P(a), P(b), P(Gc), m, P(S), ctypes.byref(val), P(u), P(v), ctypes.byref(piv)),
+           "clot_small_lot")
+    if duals:
+        return float(val.value), S, u, v, int(piv.value)
+    return float(val.value), S
 
 
 def clot_solve(C, alpha: np.ndarray, beta: np.ndarray, expand: bool = True, stream=None):
