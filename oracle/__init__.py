@@ -12,3 +12,4 @@ from .core import *        # noqa: F401,F403
 from .lot import *         # noqa: F401,F403
 from .sinkhorn import *    # noqa: F401,F403
 from .srot import *        # noqa: F401,F403
+from .twostage import *    # noqa: F401,F403

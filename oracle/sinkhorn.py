@@ -25,18 +25,19 @@ def lse(x: np.ndarray, axis) -> np.ndarray:
 # ----------------------------------------------------------------------------------------------
 # full Sinkhorn on the explicit d x d problem (the plain definition of the EROT iteration)
 # ----------------------------------------------------------------------------------------------
-def sinkhorn_full(a, b, C, eps, iters, tol=0.0, check_every=1, record=False):
+def sinkhorn_full(a, b, C, eps, iters, tol=0.0, check_every=1, record=False, g0=None):
     """Original Sinkhorn (Alg. 3 stage 2; Cuturi 2013) in the log domain of
     eq. optimal_f_sinkhorn_logdomain (P:403-411) with n = 1:
         f_I = eps (log a_I - log sum_J exp((g_J - C_IJ)/eps))      [p <- a / (K q)]
         g_J = eps (log b_J - log sum_I exp((f_I - C_IJ)/eps))      [q <- b / (K^T p)]
-    starting from q = 1 (g = 0). Stops after `iters` iterations, or earlier when tol > 0 and the
+    starting from q = 1 (g = 0), or from q = exp(g0/eps) (Alg. 3 line 11: stage 2 starts from the
+    concatenated stage-1 scalings). Stops after `iters` iterations, or earlier when tol > 0 and the
     column residual sum_J |T^T 1 - b|_J of the row-exact plan (after the f-update) is <= tol,
     checked every `check_every` iterations. Returns (f, g, iterations_done, history)."""
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
     C = np.asarray(C, dtype=np.float64)
-    g = np.zeros(C.shape[1])
+    g = np.zeros(C.shape[1]) if g0 is None else np.asarray(g0, dtype=np.float64).copy()
     f = np.zeros(C.shape[0])
     hist = []
     t = 0

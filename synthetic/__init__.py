@@ -25,7 +25,7 @@ import numpy as np
 
 __all__ = [
     "Problem", "c1_tiny", "c2_ring", "c3_image", "c4_large", "c5_batched", "appd_synthetic",
-    "counter_example", "random_cyclic", "CONFIGS", "make",
+    "counter_example", "random_cyclic", "approx_symmetric", "CONFIGS", "make",
 ]
 
 
@@ -231,6 +231,20 @@ def c3_image(seed: int = 3, H: int = 64, pair: int = 0) -> Problem:
     C = C64.astype(np.float32)
     return Problem(f"C3_image_pair{pair}", C, alpha, beta, np.array([1e-2]), iters=500, tol=0.0,
                    meta={"seed": seed, "pair": pair, "H": H})
+
+
+def approx_symmetric(p: Problem, noise: float = 0.05, seed: int = 7):
+    """NEXT-2 inputs (Alg. 3): full-length marginals a, b in Delta^d that are only
+    APPROXIMATELY periodic -- the tiled alpha, beta of `p` times (1 + noise * U(-1, 1)) per entry,
+    renormalised to sum 1 (images with "slight noise and displacement"). The cost blocks of `p` stay
+    strictly block-circulant. Stands in for Table 2's NYU mirror images (not available). Returns (a, b)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for v in (p.alpha, p.beta):
+        t = np.tile(np.asarray(v, dtype=np.float64), p.n)
+        t = t * (1.0 + noise * rng.uniform(-1.0, 1.0, size=t.shape))
+        out.append(t / t.sum())
+    return out[0], out[1]
 
 
 def c4_large(seed: int = 4, m: int = 1024, n: int = 64) -> Problem:
