@@ -262,6 +262,26 @@ int cerot_iter_fused_emulated(int nranks, const double* alpha, const double* bet
                               void* const* workspace, const size_t* ws_bytes, void* const* xbufs, void* stream);
 
 /* ---------------------------------------------------------------------------------------------- */
+/* NEXT-2: the two-stage Sinkhorn algorithm for C-EROT with APPROXIMATE cyclic symmetry (Algorithm 3,    */
+/* P:457-484). a, b: DEVICE [d] fp64 (d = n*m; in the simplex, only approximately n-periodic); C: DEVICE  */
+/* [n][m][m] the blocks of the strictly block-circulant cost; eps DEVICE [1].                    */
+/*   stage 1 (lines 2-10): alpha, beta = fold averages of a, b, cyclic Sinkhorn of the hot   */
+/*     path from q^ = 1 for iters1 iterations or until its monitor (n*sum|c - beta|) <= tol1;  */
+/*     w_hat, z_hat DEVICE [m] receive its eps-scaled potentials;                                         */
+/*   stage 2 (lines 11-16): the original Sinkhorn on the explicit d x d problem from g = concatenated     */
+/*     z_hat, without materialising the d x d cost (each CTA stages the n block rows C_k[i][:] once and   */
+/*     serves the n rows r*m + i); iters2 iterations or until sum_J |T^T 1 - b|_J of the row-exact plan   */
+/*     <= tol2 (checked every check_every); f_hat, g_hat DEVICE [d] eps-scaled potentials (out).         */
+/*   report (HOST, FULL-problem values, no factor n): transport cost, regularised primal, dual, marginal  */
+/*     residuals and mass of T = diag(p) K diag(q) (line 17); iters_done HOST [2] = stage-1, stage-2      */
+/*     iterations. Synchronises. Returns COT_NOT_CONVERGED if tol2 > 0 was not reached.                   */
+size_t cot_two_stage_workspace_bytes(int64_t n, int64_t m, int dtype);
+int cerot_two_stage(const double* a, const double* b, const void* C, int64_t n, int64_t m, int dtype,
+                    const double* eps, int64_t iters1, double tol1, int64_t iters2, double tol2,
+                    int64_t check_every, double* f_hat, double* g_hat, double* w_hat, double* z_hat,
+                    void* workspace, size_t ws_bytes, cot_report* report, int64_t* iters_done, void* stream);
+
+/* ---------------------------------------------------------------------------------------------- */
 /* NEXT-4: the small LOT of Theorem 1 (eq. small_problem_CLOT; Alg. 1 line 2), the paper's     */
 /* serial step, on the HOST: min <G, S> s.t. S 1 = alpha, S^T 1 = beta, S >= 0 by the primal network     */
 /* simplex method with exact integer flows (masses scaled to 2^50) and the       */

@@ -75,6 +75,11 @@ _SIGS = {
                                           _i64, _u32, _vp, _vp, _vp, _sz, _vp, _vp]),
     "cerot_plan_sharded": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp,
                                           _vp, _vp, _vp, _sz, _vp, _vp]),
+    # NEXT-2: two-stage Sinkhorn (Alg. 3)
+    "cot_two_stage_workspace_bytes": (_sz, [_i64, _i64, ctypes.c_int]),
+    "cerot_two_stage": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl, _i64, _dbl, _i64,
+                                       _vp, _vp, _vp, _vp, _vp, _sz, ctypes.POINTER(cot_report),
+                                       ctypes.POINTER(_i64), _vp]),
     # NEXT-4: host network simplex for the small LOT (host pointers)
     "clot_small_lot": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, ctypes.POINTER(_dbl), _vp, _vp,
                                       ctypes.POINTER(_i64)]),
@@ -332,3 +337,30 @@ def csrot_solve(C, alpha, beta, gamma, tol=0.0, max_sweeps=1000, check_every=1, 
         d.update(iters=r.iters, converged=bool(r.converged), status=STATUS[r.status])
         out.append(d)
     return w, z, T, out
+
+
+def two_stage_sinkhorn(a, b, C, eps, iters1, iters2, tol1=0.0, tol2=0.0, check_every=1, stream=None):
+    """NEXT-2: Algorithm 3 on the device (cerot_two_stage). a, b: device [d] fp64 (approximately
+    n-periodic), C: device [n][m][m]. Returns (f_hat, g_hat [d], w_hat, z_hat [m], report dict) with
+    eps-scaled potentials; report values are full-problem (no factor n)."""
+    import torch
+    n, m = C.shape[0], C.shape[1]
+    dt = _dtype_code(C)
+    dev = C.device
+    a = a.to(torch.float64).contiguous()
+    b = b.to(torch.float64).contiguous()
+    eps_t = torch.as_tensor(eps, dtype=torch.float64, device=dev).reshape(1).contiguous()
+    f = torch.zeros(n * m, dtype=torch.float64, device=dev)
+    g = torch.zeros_like(f)
+    w = torch.zeros(m, dtype=torch.float64, device=dev)
+    z = torch.zeros_like(w)
+    ws = torch.empty(int(lib().cot_two_stage_workspace_bytes(n, m, dt)), dtype=torch.uint8, device=dev)
+    rep = cot_report()
+    its = (ctypes.c_int64 * 2)()
+    code = lib().cerot_two_stage(_ptr(a), _ptr(b), _ptr(C), n, m, dt, _ptr(eps_t), iters1, tol1, iters2, tol2,
+                                 check_every, _ptr(f), _ptr(g), _ptr(w), _ptr(z), _ptr(ws), ws.numel(),
+                                 ctypes.byref(rep), its, _stream(stream))
+    _check(code, "cerot_two_stage", ok=(0, 1))
+    d = {k: getattr(rep, k) for k in REPORT_FIELDS}
+    d.update(iters1=int(its[0]), iters2=int(its[1]), converged=bool(rep.converged), status=STATUS[rep.status])
+    return f, g, w, z, d

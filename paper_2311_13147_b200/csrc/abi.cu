@@ -463,6 +463,157 @@ int cerot_solve(const double* alpha, const double* beta, const void* C, int64_t 
   return all_conv ? COT_OK : COT_NOT_CONVERGED;
 }
 
+// ------------------------------------------------------------------------------------- NEXT-2: two-stage
+static size_t two_stage_layout(int64_t n, int64_t m, int dtype, char* base, size_t* off_red, double** alpha,
+                               double** beta, void** Bt, double** dev, double** mon, double** rep_rows,
+                               double** rep_cols, double** report) {
+  const size_t esz = dtype == COT_F32 ? 4 : 8;
+  const int64_t d = n * m;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = (off + bytes + 255) / 256 * 256;
+    return base ? base + o : nullptr;
+  };
+  *off_red = off;
+  take(carve_workspace(nullptr, 1, n, m, m, dtype, device_sm_count(), nullptr));
+  *alpha = reinterpret_cast<double*>(take((size_t)m * 8));
+  *beta = reinterpret_cast<double*>(take((size_t)m * 8));
+  *Bt = take((size_t)n * m * m * esz);
+  *dev = reinterpret_cast<double*>(take((size_t)d * 8));
+  *mon = reinterpret_cast<double*>(take(8));
+  *rep_rows = reinterpret_cast<double*>(take((size_t)3 * d * 8));
+  *rep_cols = reinterpret_cast<double*>(take((size_t)3 * d * 8));
+  *report = reinterpret_cast<double*>(take(kReportDoubles * 8));
+  return off;
+}
+
+// Reduced C-EROT iterations on one problem with the state checks of cerot_solve; returns COT_* status.
+static int iterate_reduced(const IterArgs& a, const Workspace& ws, void* workspace, int64_t n, int64_t m, int dtype,
+                           int64_t max_iter, double tol, int64_t check_every, cudaStream_t s) {
+  const UnitPlan up = unit_plan(1, m, device_sm_count());
+  int64_t done = 0;
+  int64_t it = 0;
+  int32_t conv = 0;
+  double res = 0.0;
+  while (done < max_iter) {
+    const int64_t chunk = std::min<int64_t>(check_every, max_iter - done);
+    if (batch_cluster_eligible(a)) {
+      COT_CHECK_CUDA(launch_batch_cluster(a, ws, (int)chunk, s));
+    } else if (tma_eligible(a)) {
+      COT_CHECK_CUDA(launch_iter_tma(a, ws, (int)chunk, false, 0, s));
+    } else {
+      for (int64_t t = 0; t < chunk; ++t) {
+        COT_CHECK_CUDA(launch_rows(a, ws, up, (int)((done + t) & 1), s));
+        COT_CHECK_CUDA(launch_cols(a, ws, up, (int)((done + t) & 1), s));
+      }
+    }
+    done += chunk;
+    if (tol > 0.0) {
+      const int st = cerot_state(workspace, 1, m, n, dtype, &it, &conv, &res, s);
+      if (st) return st;
+      if (conv) break;
+    }
+  }
+  return COT_OK;
+}
+
+size_t cot_two_stage_workspace_bytes(int64_t n, int64_t m, int dtype) {
+  if (n < 1 || m < 1 || (dtype != COT_F32 && dtype != COT_F64)) return 0;
+  size_t o;
+  double *al, *be, *dv, *mo, *rr, *rc, *rp;
+  void* bt;
+  return two_stage_layout(n, m, dtype, nullptr, &o, &al, &be, &bt, &dv, &mo, &rr, &rc, &rp);
+}
+
+int cerot_two_stage(const double* a, const double* b, const void* C, int64_t n, int64_t m, int dtype, const double* eps,
+                    int64_t iters1, double tol1, int64_t iters2, double tol2, int64_t check_every, double* f_hat,
+                    double* g_hat, double* w_hat, double* z_hat, void* workspace, size_t ws_bytes,
+                    cot_report* report, int64_t* iters_done, void* stream) {
+  int st = check_shape(1, n, m, dtype);
+  if (st) return st;
+  if (!a || !b || !C || !eps || !f_hat || !g_hat || !w_hat || !z_hat)
+    return arg_error("cerot_two_stage: NULL argument");
+  if (iters1 < 0 || iters2 < 0 || tol1 < 0 || tol2 < 0) return arg_error("cerot_two_stage: negative count or tol");
+  if (check_every < 1) check_every = 1;
+  const size_t need = cot_two_stage_workspace_bytes(n, m, dtype);
+  if (!workspace || ws_bytes < need || reinterpret_cast<uintptr_t>(workspace) % 256) {
+    set_error("cerot_two_stage: workspace too small or misaligned: need " + std::to_string(need));
+    return COT_E_WORKSPACE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  char* base = static_cast<char*>(workspace);
+  size_t off_red;
+  double *alpha, *beta, *dev, *mon, *rep_rows, *rep_cols, *rep;
+  void* Bt;
+  two_stage_layout(n, m, dtype, base, &off_red, &alpha, &beta, &Bt, &dev, &mon, &rep_rows, &rep_cols, &rep);
+  void* red = base + off_red;
+  const size_t red_bytes = carve_workspace(nullptr, 1, n, m, m, dtype, device_sm_count(), nullptr);
+  Workspace ws;
+  carve_workspace(red, 1, n, m, m, dtype, device_sm_count(), &ws);
+  const int64_t d = n * m;
+  // ---- stage 1 (Alg. 3 lines 2-10): fold averages, then the cyclic Sinkhorn of the hot path
+  COT_CHECK_CUDA(launch_fold(a, b, n, m, alpha, beta, s));
+  COT_CHECK_CUDA(launch_aggregate(C, 1, n, m, dtype, ws.G, ws.A, ws.nonfinite, s));
+  st = cot_check_nonfinite(ws.nonfinite, stream);
+  if (st) return st;
+  st = cerot_init(alpha, beta, 1, m, COT_COLD_START, z_hat, red, red_bytes, stream);
+  if (st) return st;
+  const IterArgs ia = make_args(alpha, beta, C, ws.G, 1, n, m, dtype, eps, tol1, check_every, 0, w_hat, z_hat);
+  st = iterate_reduced(ia, ws, red, n, m, dtype, iters1, tol1, check_every, s);
+  if (st) return st;
+  int64_t it1 = 0;
+  int32_t conv1 = 0;
+  double res1 = 0.0;
+  st = cerot_state(red, 1, m, n, dtype, &it1, &conv1, &res1, stream);
+  if (st) return st;
+  // ---- stage 2 (lines 11-16): g = concatenated z_hat, then the original Sinkhorn on the explicit problem
+  COT_CHECK_CUDA(launch_tile(z_hat, n, m, g_hat, s));
+  COT_CHECK_CUDA(launch_transpose_blocks(C, n, m, dtype, Bt, s));
+  int64_t it2 = 0;
+  double residual = 0.0;
+  bool have_res = false;
+  for (int64_t t = 0; t < iters2; ++t) {
+    COT_CHECK_CUDA(launch_full_pass(C, n, m, dtype, eps, a, g_hat, f_hat, nullptr, nullptr, 0, s));   // p-update
+    COT_CHECK_CUDA(launch_full_pass(Bt, n, m, dtype, eps, b, f_hat, g_hat, dev, nullptr, 1, s));     // q-update
+    ++it2;
+    const bool check = (tol2 > 0.0 && it2 % check_every == 0) || t == iters2 - 1;
+    if (check) {
+      COT_CHECK_CUDA(launch_full_monitor(dev, d, mon, s));
+      COT_CHECK_CUDA(cudaMemcpyAsync(&residual, mon, 8, cudaMemcpyDeviceToHost, s));
+      COT_CHECK_CUDA(cudaStreamSynchronize(s));
+      have_res = true;
+      if (tol2 > 0.0 && it2 % check_every == 0 && residual <= tol2) break;
+    }
+  }
+  // ---- report of the returned plan T = diag(p) K diag(q) (line 17)
+  COT_CHECK_CUDA(launch_full_pass(C, n, m, dtype, eps, a, g_hat, f_hat, nullptr, rep_rows, 2, s));
+  COT_CHECK_CUDA(launch_full_pass(Bt, n, m, dtype, eps, b, f_hat, g_hat, nullptr, rep_cols, 2, s));
+  COT_CHECK_CUDA(launch_full_finalize(rep_rows, rep_cols, a, b, f_hat, g_hat, d, eps, have_res ? residual : res1,
+                                      rep, s));
+  double h[kReportDoubles];
+  COT_CHECK_CUDA(cudaMemcpyAsync(h, rep, sizeof(h), cudaMemcpyDeviceToHost, s));
+  COT_CHECK_CUDA(cudaStreamSynchronize(s));
+  if (report) {
+    report->objective = h[0];
+    report->reg_primal = h[1];
+    report->dual = h[2];
+    report->row_l1 = h[3];
+    report->col_l1 = h[4];
+    report->col_l2 = h[5];
+    report->mass = h[6];
+    report->residual = h[7];
+    report->iters = it2;
+    report->converged = tol2 > 0.0 && have_res && residual <= tol2;
+    report->status = (tol2 > 0.0 && !report->converged) ? COT_NOT_CONVERGED : COT_OK;
+  }
+  if (iters_done) {
+    iters_done[0] = it1;
+    iters_done[1] = it2;
+  }
+  return (tol2 > 0.0 && !(have_res && residual <= tol2)) ? COT_NOT_CONVERGED : COT_OK;
+}
+
 // ------------------------------------------------------------------------------------- NEXT-3: C-SROT
 int csrot_solve(const double* alpha, const double* beta, const void* C, int64_t B, int64_t n, int64_t m, int dtype,
                 int reg, const double* reg_param, double tol, int64_t max_sweeps, int64_t check_every, uint32_t flags,

@@ -134,4 +134,16 @@ cudaError_t launch_plan_reduce_local(const IterArgs& a, const Workspace& ws, con
 cudaError_t launch_plan_finalize_buf(const IterArgs& a, const Workspace& ws, const double* buf, double* report,
                                      cudaStream_t s);
 
+// NEXT-2 (k_full.cu): fold averages, tiling, transposed blocks, stage-2 half-iterations and report
+cudaError_t launch_fold(const double* a, const double* b, int64_t n, int64_t m, double* alpha, double* beta,
+                        cudaStream_t s);
+cudaError_t launch_tile(const double* z, int64_t n, int64_t m, double* g, cudaStream_t s);
+cudaError_t launch_transpose_blocks(const void* C, int64_t n, int64_t m, int dtype, void* Bt, cudaStream_t s);
+cudaError_t launch_full_pass(const void* X, int64_t n, int64_t m, int dtype, const double* eps, const double* mu,
+                             const double* in, double* out, double* dev, double* rep, int mode, cudaStream_t s);
+cudaError_t launch_full_monitor(const double* dev, int64_t d, double* out, cudaStream_t s);
+cudaError_t launch_full_finalize(const double* rep_rows, const double* rep_cols, const double* a, const double* b,
+                                 const double* f, const double* g, int64_t d, const double* eps, double residual,
+                                 double* report, cudaStream_t s);
+
 }  // namespace cot

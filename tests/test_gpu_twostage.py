@@ -1,0 +1,87 @@
+"""GPU parity of NEXT-2, the two-stage Sinkhorn algorithm (Algorithm 3), through the C ABI
+(cerot_two_stage) against the oracle (oracle.two_stage_sinkhorn) iterate for iterate from the same start.
+Bars as DESIGN.md §4: fp32 costs -- plan L1 and marginals 1e-5, objective / dual 1e-6 relative; fp64 costs
+-- 1e-10."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic
+
+pytestmark = pytest.mark.gpu
+
+cot = pytest.importorskip("paper_2311_13147_b200")
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2311_13147_b200 import build
+    build.build()
+    cot.lib()
+
+
+def _dev(x):
+    return torch.as_tensor(np.ascontiguousarray(x), device=DEV)
+
+
+def _full_report(f, g, a, b, C, eps):
+    T = oracle.plan_full(f, g, C, eps)
+    return {"objective": float((C * T).sum()), "row_l1": float(np.abs(T.sum(1) - a).sum()),
+            "col_l1": float(np.abs(T.sum(0) - b).sum()), "dual": float(f @ a + g @ b - eps * T.sum()),
+            "mass": float(T.sum())}, T
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.float32, 1e-5), (np.float64, 1e-10)], ids=["f32", "f64"])
+@pytest.mark.parametrize("H,noise", [(16, 0.1), (8, 0.3)])
+def test_two_stage_matches_oracle(dtype, tol, H, noise):
+    p = synthetic.c3_image(H=H)
+    a, b = synthetic.approx_symmetric(p, noise=noise)
+    C = p.C.astype(dtype)
+    eps = 0.05
+    f, g, w, z, rep = cot.two_stage_sinkhorn(_dev(a), _dev(b), _dev(C), eps, 15, 25)
+    assert (rep["iters1"], rep["iters2"]) == (15, 25)
+    fo, go, _, _ = oracle.two_stage_sinkhorn(a, b, C, eps, 15, 25)
+    Cf = oracle.expand_cost(C.astype(np.float64))
+    ro, To = _full_report(fo, go, a, b, Cf, eps)
+    Tg = oracle.plan_full(f.cpu().numpy() * eps, g.cpu().numpy() * eps, Cf, eps)
+    assert np.abs(Tg - To).sum() < tol
+    rel = 1e-6 if dtype == np.float32 else 1e-10
+    assert abs(rep["objective"] - ro["objective"]) <= rel * abs(ro["objective"])
+    assert abs(rep["dual"] - ro["dual"]) <= rel * abs(ro["dual"])
+    assert abs(rep["row_l1"] - ro["row_l1"]) <= tol
+    assert abs(rep["col_l1"] - ro["col_l1"]) <= tol
+    # stage-1 potentials: the cyclic Sinkhorn of the fold averages (gauge-invariant: the reduced plan)
+    wo, zo, _, _ = oracle.cyclic_sinkhorn(oracle.fold_average(a, p.n), oracle.fold_average(b, p.n), C, eps, 15)
+    Tr = oracle.plan_blocks(w.cpu().numpy() * eps, z.cpu().numpy() * eps, C, eps)
+    assert p.n * np.abs(Tr - oracle.plan_blocks(wo, zo, C, eps)).sum() < tol
+
+
+def test_two_stage_exact_symmetry_continues_the_cyclic_iteration():
+    p = synthetic.c2_ring(eps_factor=1e-1)
+    eps = float(p.eps[0])
+    a = oracle.expand_vector(p.alpha, p.n)
+    b = oracle.expand_vector(p.beta, p.n)
+    f, g, w, z, rep = cot.two_stage_sinkhorn(_dev(a), _dev(b), _dev(p.C), eps, 10, 5)
+    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), p.eps).init().iterate(15)
+    torch.cuda.synchronize()
+    C = oracle.expand_cost(p.C.astype(np.float64))
+    Tg = oracle.plan_full(f.cpu().numpy() * eps, g.cpu().numpy() * eps, C, eps)
+    Tc = oracle.expand_plan(oracle.plan_blocks(prob.w_hat.cpu().numpy() * eps, prob.z_hat.cpu().numpy() * eps,
+                                               p.C, eps))
+    assert np.abs(Tg - Tc).sum() < 1e-5
+
+
+def test_two_stage_converges_with_the_oracle():
+    p = synthetic.c3_image(H=16)
+    a, b = synthetic.approx_symmetric(p, noise=0.1)
+    C = p.C.astype(np.float64)
+    eps = 0.05
+    f, g, w, z, rep = cot.two_stage_sinkhorn(_dev(a), _dev(b), _dev(C), eps, 30, 2000, tol2=1e-9)
+    fo, go, t1, t2 = oracle.two_stage_sinkhorn(a, b, C, eps, 30, 2000, tol2=1e-9)
+    assert rep["converged"] and t2 < 2000
+    assert abs(rep["iters2"] - t2) <= 1
+    assert rep["residual"] <= 1e-9
