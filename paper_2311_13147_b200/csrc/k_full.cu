@@ -58,10 +58,11 @@ __device__ __forceinline__ double exp_arg(double x);
 template <>
 __device__ __forceinline__ double exp_arg<double>(double x) { return exp(x); }
 template <>
-__device__ __forceinline__ double exp_arg<float>(double x) {   // e^x, x <= 0: exact 2^round, MUFU 2^frac
-  const double a = fmax(x * COT_LOG2E, -1022.0);
-  const double ai = rint(a);
-  return (double)ex2((float)(a - ai)) * __longlong_as_double((long long)(ai + 1023.0) << 52);
+__device__ __forceinline__ double exp_arg<float>(double x) {   // e^x, x <= ~0: exact 2^round, MUFU 2^frac
+  const double a = x * COT_LOG2E;
+  const double big = a + 6755399441055744.0;   // round to nearest integer (|a| < 2^51)
+  const int ai = max(__double2loint(big), -1022);
+  return (double)ex2((float)(a - (big - 6755399441055744.0))) * __hiloint2double((ai + 1023) << 20, 0);
 }
 
 __device__ __forceinline__ double blk_reduce(double v, bool is_max, double* sh) {
@@ -80,9 +81,10 @@ __device__ __forceinline__ double blk_reduce(double v, bool is_max, double* sh) 
 // mode 0: out = the new potential. mode 1 (column half, monitor): also dev_I = |exp(out_old_I + LSE) - mu_I|,
 // the column residual of the row-exact plan. mode 2 (report): row sums r_I, transport and
 // entropy terms of T_IJ = exp(in_J + out_I - X_IJ/eps) with out read, not written.
-// grid = m (one CTA per i), 256 threads; X rows staged in shared memory when they fit (xs != 0).
+// grid = m (one CTA per i), 256 threads; X rows staged in shared memory when they fit (xs != 0). The loops
+// run over the column block s (block k = (s - r) mod n) and then j, so no division in the inner loop.
 template <typename T>
-__global__ void __launch_bounds__(256) k_full_pass(const T* __restrict__ X, int64_t n, int64_t m,
+__global__ void __launch_bounds__(256) k_full_pass(const T* __restrict__ X, int n, int m,
                                                    const double* __restrict__ eps, const double* __restrict__ mu,
                                                    const double* __restrict__ in, double* __restrict__ out,
                                                    double* __restrict__ dev, double* __restrict__ rep, int mode,
@@ -90,30 +92,28 @@ __global__ void __launch_bounds__(256) k_full_pass(const T* __restrict__ X, int6
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* row = reinterpret_cast<T*>(smem_raw);   // [n][m] when xs
   __shared__ double sh[32];
-  const int64_t i = blockIdx.x;
-  const int64_t nm = n * m;
+  const int i = blockIdx.x;
   const double inv_eps = 1.0 / eps[0];
   if (xs)
-    for (int64_t e = threadIdx.x; e < nm; e += blockDim.x) row[e] = X[((e / m) * m + i) * m + e % m];
+    for (int k = 0; k < n; ++k)
+      for (int j = threadIdx.x; j < m; j += blockDim.x) row[(size_t)k * m + j] = X[((size_t)k * m + i) * m + j];
   __syncthreads();
-  auto xval = [&](int64_t k, int64_t j) -> double {
-    return xs ? (double)row[k * m + j] : (double)X[(k * m + i) * m + j];
-  };
-  for (int64_t r = 0; r < n; ++r) {
-    const int64_t I = r * m + i;
-    double mx = -INFINITY;
-    for (int64_t e = threadIdx.x; e < nm; e += blockDim.x) {
-      const int64_t s = e / m, j = e - s * m;
-      const int64_t k = (s - r + n) % n;
-      mx = fmax(mx, in[e] - xval(k, j) * inv_eps);
-    }
-    mx = blk_reduce(mx, true, sh);
+  auto xrow = [&](int k) -> const T* { return xs ? row + (size_t)k * m : X + ((size_t)k * m + i) * m; };
+  for (int r = 0; r < n; ++r) {
+    const int I = r * m + i;
     if (mode < 2) {
+      double mx = -INFINITY;
+      for (int s = 0; s < n; ++s) {
+        const T* xr = xrow(s >= r ? s - r : s - r + n);
+        const double* ir = in + (size_t)s * m;
+        for (int j = threadIdx.x; j < m; j += blockDim.x) mx = fmax(mx, ir[j] - (double)xr[j] * inv_eps);
+      }
+      mx = blk_reduce(mx, true, sh);
       double sum = 0.0;
-      for (int64_t e = threadIdx.x; e < nm; e += blockDim.x) {
-        const int64_t s = e / m, j = e - s * m;
-        const int64_t k = (s - r + n) % n;
-        sum += exp_arg<T>(in[e] - xval(k, j) * inv_eps - mx);
+      for (int s = 0; s < n; ++s) {
+        const T* xr = xrow(s >= r ? s - r : s - r + n);
+        const double* ir = in + (size_t)s * m;
+        for (int j = threadIdx.x; j < m; j += blockDim.x) sum += exp_arg<T>(ir[j] - (double)xr[j] * inv_eps - mx);
       }
       sum = blk_reduce(sum, false, sh);
       if (threadIdx.x == 0) {
@@ -124,15 +124,17 @@ __global__ void __launch_bounds__(256) k_full_pass(const T* __restrict__ X, int6
     } else {
       const double o = out[I];
       double rs = 0.0, tr = 0.0, en = 0.0;
-      for (int64_t e = threadIdx.x; e < nm; e += blockDim.x) {
-        const int64_t s = e / m, j = e - s * m;
-        const int64_t k = (s - r + n) % n;
-        const double c = xval(k, j);
-        const double lt = in[e] + o - c * inv_eps;   // log T_IJ
-        const double t = exp(lt);
-        rs += t;
-        tr += c * t;
-        en += t * (lt - 1.0);
+      for (int s = 0; s < n; ++s) {
+        const T* xr = xrow(s >= r ? s - r : s - r + n);
+        const double* ir = in + (size_t)s * m;
+        for (int j = threadIdx.x; j < m; j += blockDim.x) {
+          const double c = (double)xr[j];
+          const double lt = ir[j] + o - c * inv_eps;   // log T_IJ
+          const double t = exp(lt);
+          rs += t;
+          tr += c * t;
+          en += t * (lt - 1.0);
+        }
       }
       rs = blk_reduce(rs, false, sh);
       tr = blk_reduce(tr, false, sh);
@@ -223,13 +225,13 @@ cudaError_t launch_full_pass(const void* X, int64_t n, int64_t m, int dtype, con
   if (dtype == COT_F32) {
     e = cudaFuncSetAttribute(k_full_pass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_full_pass<float><<<(unsigned)m, 256, smem, s>>>(static_cast<const float*>(X), n, m, eps, mu, in, out, dev, rep,
-                                                      mode, xs);
+    k_full_pass<float><<<(unsigned)m, 256, smem, s>>>(static_cast<const float*>(X), (int)n, (int)m, eps, mu, in, out,
+                                                      dev, rep, mode, xs);
   } else {
     e = cudaFuncSetAttribute(k_full_pass<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_full_pass<double><<<(unsigned)m, 256, smem, s>>>(static_cast<const double*>(X), n, m, eps, mu, in, out, dev,
-                                                       rep, mode, xs);
+    k_full_pass<double><<<(unsigned)m, 256, smem, s>>>(static_cast<const double*>(X), (int)n, (int)m, eps, mu, in,
+                                                       out, dev, rep, mode, xs);
   }
   return cudaGetLastError();
 }

@@ -31,13 +31,13 @@ def main():
     p = synthetic.c3_image()
     a, b = synthetic.approx_symmetric(p, noise=noise)
     D = lambda x: torch.as_tensor(np.ascontiguousarray(x), device=dev)
-    eps = float(p.eps[0])
+    eps = float(p.eps[0]) * float(os.environ.get("EPS_SCALE", "1"))
     tol2 = 1e-6
     run(D(a), D(b), D(p.C), eps, 10, 10, 0.0, 0.0)   # warm-up (module load, workspace)
     for name, it1, tol1 in (("two_stage", 5000, 1e-3), ("sinkhorn_cold", 0, 0.0)):
         ms, rep = run(D(a), D(b), D(p.C), eps, it1, 20000, tol1, tol2)
         d = p.n * p.m
-        print(json.dumps({"mode": name, "workload": "C3_approx_noise%.2f" % noise, "d": d, "eps": eps,
+        print(json.dumps({"mode": name, "workload": "C3_approx_noise%.2f_eps%.0e" % (noise, eps), "d": d, "eps": eps,
                           "tol1_monitor": tol1, "tol2_col_l1": tol2, "ms": ms, "iters1": rep["iters1"],
                           "iters2": rep["iters2"], "objective": rep["objective"], "col_l1": rep["col_l1"],
                           "row_l1": rep["row_l1"],
