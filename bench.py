@@ -168,8 +168,10 @@ class Runner:
         self.flags = int(os.environ.get("COT_BENCH_FLAGS", "0"))
         self.pre = os.environ.get("COT_BENCH_MODE") == "precomputed"   # NEXT-1 line (separate metric)
         self.S = torch.empty((self.B, 1, self.m, self.m), dtype=self.C.dtype, device=dev) if self.pre else None
-        # the persistent TMA kernel runs all iterations in one launch (B == 1, fp32, m % 4 == 0)
-        self.persistent = (self.B == 1 and self.dt == cot.COT_F32 and self.m % 4 == 0 and not (self.flags & 2))
+        # which iteration kernel the library runs: 1 = persistent TMA stream (all iterations in one launch),
+        # 2 = cluster-resident (all iterations in one launch, whole problems on chip), 0 = launch pair / iteration
+        self.path = int(self.L.cot_iter_path(self.B, 1 if self.pre else self.n, self.m, self.dt, self.flags))
+        self.persistent = self.path in (1, 2)
         self.launches_per_step = 1 + 1 + (1 if self.persistent else 2 * iters) + 3 + 1 + (1 if self.pre else 0)
         self.bytes_iter = float(p.B) * ((2 if self.pre else p.n + 1) * p.m * p.m) * p.C.itemsize
 
@@ -382,13 +384,21 @@ def run_ours(args, rank, world, local_rank):
     per_launch_ms = it_mean if R.persistent else it_mean / iters
     achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
     dom_share = it_mean / ms_step
+    clocks = clk.summary()
+    cluster = getattr(R, "path", None) == 2
+    if cluster:   # whole problems on chip: the bound is the SFU (one MUFU.EX2 per Gibbs evaluation), DESIGN.md §6
+        ex2_launch = float(B_local_evals(p, iters))
+        achieved_sfu = ex2_launch / (per_launch_ms / 1e3)
+        mhz = clocks.get("sm_mhz") or 1965.0
+        peak_sfu = 148 * 16 * mhz * 1e6
     if mode == "row_sharded":
         kernel = ("k_iter_tma fused (persistent, all iterations in one launch per rank; column sums exchanged "
                   "in-kernel through peer-mapped LL lines)" if R.fused else
                   "per iteration: k_iter_tma rows-only + k_colsum + ncclAllReduce + k_zupdate")
     else:
-        kernel = ("k_iter_tma (persistent: all iterations in one launch)" if R.persistent else
-                  "k_rows_ldg + k_cols (one launch pair per iteration)")
+        kernel = {1: "k_iter_tma (persistent: all iterations in one launch)",
+                  2: "k_batch_cluster (8-CTA cluster per problem, all iterations in one launch, on chip)"}.get(
+                      getattr(R, "path", 0), "k_rows_ldg + k_cols (one launch pair per iteration)")
     trf = _ncu_traffic_per_iter(args.workload) if world == 1 else None
     metric = _metric()
     if getattr(R, "pre", False):   # NEXT-1 is reported on its own line, never under the n*m^2 streaming metric
@@ -410,13 +420,20 @@ def run_ours(args, rank, world, local_rank):
                                                    else f"rows over {world} GPUs, 1 ncclAllReduce (m fp64) per "
                                                         f"iteration"),
                                    "problem_sharded": f"problems over {world} GPUs, no collective"}[mode]},
-        "roofline": {"bound": "hbm", "kernel": kernel,
+        "roofline": ({"bound": "alu", "kernel": kernel, "achieved": achieved_sfu, "peak": peak_sfu, "unit": "ex2/s",
+                      "frac": achieved_sfu / peak_sfu,
+                      "peak_source": "derived: 148 SMs x 16 MUFU.EX2/clk/SM (measured 15.75-15.9, scripts/ubench) x "
+                                     "the median SM clock under load (NVML)",
+                      "traffic": None, "algorithmic_ex2_per_launch": ex2_launch,
+                      "launch_ms_mean": per_launch_ms, "launch_samples": nsamp, "share_of_step": dom_share,
+                      "us_per_iter": it_mean * 1e3 / iters} if cluster else
+                     {"bound": "hbm", "kernel": kernel,
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src,
                      "traffic": None if trf is None else trf * (iters if R.persistent else 1),
                      "algorithmic_bytes_per_launch": bytes_launch, "algorithmic_bytes_per_iter": bytes_iter,
                      "launch_ms_mean": per_launch_ms, "launch_samples": nsamp, "share_of_step": dom_share,
-                     "us_per_iter": it_mean * 1e3 / iters},
+                     "us_per_iter": it_mean * 1e3 / iters}),
         "iter_only_evals_per_s": evals_step / (it_mean / 1e3),
         "gpu_launches": R.launches_per_step * args.steps,
         "result": {"objective": float(rep0[0]), "dual": float(rep0[2]), "row_l1": float(rep0[3])},
@@ -425,12 +442,17 @@ def run_ours(args, rank, world, local_rank):
         out["e2e"] = e2e
     if not args.no_cpu and rank == 0:
         out["cpu_baseline"] = cpu_baseline(p, args)
-    out["clocks"] = clk.summary()
+    out["clocks"] = clocks
     if mode == "row_sharded":
         if R.xchg is not None:
             R.xchg.close()
         R.comm.close()
     return out
+
+
+def B_local_evals(p, iters):
+    """Gibbs evaluations (= MUFU.EX2) of one persistent launch on this rank: n*m^2 per problem per iteration."""
+    return float(p.B) * p.n * p.m * p.m * iters
 
 
 def run_e2e(R, p, steps, stream):

@@ -48,6 +48,7 @@ _SIGS = {
     "cot_check_nonfinite": (ctypes.c_int, [_vp, _vp]),
     "clot_expand": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp]),
     "cerot_init": (ctypes.c_int, [_vp, _vp, _i64, _i64, _u32, _vp, _vp, _sz, _vp]),
+    "cot_iter_path": (ctypes.c_int, [_i64, _i64, _i64, ctypes.c_int, _u32]),
     "cerot_iter": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl, _i64, _u32,
                                   _vp, _vp, _vp, _sz, _vp]),
     "cerot_rows": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _u32, _vp, _vp, _vp, _sz,

@@ -318,6 +318,15 @@ int cerot_iter(const double* alpha, const double* beta, const void* C, const voi
   return COT_OK;
 }
 
+int cot_iter_path(int64_t B, int64_t n, int64_t m, int dtype, uint32_t flags) {
+  if (B < 1 || n < 1 || m < 1) return -1;
+  const IterArgs a = make_args(nullptr, nullptr, nullptr, nullptr, B, n, m, dtype, nullptr, 0.0, 1, flags, nullptr,
+                               nullptr);
+  if (batch_cluster_eligible(a)) return 2;
+  if (tma_eligible(a)) return 1;
+  return 0;
+}
+
 int cerot_rows(const double* alpha, const void* C, const void* G, int64_t B, int64_t n, int64_t m, int dtype,
                const double* eps, uint32_t flags, const double* z_hat, double* w_hat, void* workspace,
                size_t ws_bytes, int parity, void* stream) {
