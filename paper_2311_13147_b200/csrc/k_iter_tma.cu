@@ -116,6 +116,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 constexpr unsigned long long kPeerTimeoutNs = 20000000000ull;   // 20 s without a peer's line: give up
+#ifndef COT_POLL_BACKOFF_NS
+#define COT_POLL_BACKOFF_NS 0
+#endif
+constexpr unsigned kPollBackoffNs = COT_POLL_BACKOFF_NS;
 constexpr int kColScratch = 256 + kMaxRanks * 8;   // doubles: column-pass groups, then the rank exchange
 constexpr int kRankScratch = 256;
 
@@ -136,6 +140,7 @@ __device__ __forceinline__ bool poll_line(const uint4* a, unsigned g, double& v)
   }
   const unsigned long long t0 = gtimer();
   while (true) {
+    if (kPollBackoffNs) __nanosleep(kPollBackoffNs);   // fewer L2 requests while waiting
     l = ld_line(a);
     if (ll_ready(l, g)) {
       v = ll_value(l);
@@ -146,6 +151,19 @@ __device__ __forceinline__ bool poll_line(const uint4* a, unsigned g, double& v)
       return false;
     }
   }
+}
+
+// Sum (or max) of up to 8 values r[0], r[stride], ...: all loads issued first, then a fixed pairwise tree
+// (one shared-memory latency instead of a chain of nw).
+__device__ __forceinline__ double tree8(const double* r, int nw, bool is_max) {
+  double v[8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) v[w] = w < nw ? r[w] : (is_max ? -INFINITY : 0.0);
+#pragma unroll
+  for (int h = 4; h >= 1; h >>= 1)
+#pragma unroll
+    for (int w = 0; w < h; ++w) v[w] = is_max ? fmax(v[w], v[w + h]) : v[w] + v[w + h];
+  return v[0];
 }
 
 // Two-cbar block reduction for rare uses (monitor partial).
@@ -172,13 +190,8 @@ __device__ __forceinline__ void cblk_maxsum(double& mx, double& sm, double* red2
     r[32 + wid] = sm;
   }
   cbar(nct);
-  double M = r[0], S = r[32];
-  for (int w = 1; w < (nct >> 5); ++w) {
-    M = fmax(M, r[w]);
-    S += r[32 + w];
-  }
-  mx = M;
-  sm = S;
+  mx = tree8(r, nct >> 5, true);
+  sm = tree8(r + 32, nct >> 5, false);
   buf ^= 1;
 }
 __device__ __forceinline__ double cblk_max1(double v, double* red2, int& buf, int nct, int wbase) {
@@ -246,11 +259,7 @@ __device__ __forceinline__ void cblk_sumN(double* v, double* red2, int& buf, int
   }
   cbar(nct);
 #pragma unroll
-  for (int q = 0; q < N; ++q) {
-    double x = r[q * 8];
-    for (int w = 1; w < (nct >> 5); ++w) x += r[q * 8 + w];
-    v[q] = x;
-  }
+  for (int q = 0; q < N; ++q) v[q] = tree8(r + q * 8, nct >> 5, false);
   buf ^= 1;
 }
 template <int N>
@@ -264,11 +273,7 @@ __device__ __forceinline__ void cblk_maxN(double* v, double* red2, int& buf, int
   }
   cbar(nct);
 #pragma unroll
-  for (int k = 0; k < N; ++k) {
-    double x = r[k * 8];
-    for (int w = 1; w < (nct >> 5); ++w) x = fmax(x, r[k * 8 + w]);
-    v[k] = x;
-  }
+  for (int k = 0; k < N; ++k) v[k] = tree8(r + k * 8, nct >> 5, true);
   buf ^= 1;
 }
 
@@ -619,7 +624,10 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       return cblk_sum1(v, red2, rbuf, net, nk);
     };
     // log beta_j of the first 8 columns of this CTA's slice (the usual whole slice), once per launch
-    const double lbeta0 = (sync && et < 8 && col0 + et < col1) ? log(p.beta[col0 + et]) : 0.0;   // no beta: rows_only
+    const bool own0 = sync && et < 8 && col0 + et < col1;   // rows_only launches have no beta
+    const double beta0 = own0 ? p.beta[col0 + et] : 1.0;
+    const double lbeta0 = own0 ? log(beta0) : 0.0;
+    double zown0 = own0 ? __ldcg(p.z_hat + col0 + et) : 0.0;   // this thread's z_hat of the slice, kept in a register
     int done = 0;   // iterations completed (q-update applied) in this launch
     bool halted = false;
     for (int t = 0; active0 && t < p.iters; ++t) {
@@ -630,9 +638,24 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
           const int jv = q * net + et;
-          if (jv < mv) {
+          if (jv < mv) {   // the 4 lines of this thread's columns, re-polled together while any is missing
+            uint4 zl[VEC];
+            unsigned todo = (1u << VEC) - 1u;
+            const unsigned long long tz0 = gtimer();
+            while (todo) {
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) timeout |= !poll_line(p.zlines + VEC * jv + v, g, z[q][v]);
+              for (int v = 0; v < VEC; ++v)
+                if (todo & (1u << v)) {
+                  zl[v] = ld_line(p.zlines + VEC * jv + v);
+                  if (ll_ready(zl[v], g)) todo &= ~(1u << v);
+                }
+              if (todo && gtimer() - tz0 > kPeerTimeoutNs) {
+                timeout = true;
+                break;
+              }
+            }
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) z[q][v] = ll_value(zl[v]);
           }
         }
         if (need_resid(t - 1)) st.residual = read_resid(g) * (double)n;
@@ -839,13 +862,26 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
             const int u2 = ub + k * ngrp;
             l[k] = (colok && u2 < nblk) ? ld_line(plr + (size_t)u2 * m + cb + c) : make_uint4(0u, g1, 0u, g1);
           }
+          // re-poll every line still missing in the same round (one round trip per round, not per line)
+          unsigned todo = 0;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int u2 = ub + k * ngrp;
-            double v = ll_value(l[k]);
-            if (colok && u2 < nblk && !ll_ready(l[k], g1)) timeout |= !poll_line(plr + (size_t)u2 * m + cb + c, g1, v);
-            acc += v;
+          for (int k = 0; k < 8; ++k)
+            if (colok && ub + k * ngrp < nblk && !ll_ready(l[k], g1)) todo |= 1u << k;
+          const unsigned long long tp0 = todo ? gtimer() : 0ull;
+          while (todo) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (todo & (1u << k)) {
+                l[k] = ld_line(plr + (size_t)(ub + k * ngrp) * m + cb + c);
+                if (ll_ready(l[k], g1)) todo &= ~(1u << k);
+              }
+            if (todo && gtimer() - tp0 > kPeerTimeoutNs) {
+              timeout = true;
+              break;
+            }
           }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc += ll_value(l[k]);   // unit order
         }
         if (p.trace) c_cp1 += clock64() - tc0;
         // groups of a warp (lanes c, c+8, c+16, c+24) by two shuffle levels, then the warps in order
@@ -856,7 +892,14 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
         double cj = 0.0;
         if (et < 8) {
-          for (int w2 = 0; w2 < (ngrp >> 2); ++w2) cj += xs[w2 * 8 + et];
+          double v8[8];
+#pragma unroll
+          for (int w2 = 0; w2 < 8; ++w2) v8[w2] = w2 < (ngrp >> 2) ? xs[w2 * 8 + et] : 0.0;
+#pragma unroll
+          for (int h = 4; h >= 1; h >>= 1)
+#pragma unroll
+            for (int w2 = 0; w2 < h; ++w2) v8[w2] += v8[w2 + h];
+          cj = v8[0];
         }
         if (fused) {
           // ---- the exchange step across GPUs: this rank's slice sums -> every rank's x-lines (NVLink peer
@@ -881,10 +924,12 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         }
         if (et < 8 && cb + et < col1) {
           const int j = cb + et;
-          const double bj = p.beta[j];
+          const double bj = cb == col0 ? beta0 : p.beta[j];
           dev += fabs(cj - bj);
           if (!(cj >= 1e-28)) atomicOr(&p.state[0].flags, (int)STATE_UNDERFLOW);
-          const double zj = __ldcg(p.z_hat + j) + ((cb == col0 ? lbeta0 : log(bj)) - log(cj));
+          const double zold = cb == col0 ? zown0 : __ldcg(p.z_hat + j);
+          const double zj = zold + ((cb == col0 ? lbeta0 : log(bj)) - log(cj));
+          if (cb == col0) zown0 = zj;
           p.z_hat[j] = zj;
           st_line(p.zlines + j, ll_pack(zj, g1));
         }
@@ -917,6 +962,12 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       if (fused) *(volatile unsigned long long*)p.xepoch = xep0 + (unsigned long long)done;
     }
     if (timeout) atomicOr(&p.state[0].flags, (int)STATE_PEER_TIMEOUT);
+    if (p.trace && et == net - 32) {   // the last epilogue warp's view (skew diagnostics)
+      p.trace[bid * 16 + 12] = c_cmp;
+      p.trace[bid * 16 + 13] = c_red;
+      p.trace[bid * 16 + 14] = c_epi;
+      p.trace[bid * 16 + 15] = c_wait;
+    }
     if (p.trace && et == 0) {
       p.trace[bid * 16 + 4] = c_epi;
       p.trace[bid * 16 + 5] = c_wait;
@@ -1116,10 +1167,11 @@ void trace_end(const unsigned long long* trace, int grid, int iters, cudaStream_
   fprintf(stderr,
           "[cot trace] iters=%d per-iter cycles (mean/max over CTAs): prod_wait %.0f/%.0f prod_total %.0f/%.0f "
           "ksum %.0f/%.0f epi_busy %.0f/%.0f epi_wait_z %.0f/%.0f [epi: compute %.0f reduce %.0f; colpass %.0f; "
-          "queue wait %.0f/%.0f; ksum queue wait %.0f; colpass poll %.0f; publish %.0f]\n",
+          "queue wait %.0f/%.0f; ksum queue wait %.0f; colpass poll %.0f; publish %.0f] last epilogue warp: compute "
+          "%.0f reduce %.0f busy %.0f wait_z %.0f\n",
           iters, acc[0] / it, mx[0] / it, acc[1] / it, mx[1] / it, acc[3] / it, mx[3] / it, acc[4] / it,
           mx[4] / it, acc[5] / it, mx[5] / it, acc[2] / it, acc[6] / it, acc[7] / it, acc[8] / it, mx[8] / it,
-          acc[9] / it, acc[10] / it, acc[11] / it);
+          acc[9] / it, acc[10] / it, acc[11] / it, acc[12] / it, acc[13] / it, acc[14] / it, acc[15] / it);
 }
 }  // namespace
 
