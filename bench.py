@@ -249,9 +249,28 @@ class ShardedRunner:
         # fused (default): the exchange inside the persistent kernel over peer-mapped buffers (cerot_iter_fused);
         # COT_SHARD_IMPL=nccl: the baseline, one ncclAllReduce + 3 launches per iteration (cerot_iter_sharded)
         self.fused = os.environ.get("COT_SHARD_IMPL", "fused") == "fused"
+        self.fused_note = None
         with stdout_to_stderr():
             self.comm = cdist.NcclComm()
-            self.xchg = cdist.PeerExchange(p.m) if self.fused else None
+            self.xchg = None
+            if self.fused:
+                # the peer mappings need CUDA IPC between the ranks' GPUs; every rank must agree on the path
+                ok, err = 1, ""
+                try:
+                    self.xchg = cdist.PeerExchange(p.m)
+                except Exception as e:   # e.g. IPC not permitted in this container
+                    ok, err = 0, str(e)
+                flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+                import torch.distributed as tdist
+                if tdist.is_initialized():
+                    tdist.all_reduce(flag, op=tdist.ReduceOp.MIN)
+                if int(flag.item()) == 0:
+                    if self.xchg is not None:
+                        self.xchg.close()
+                        self.xchg = None
+                    self.fused = False
+                    self.fused_note = f"fused exchange unavailable ({err or 'on another rank'}): NCCL baseline"
+                    print(f"[bench] {self.fused_note}", file=sys.stderr)
         Cl = np.ascontiguousarray(p.C[:, self.row_begin:self.row_begin + self.R, :])
         self.Cl_host = Cl
         self.sh = cdist.ShardedCerot(torch.as_tensor(Cl, device=dev), torch.as_tensor(p.alpha, device=dev),
@@ -394,7 +413,8 @@ def run_ours(args, rank, world, local_rank):
     if mode == "row_sharded":
         kernel = ("k_iter_tma fused (persistent, all iterations in one launch per rank; column sums exchanged "
                   "in-kernel through peer-mapped LL lines)" if R.fused else
-                  "per iteration: k_iter_tma rows-only + k_colsum + ncclAllReduce + k_zupdate")
+                  "per iteration: k_iter_tma rows-only + k_colsum + ncclAllReduce + k_zupdate" +
+                  (f" [{R.fused_note}]" if R.fused_note else ""))
     else:
         kernel = {1: "k_iter_tma (persistent: all iterations in one launch)",
                   2: "k_batch_cluster (8-CTA cluster per problem, all iterations in one launch, on chip)"}.get(

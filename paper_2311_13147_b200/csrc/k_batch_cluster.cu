@@ -249,10 +249,15 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
     }
     const long long c1t = p.trace ? clock64() : 0;
     __syncthreads();
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {   // CTA partial: warps in order
-      double acc = 0.0;
-      for (int w = 0; w < nwarps; ++w) acc += wpart[(size_t)w * m + j];
-      cpart[j] = acc;
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {   // CTA partial: warps in a fixed pairwise tree
+      double v16[16];
+#pragma unroll
+      for (int w = 0; w < 16; ++w) v16[w] = w < nwarps ? wpart[(size_t)w * m + j] : 0.0;
+#pragma unroll
+      for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+        for (int w = 0; w < h; ++w) v16[w] += v16[w + h];
+      cpart[j] = v16[0];
     }
     // ================= B1: publish the CTA partial; stream the first half of the next k-sums meanwhile
     const long long c2t = p.trace ? clock64() : 0;
