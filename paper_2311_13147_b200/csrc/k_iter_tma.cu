@@ -1,27 +1,27 @@
 // K-ITER (TMA path): a persistent, warp-specialised cyclic Sinkhorn kernel for one problem (B == 1) with
-// fp32 costs and m % 4 == 0. Same arithmetic as k_rows_ldg + k_cols (k_iter.cu), organised for HBM.
-// Three warp roles per CTA (one CTA per SM, one unit of consecutive rows per CTA):
+// fp32 costs and m % 4 == 0 (Alg. 2 lines 4-5, in the log domain of eq. P:403-411). Same arithmetic
+// as k_rows_ldg + k_cols (k_iter.cu), organised for HBM. One CTA per SM owns a unit of consecutive rows;
+// three warp roles:
 //
 //   producer warp (1 elected lane): streams the CTA's rows of C through an NSLOT-deep ring of shared-
 //     memory slots with 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP); a slot holds KS consecutive
 //     k-rows C[k][i][0..m) of one row i; completion via mbarrier transaction counts (full[]), reuse via
 //     consumer-warp arrivals (empty[]). It never depends on the potentials, so it runs ahead across
-//     epilogues, device-wide syncs and iteration boundaries.
-//   consumer warps (VEC consecutive columns per thread): per row, the streamed k-sum
-//     s_ij = sum_k exp2((G_ij - C_ijk) * log2e/eps) (one FFMA + one MUFU.EX2 + one FADD per element), then
-//     the fp64 epilogue: x_ij = z_hat_j - G_ij/eps, r_i = sum_j s_ij exp(x_ij - M'_i) and M_i = max_j x_ij in
-//     ONE combined block reduction against the previous iteration's row maximum M'_i (exact exponent split:
-//     no precision cost), w_hat_i = log alpha_i - M'_i - log r_i, P_j += (alpha_i / r_i) s_ij exp(x_ij - M'_i).
-//     Rows whose potentials are not ready yet (the previous q-update is still in flight) are parked in
-//     shared memory; k-sums run at most one iteration ahead of epilogues.
-//   sync warp: owns every device-wide step, off the consumers' critical path: waits for the consumers to
-//     publish the CTA's column partial (bar.arrive / bar.sync), arrives on device barrier B1, reduces this
-//     CTA's slice of columns over all units in a fixed order (deterministic), applies the q-update
-//     z_hat_j += log beta_j - log c_j, arrives on B2, evaluates the monitor / freeze rule, and publishes the
-//     new z generation to the consumers through shared memory (st.release / ld.acquire at CTA scope).
+//     epilogues, device-wide steps and iteration boundaries.
+//   k-sum warps: s_ij = sum_k exp2((G_ij - C_ijk) * log2e/eps) (one FFMA + one MUFU.EX2 + one FADD per
+//     element) into a shared-memory row queue; s is iterate-independent, so they run up to a queue ahead.
+//   epilogue warps: rows in batches of RB with one block reduction per batch: x_ij = z_hat_j - G_ij/eps
+//     (-G/eps staged in fp64 shared memory), t_ij = s_ij exp(x_ij - M'_i) against the row's log-sum-exp of the
+//     previous iteration (exact exponent split; a batch out of range is redone exactly), r_i, w_hat_i,
+//     P_j += (alpha_i / r_i) t_ij; then the device-wide steps WITHOUT a grid barrier: the CTA's partial is
+//     published as LL lines (16-byte stores carrying the iteration's generation), the owner of each column
+//     slice polls the slice's lines of every unit and sums them in unit order (deterministic), [fused
+//     multi-GPU: exchanges the slice sums with every rank through peer-mapped LL lines, summed in rank order],
+//     applies the q-update z_hat_j += log beta_j - log c_j and publishes z_hat as LL lines, which every CTA
+//     polls before its next iteration; the monitor is one LL line per slice owner.
 //
 // The grid is co-resident (cooperative launch). With rows_only = 1 the kernel performs only the row pass
-// of one iteration (no device-wide steps): cerot_rows.
+// of one iteration into plain fp64 partials (no device-wide steps): cerot_rows / cerot_rows_shard.
 #include "common.cuh"
 #include "internal.h"
 
@@ -1206,7 +1206,8 @@ cudaError_t launch_iter_tma_fused(const FusedRank* r, int nv, int nranks, bool e
       (!emulate && nv != 1))
     return cudaErrorInvalidValue;
   const int sms_dev = device_sm_count();
-  const int sms = emulate ? sms_dev / nranks : sms_dev;   // emulation: each virtual rank gets 1/nranks of the SMs
+  int sms = emulate ? sms_dev / nranks : sms_dev;   // emulation: each virtual rank gets 1/nranks of the SMs
+  if (const char* ev = getenv("COT_MAX_CTAS")) sms = std::max(1, std::min(sms, atoi(ev)));   // experiments
   if (sms < 1) return cudaErrorInvalidConfiguration;
   TmaMulti pm;
   memset(&pm, 0, sizeof(pm));
