@@ -660,7 +660,9 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         }
         if (need_resid(t - 1)) st.residual = read_resid(g) * (double)n;
         if (p.trace) c_wait += clock64() - tw0;
-        if (fused && (__ldcg(&p.state[0].flags) & STATE_PEER_TIMEOUT)) halted = true;
+        // a CTA that gave up waiting halts (its peers then time out on its lines and halt too); no global read
+        // of the state flags on the per-iteration critical path
+        if (timeout) halted = true;
         if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
           st.active = 0;
           st.converged = 1;
