@@ -176,3 +176,16 @@ def test_fused_argument_errors():
     q = synthetic.random_cyclic(seed=2, n=3, m=30, dtype=np.float32, eps=0.1)   # m % 4 != 0
     with pytest.raises(cot.CotError):
         cdist.emulate_fused(_shards(q, 2), 3)
+
+
+def test_emulated_fused_c4_full_size_8_ranks():
+    """C4 (configs[3]) at full size (n = 64, m = 1024) split 8 ways -- the partition of the 8-GPU bench line --
+    as 8 emulated ranks, 20 iterations, against the oracle (Alg. 2 with K precomputed, pinned equal to the
+    streaming form)."""
+    p = synthetic.c4_large()
+    shards = _shards(p, 8)
+    xb = cdist.emulate_fused(shards, 20)
+    try:
+        _check_against_oracle(p, shards, 20)
+    finally:
+        cdist.free_xbufs(xb)

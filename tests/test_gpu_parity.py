@@ -334,3 +334,30 @@ def test_precomputed_mode_matches_alg2(maker, path):
         w, z, _, _ = oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, float(q.eps[0]), iters, form="kernel")
         fp64 = q.C.dtype == np.float64
         _compare(q, rep[b], T[b], w, z, obj_rtol=1e-10 if fp64 else 1e-6, l1_tol=1e-10 if fp64 else 1e-5)
+
+
+def test_c5_full_batch_in_the_bench_launch_configuration_sampled():
+    """C5 (configs[4]) at full size -- 4096 problems, one batched launch of each step exactly as bench.py times
+    it (clot_aggregate, cerot_init, 200 iterations, cerot_plan with T blocks, clot_expand of the C-EROT blocks
+    to the 68.7 GB dense plans) -- checked on a sample of problems the oracle computes one by one: G and argmin
+    bit-exact, the report and the plan blocks within the bar, the expanded plans bit-exact."""
+    p = synthetic.c5_batched(B=4096)
+    C = _dev(p.C)
+    G, A = cot.clot_aggregate(C)
+    prob = cot.CerotProblem(C, _dev(p.alpha), _dev(p.beta), _dev(p.eps))
+    prob.init().iterate(200)
+    T, rep = prob.plan(T_blocks=True)
+    Tfull = cot.clot_expand(T, p.n)
+    torch.cuda.synchronize()
+    rep = rep.cpu().numpy()
+    for b in (0, 1, 777, 2048, 4000, 4095):
+        q = p.single(b)
+        Go, Ao = oracle.aggregate(q.C)
+        assert np.array_equal(G[b].cpu().numpy().view(np.uint32), Go.view(np.uint32))
+        assert np.array_equal(A[b].cpu().numpy(), Ao)
+        w, z, _, _ = oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, float(q.eps[0]), 200, form="kernel")
+        Tb = T[b].cpu().numpy()
+        _compare(q, rep[b], Tb, w, z)
+        assert np.array_equal(Tfull[b].cpu().numpy(), oracle.expand_plan(Tb))
+    del Tfull, T, C, prob
+    torch.cuda.empty_cache()
