@@ -71,22 +71,6 @@ struct TmaParams {
 __device__ __forceinline__ void cbar(int nthreads) {   // consumer-only named barrier
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned x) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(x) : "memory");
-  return old;
-}
-__device__ __forceinline__ void red_add_release(unsigned* p, unsigned x) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
-}
-__device__ __forceinline__ void st_relaxed(unsigned* p, unsigned x) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
-}
 __device__ __forceinline__ unsigned lds_volatile(const unsigned* p) { return *(volatile const unsigned*)p; }
 __device__ __forceinline__ unsigned lds_acquire(const unsigned* p) {
   unsigned v;
@@ -166,17 +150,6 @@ __device__ __forceinline__ double tree8(const double* r, int nw, bool is_max) {
   return v[0];
 }
 
-// Two-cbar block reduction for rare uses (monitor partial).
-__device__ __forceinline__ double cblk_sum(double v, double* sh, int nct) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  v = warp_sum(v);
-  if (lane == 0) sh[wid] = v;
-  cbar(nct);
-  double t = 0.0;
-  for (int w = 0; w < (nct >> 5); ++w) t += sh[w];
-  cbar(nct);
-  return t;
-}
 // One-cbar block reductions for the epilogues: double-buffered scratch (`buf` alternates; the next
 // reduction's cbar orders every read of this buffer before its reuse two reductions later).
 __device__ __forceinline__ void cblk_maxsum(double& mx, double& sm, double* red2, int& buf, int nct,
@@ -194,25 +167,10 @@ __device__ __forceinline__ void cblk_maxsum(double& mx, double& sm, double* red2
   sm = tree8(r + 32, nct >> 5, false);
   buf ^= 1;
 }
-__device__ __forceinline__ double cblk_max1(double v, double* red2, int& buf, int nct, int wbase) {
-  double s = 0.0;
-  cblk_maxsum(v, s, red2, buf, nct, wbase);
-  return v;
-}
 __device__ __forceinline__ double cblk_sum1(double v, double* red2, int& buf, int nct, int wbase) {
   double m = -INFINITY;
   cblk_maxsum(m, v, red2, buf, nct, wbase);
   return v;
-}
-
-// exp(d) for d in fp64, |d| < ~700: 2^(round) exactly in fp64 times MUFU 2^frac with |frac| <= 1/2, so the
-// fp32 rounding of the argument costs < 3e-8 relative regardless of |d|.
-__device__ __forceinline__ double exp_split(double d) {
-  const double a = d * COT_LOG2E;
-  const double ai = fmax(rint(a), -1022.0);   // below 2^-1022: f is very negative and ex2(f) flushes to 0
-  const float f = (float)(a - ai);
-  const long long e = (long long)ai + 1023;
-  return (double)ex2(f) * __longlong_as_double(e << 52);
 }
 
 // s * e^d for d in fp64 and s in fp32: 2^round(d log2e) built exactly in the exponent bits (the round by the
@@ -276,51 +234,6 @@ __device__ __forceinline__ void cblk_maxN(double* v, double* red2, int& buf, int
   for (int k = 0; k < N; ++k) v[k] = tree8(r + k * 8, nct >> 5, true);
   buf ^= 1;
 }
-
-// One-barrier block reduction of two rows' (max, sum) over the epilogue warps (double-buffered scratch).
-__device__ __forceinline__ void cblk_maxsum2(double* mx, double* sm, double* red2, int& buf, int nct, int wbase) {
-  const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) - wbase;
-  double a0 = warp_max(mx[0]), a1 = warp_max(mx[1]);
-  double b0 = warp_sum(sm[0]), b1 = warp_sum(sm[1]);
-  double* r = red2 + buf * 64;
-  if (lane == 0) {
-    r[wid] = a0;
-    r[8 + wid] = a1;
-    r[16 + wid] = b0;
-    r[24 + wid] = b1;
-  }
-  cbar(nct);
-  a0 = r[0];
-  a1 = r[8];
-  b0 = r[16];
-  b1 = r[24];
-  for (int w = 1; w < (nct >> 5); ++w) {
-    a0 = fmax(a0, r[w]);
-    a1 = fmax(a1, r[8 + w]);
-    b0 += r[16 + w];
-    b1 += r[24 + w];
-  }
-  mx[0] = a0;
-  mx[1] = a1;
-  sm[0] = b0;
-  sm[1] = b1;
-  buf ^= 1;
-}
-
-template <int VEC>
-struct VecF;
-template <>
-struct VecF<2> {
-  using type = float2;
-  __device__ static void get(const type& v, float* o) { o[0] = v.x; o[1] = v.y; }
-  __device__ static type make(const float* o) { return make_float2(o[0], o[1]); }
-};
-template <>
-struct VecF<4> {
-  using type = float4;
-  __device__ static void get(const type& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
-  __device__ static type make(const float* o) { return make_float4(o[0], o[1], o[2], o[3]); }
-};
 
 template <int CPT, int EPT, int KS>
 __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid, const int nblk) {
