@@ -108,28 +108,55 @@ __global__ void __launch_bounds__(256) k_plan(PlanParams p) {
         }
       }
       double row = 0.0;
-      for (int64_t k = 0; k < p.n; ++k) {
+      // blocks in groups of KU: the KU loads of a group are issued before any arithmetic (memory parallelism)
+      constexpr int KU = 4;
+      auto element = [&](int q, const VT& cvv, T* tout) {
+        T c[V];
+        VecP<T, V>::unpack(cvv, c);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const double a = ((double)g[q][v] - (double)c[v]) * inv_eps;   // <= 0
+          double e;
+          if constexpr (sizeof(T) == 4)
+            e = (double)exp2f((float)(a * COT_LOG2E));
+          else
+            e = exp(a);
+          const double Tv = E[q][v] * e;
+          transport = fma((double)c[v], Tv, transport);
+          ent = fma(Tv, (y[q][v] + a) - 1.0, ent);
+          row += Tv;
+          P[q][v] += Tv;
+          tout[v] = (T)Tv;
+        }
+      };
+      int64_t k = 0;
+      for (; k + KU <= p.n; k += KU) {
+        VT cv[KU][CPT];
+#pragma unroll
+        for (int kk = 0; kk < KU; ++kk)
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            const int64_t jv = (int64_t)q * NT + threadIdx.x;
+            if (jv < mv) cv[kk][q] = __ldcs(Crow + (k + kk) * kstride + jv);
+          }
+#pragma unroll
+        for (int kk = 0; kk < KU; ++kk)
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            const int64_t jv = (int64_t)q * NT + threadIdx.x;
+            if (jv >= mv) continue;
+            T tout[V];
+            element(q, cv[kk][q], tout);
+            if (Trow) __stcs(Trow + (k + kk) * kstride + jv, VecP<T, V>::pack(tout));
+          }
+      }
+      for (; k < p.n; ++k) {
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
           const int64_t jv = (int64_t)q * NT + threadIdx.x;
           if (jv >= mv) continue;
-          T c[V], tout[V];
-          VecP<T, V>::unpack(__ldcs(Crow + k * kstride + jv), c);
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const double a = ((double)g[q][v] - (double)c[v]) * inv_eps;   // <= 0
-            double e;
-            if constexpr (sizeof(T) == 4)
-              e = (double)exp2f((float)(a * COT_LOG2E));
-            else
-              e = exp(a);
-            const double Tv = E[q][v] * e;
-            transport = fma((double)c[v], Tv, transport);
-            ent = fma(Tv, (y[q][v] + a) - 1.0, ent);
-            row += Tv;
-            P[q][v] += Tv;
-            tout[v] = (T)Tv;
-          }
+          T tout[V];
+          element(q, __ldcs(Crow + k * kstride + jv), tout);
           if (Trow) __stcs(Trow + k * kstride + jv, VecP<T, V>::pack(tout));
         }
       }

@@ -78,20 +78,34 @@ __global__ void __launch_bounds__(256) k_zupdate(const double* __restrict__ c, i
 }
 
 // Local plan reductions into buf[b] = {transport, entropy sum, sum_i |r_i - alpha_i|, mass,
-// sum_{held rows} w_hat_i alpha_i, c_0 .. c_{m-1}} (all over the rows this call holds). One block per problem.
+// sum_{held rows} w_hat_i alpha_i, c_0 .. c_{m-1}} (all over the rows this call holds).
+// grid = (ceil(m/32), B), 256 threads: block x sums its 32 columns over the units (warp w takes units w, w+8,
+// ..., lanes the columns; the 8 warp sums combined in order, as k_colsum); block 0 also forms the scalars.
 __global__ void __launch_bounds__(256) k_plan_reduce_local(const double* __restrict__ partials,
                                                            const double* __restrict__ scal, int64_t upp, int64_t m,
                                                            int64_t row_begin, int64_t R,
                                                            const double* __restrict__ alpha,
                                                            const double* __restrict__ w_hat, double* __restrict__ buf) {
   __shared__ double sh[32];
-  const int64_t b = blockIdx.x;
+  __shared__ double shc[8][33];
+  const int64_t b = blockIdx.y;
   double* o = buf + b * (kPlanBufHead + m);
-  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
-    double c = 0.0;
-    for (int64_t u = 0; u < upp; ++u) c += partials[(b * upp + u) * m + j];
-    o[kPlanBufHead + j] = c;
+  {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+    double acc = 0.0;
+    if (j < m)
+      for (int64_t u = w; u < upp; u += 8) acc += partials[(b * upp + u) * m + j];
+    shc[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && j < m) {
+      double c = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) c += shc[ww][lane];
+      o[kPlanBufHead + j] = c;
+    }
   }
+  if (blockIdx.x != 0) return;
   double dot = 0.0;
   for (int64_t i = threadIdx.x; i < R; i += blockDim.x) dot += w_hat[b * m + row_begin + i] * alpha[b * m + row_begin + i];
   dot = warp_sum(dot);
@@ -182,8 +196,9 @@ cudaError_t launch_zupdate(const double* c, const double* beta, int64_t B, int64
 
 cudaError_t launch_plan_reduce_local(const IterArgs& a, const Workspace& ws, const UnitPlan& up, double* buf,
                                      cudaStream_t s) {
-  k_plan_reduce_local<<<(unsigned)a.B, 256, 0, s>>>(ws.partials[0], ws.plan_scal, up.upp, a.m, a.row_begin, a.R,
-                                                    a.alpha, a.w_hat, buf);
+  dim3 grid((unsigned)((a.m + 31) / 32), (unsigned)a.B);
+  k_plan_reduce_local<<<grid, 256, 0, s>>>(ws.partials[0], ws.plan_scal, up.upp, a.m, a.row_begin, a.R, a.alpha,
+                                           a.w_hat, buf);
   return cudaGetLastError();
 }
 
