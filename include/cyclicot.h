@@ -224,6 +224,15 @@ int cerot_plan_sharded(const double* alpha, const double* beta, const void* C_lo
                        const double* w_hat, const double* z_hat, void* T_local, double* d_report,
                        void* workspace, size_t ws_bytes, void* comm, void* stream);
 
+/* The whole solve of this rank: clot_aggregate of the held rows (into the workspace), cold  */
+/* start, cerot_iter_sharded in chunks of check_every with the freeze rule when tol > 0, then the   */
+/* plan of the held rows (T_local [n][R][m] if non-NULL) and the report reduced across ranks (HOST,       */
+/* identical on every rank). Synchronises. COT_NOT_CONVERGED if tol > 0 was not reached.                 */
+int cerot_solve_sharded(const double* alpha, const double* beta, const void* C_local, int64_t n, int64_t m,
+                        int64_t row_begin, int64_t R, int dtype, const double* eps, double tol, int64_t max_iter,
+                        int64_t check_every, uint32_t flags, double* w_hat, double* z_hat, void* T_local,
+                        void* workspace, size_t ws_bytes, void* comm, cot_report* report, void* stream);
+
 /* ---------------------------------------------------------------------------------------------- */
 /* Fused row sharding: the same partition and arithmetic as cerot_iter_sharded, but the    */
 /* exchange step runs INSIDE the persistent iteration kernel (one cooperative launch per rank for all     */

@@ -84,6 +84,9 @@ _SIGS = {
     # NEXT-4: host network simplex for the small LOT (host pointers)
     "clot_small_lot": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, ctypes.POINTER(_dbl), _vp, _vp,
                                       ctypes.POINTER(_i64)]),
+    "cerot_solve_sharded": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _dbl, _i64,
+                                           _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp, ctypes.POINTER(cot_report),
+                                           _vp]),
     # fused row sharding (in-kernel peer exchange; dist.py)
     "cot_xchg_bytes": (_sz, [_i64, ctypes.c_int]),
     "cot_xchg_alloc": (ctypes.c_int, [_i64, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), _vp]),

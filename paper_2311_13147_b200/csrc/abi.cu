@@ -943,4 +943,63 @@ int cerot_plan_sharded(const double* alpha, const double* beta, const void* C_lo
   return plan_and_report(a, ws, T_local, d_report, comm, (cudaStream_t)stream);
 }
 
+// Whole row-sharded solve of this rank (SURVEY §8(b) cerot_solve_sharded): A2 on the held rows, cold start,
+// iterations with the NCCL exchange (or none when comm == NULL) and the freeze rule checked every check_every,
+// plan of the held rows and the report reduced across ranks.
+int cerot_solve_sharded(const double* alpha, const double* beta, const void* C_local, int64_t n, int64_t m,
+                        int64_t row_begin, int64_t R, int dtype, const double* eps, double tol, int64_t max_iter,
+                        int64_t check_every, uint32_t flags, double* w_hat, double* z_hat, void* T_local,
+                        void* workspace, size_t ws_bytes, void* comm, cot_report* report, void* stream) {
+  int st = check_shape(1, n, m, dtype);
+  if (st) return st;
+  if (R < 1 || row_begin < 0 || row_begin + R > m) return arg_error("cerot_solve_sharded: bad row range");
+  if (!alpha || !beta || !C_local || !eps || !w_hat || !z_hat || !report)
+    return arg_error("cerot_solve_sharded: NULL argument");
+  if (max_iter < 0 || tol < 0) return arg_error("cerot_solve_sharded: max_iter >= 0 and tol >= 0 required");
+  if (check_every < 1) check_every = 1;
+  Workspace ws;
+  st = check_ws(workspace, ws_bytes, 1, n, m, R, dtype, &ws);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  COT_CHECK_CUDA(launch_aggregate(C_local, 1, n, m, dtype, ws.G, ws.A, ws.nonfinite, s, R));
+  st = cot_check_nonfinite(ws.nonfinite, stream);
+  if (st) return st;
+  COT_CHECK_CUDA(launch_init(alpha, beta, 1, m, flags | COT_COLD_START, z_hat, ws, s));
+  int64_t done = 0, it = 0;
+  int32_t conv = 0;
+  double res = 0.0;
+  while (done < max_iter) {
+    const int64_t chunk = std::min<int64_t>(check_every, max_iter - done);
+    st = cerot_iter_sharded(alpha, beta, C_local, ws.G, n, m, row_begin, R, dtype, eps, chunk, tol, check_every, flags,
+                            w_hat, z_hat, workspace, ws_bytes, comm, stream);
+    if (st) return st;
+    done += chunk;
+    if (tol > 0.0) {
+      st = cerot_state(workspace, 1, m, n, dtype, &it, &conv, &res, stream);
+      if (st) return st;
+      if (conv) break;
+    }
+  }
+  double* d_rep = ws.report;
+  st = cerot_plan_sharded(alpha, beta, C_local, ws.G, n, m, row_begin, R, dtype, eps, w_hat, z_hat, T_local, d_rep,
+                          workspace, ws_bytes, comm, stream);
+  if (st) return st;
+  double h[kReportDoubles];
+  COT_CHECK_CUDA(cudaMemcpyAsync(h, d_rep, sizeof(h), cudaMemcpyDeviceToHost, s));
+  st = cerot_state(workspace, 1, m, n, dtype, &it, &conv, &res, stream);
+  if (st) return st;
+  report->objective = h[0];
+  report->reg_primal = h[1];
+  report->dual = h[2];
+  report->row_l1 = h[3];
+  report->col_l1 = h[4];
+  report->col_l2 = h[5];
+  report->mass = h[6];
+  report->residual = h[7];
+  report->iters = it;
+  report->converged = conv;
+  report->status = (tol > 0.0 && !conv) ? COT_NOT_CONVERGED : COT_OK;
+  return report->status;
+}
+
 }  // extern "C"

@@ -180,6 +180,21 @@ class ShardedCerot:
                                         self._comm, _stream(self.stream)), "cerot_iter_sharded")
         return self
 
+    def solve(self, tol: float = 0.0, max_iter: int = 1000, check_every: int = 1, T_local: bool = False):
+        """The whole solve of this rank (cerot_solve_sharded): returns (T_local or None, report dict)."""
+        import torch
+        from . import cot_report, STATUS
+        T = torch.empty_like(self.C) if T_local else None
+        rep = cot_report()
+        code = lib().cerot_solve_sharded(_ptr(self.alpha), _ptr(self.beta), _ptr(self.C), self.n, self.m,
+                                         self.row_begin, self.R, self.dt, _ptr(self.eps), tol, max_iter, check_every,
+                                         COT_COLD_START, _ptr(self.w_hat), _ptr(self.z_hat), _ptr(T), _ptr(self.ws),
+                                         self.ws.numel(), self._comm, ctypes.byref(rep), _stream(self.stream))
+        _check(code, "cerot_solve_sharded", ok=(0, 1))
+        d = {f: getattr(rep, f) for f in REPORT_FIELDS}
+        d.update(iters=rep.iters, converged=bool(rep.converged), status=STATUS[rep.status])
+        return T, d
+
     def iterate_fused(self, xchg: "PeerExchange", iters: int, tol: float = 0.0, check_every: int = 1,
                       flags: int = 0):
         """`iters` iterations with the exchange inside the persistent kernel (cerot_iter_fused)."""

@@ -149,3 +149,28 @@ def test_batched_problem_sharding_is_exact():
     fullq = cot.CerotProblem(_dev(q.C), _dev(q.alpha), _dev(q.beta), _dev(q.eps)).init().iterate(20)
     part = cot.CerotProblem(_dev(q.C[1:3]), _dev(q.alpha[1:3]), _dev(q.beta[1:3]), _dev(q.eps[1:3])).init().iterate(20)
     assert np.allclose(part.z_hat.cpu().numpy(), fullq.z_hat.cpu().numpy()[1:3], rtol=0, atol=1e-9)
+
+
+def test_solve_sharded_single_rank_matches_solve():
+    """cerot_solve_sharded (the whole solve of one rank) with a 1-rank NCCL communicator and without one:
+    same iteration count and report as cerot_solve on the unsharded problem (C3, to tol 1e-8)."""
+    L = cot.lib()
+    uid = ctypes.create_string_buffer(128)
+    assert L.cot_nccl_unique_id(uid) == 0, L.cot_last_error()
+    comm = ctypes.c_void_p()
+    assert L.cot_comm_init(uid, 1, 0, ctypes.byref(comm)) == 0, L.cot_last_error()
+
+    class _C:
+        handle = comm
+    try:
+        p = synthetic.c3_image(pair=2)
+        _, _, _, reps = cot.cerot_solve(_dev(p.C), _dev(p.alpha), _dev(p.beta), p.eps, tol=1e-8, max_iter=3000,
+                                        check_every=5)
+        for c in (_C(), None):
+            sh = cdist.ShardedCerot(_dev(p.C), _dev(p.alpha), _dev(p.beta), float(p.eps[0]), 0, p.m, comm=c)
+            _, r = sh.solve(tol=1e-8, max_iter=3000, check_every=5)
+            assert r["converged"] and r["iters"] == reps[0]["iters"]
+            for k in ("objective", "dual"):
+                assert abs(r[k] - reps[0][k]) <= 1e-6 * abs(reps[0][k])
+    finally:
+        L.cot_comm_destroy(comm)
