@@ -48,7 +48,6 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, i
   (void)n;
   const UnitPlan up = unit_plan(B, R, sm_count);
   const size_t esz = dtype == COT_F32 ? 4 : 8;
-  const int64_t ntiles = (m + 31) / 32;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
@@ -63,7 +62,8 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, i
   w.grid_bar = reinterpret_cast<unsigned*>(take(16));
   w.nonfinite = reinterpret_cast<int32_t*>(take(4));
   w.report = reinterpret_cast<double*>(take((size_t)B * kReportDoubles * 8));
-  w.resid_part = reinterpret_cast<double*>(take((size_t)std::max<int64_t>(B * ntiles, sm_count) * 8));
+  // monitor partials: per 32-column tile (k_cols, k_zupdate) or per 8-column tile (C-SROT z-step)
+  w.resid_part = reinterpret_cast<double*>(take((size_t)std::max<int64_t>(B * ((m + 7) / 8), sm_count) * 8));
   if (B == 1) {   // LL lines of the persistent kernel
     const size_t o0 = off;
     w.lepoch = reinterpret_cast<unsigned long long*>(take(256));

@@ -86,32 +86,49 @@ __global__ void __launch_bounds__(256) k_srot_rows(const T* __restrict__ C, cons
   }
 }
 
-// z-step: lanes <-> 32 consecutive columns, 8 warps split the (i, k) range; per-column Newton, all columns
-// of the tile iterate together. First evaluation at the old z gives the plan's column sums c_j (monitor).
+// z-step: a block owns TW = 8 consecutive columns; thread t handles column t % TW and the (k, i) pairs
+// (t / TW) + q * (256 / TW) -- 32 partial sums per column, combined in a fixed order (deterministic). All
+// columns of the tile iterate their Newton steps together. The first evaluation at the old z gives the plan's
+// column sums c_j (monitor). grid = (ceil(m / TW), B).
+constexpr int kSrotTW = 8;
 template <typename T>
 __global__ void __launch_bounds__(256) k_srot_cols(const T* __restrict__ C, const double* __restrict__ beta,
                                                    const double* __restrict__ w, double* __restrict__ z,
                                                    const double* __restrict__ gam, int64_t n, int64_t m,
                                                    double* __restrict__ resid_part, SolverState* __restrict__ state,
                                                    unsigned* __restrict__ counters, double tol, int64_t check_every) {
+  constexpr int TW = kSrotTW, NG = 256 / TW;
   const int64_t b = blockIdx.y;
   const int ntiles = gridDim.x;
   if (!state[b].active) return;
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  const int c = threadIdx.x % TW, grp = threadIdx.x / TW;
+  const int64_t j = (int64_t)blockIdx.x * TW + c;
   const bool ok = j < m;
-  __shared__ double sS[8][32], sN[8][32];
+  __shared__ double sS[NG][TW], sN[NG][TW];
   __shared__ int any_active;
   __shared__ bool is_last;
   const double g = gam[b];
   const double Bt = ok ? beta[b * m + j] / g : 0.0;
   const T* Cb = C + b * n * m * m;
   const int64_t L = n * m;   // (k, i) pairs
+  auto reduce = [&](double& S, double& N, bool is_min) {
+    sS[grp][c] = S;
+    sN[grp][c] = N;
+    __syncthreads();
+    double a0 = sS[0][c], a1 = sN[0][c];
+    for (int q = 1; q < NG; ++q) {
+      a0 = is_min ? fmin(a0, sS[q][c]) : a0 + sS[q][c];
+      a1 += sN[q][c];
+    }
+    __syncthreads();
+    S = a0;
+    N = a1;
+  };
   auto pass = [&](double x, double& S, double& N) {
     S = 0.0;
     N = 0.0;
     if (ok)
-      for (int64_t l = wp; l < L; l += nw) {
+      for (int64_t l = grp; l < L; l += NG) {
         const int64_t k = l / m, i = l - k * m;
         const double d = x - ((double)Cb[(k * m + i) * m + j] - w[b * m + i]);
         if (d > 0.0) {
@@ -119,36 +136,23 @@ __global__ void __launch_bounds__(256) k_srot_cols(const T* __restrict__ C, cons
           N += 1.0;
         }
       }
-    sS[wp][lane] = S;
-    sN[wp][lane] = N;
-    __syncthreads();
-    S = 0.0;
-    N = 0.0;
-    for (int q = 0; q < nw; ++q) {
-      S += sS[q][lane];
-      N += sN[q][lane];
-    }
-    __syncthreads();
+    reduce(S, N, false);
   };
   // monitor: column sums of the plan after the w-step, at the old z
   const double zold = ok ? z[b * m + j] : 0.0;
   double S0, N0;
   pass(zold, S0, N0);
   const double cj = g * S0;
-  double dev = ok ? fabs(cj - beta[b * m + j]) : 0.0;
+  const double dev = ok && grp == 0 ? fabs(cj - beta[b * m + j]) : 0.0;
   // minimum breakpoint of this column
-  double lmin = INFINITY;
+  double lmin = INFINITY, dummy = 0.0;
   if (ok)
-    for (int64_t l = wp; l < L; l += nw) {
+    for (int64_t l = grp; l < L; l += NG) {
       const int64_t k = l / m, i = l - k * m;
       lmin = fmin(lmin, (double)Cb[(k * m + i) * m + j] - w[b * m + i]);
     }
-  sS[wp][lane] = lmin;
-  __syncthreads();
-  double bmin = INFINITY;
-  for (int q = 0; q < nw; ++q) bmin = fmin(bmin, sS[q][lane]);
-  __syncthreads();
-  double x = bmin + Bt;
+  reduce(lmin, dummy, true);
+  double x = lmin + Bt;
   bool act = ok;
   for (int it = 0; it < 200; ++it) {
     double S, N;
@@ -162,11 +166,15 @@ __global__ void __launch_bounds__(256) k_srot_cols(const T* __restrict__ C, cons
     __syncthreads();
     if (!any_active) break;
   }
-  if (ok && wp == 0) z[b * m + j] = x;
-  // monitor reduction (last block per problem, fixed order) + freeze rule
-  if (wp == 0) {
-    dev = warp_sum(dev);
-    if (lane == 0) resid_part[b * ntiles + blockIdx.x] = dev;
+  if (ok && grp == 0) z[b * m + j] = x;
+  // monitor reduction (per block in column order, then last block per problem in block order) + freeze rule
+  __shared__ double sdev[TW];
+  if (grp == 0) sdev[c] = dev;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double d = 0.0;
+    for (int q = 0; q < TW; ++q) d += sdev[q];
+    resid_part[b * ntiles + blockIdx.x] = d;
   }
   __threadfence();
   __syncthreads();
@@ -185,6 +193,35 @@ __global__ void __launch_bounds__(256) k_srot_cols(const T* __restrict__ C, cons
       st.converged = 1;
     }
     counters[b] = 0u;
+  }
+}
+
+// Column sums c_j of the plan gamma max(w_i + z_j - C_ijk, 0) for the report (same tile layout as the z-step).
+template <typename T>
+__global__ void __launch_bounds__(256) k_srot_colsum(const T* __restrict__ C, const double* __restrict__ w,
+                                                     const double* __restrict__ z, const double* __restrict__ gam,
+                                                     int64_t n, int64_t m, double* __restrict__ colsum) {
+  constexpr int TW = kSrotTW, NG = 256 / TW;
+  const int64_t b = blockIdx.y;
+  const int c = threadIdx.x % TW, grp = threadIdx.x / TW;
+  const int64_t j = (int64_t)blockIdx.x * TW + c;
+  __shared__ double sS[NG][TW];
+  double S = 0.0;
+  if (j < m) {
+    const double zj = z[b * m + j];
+    const T* Cb = C + b * n * m * m;
+    for (int64_t l = grp; l < n * m; l += NG) {
+      const int64_t k = l / m, i = l - k * m;
+      const double y = w[b * m + i] + zj - (double)Cb[(k * m + i) * m + j];
+      S += y > 0.0 ? y : 0.0;
+    }
+  }
+  sS[grp][c] = S;
+  __syncthreads();
+  if (grp == 0 && j < m) {
+    double t = 0.0;
+    for (int q = 0; q < NG; ++q) t += sS[q][c];
+    colsum[b * m + j] = gam[b] * t;
   }
 }
 
@@ -235,21 +272,18 @@ __global__ void __launch_bounds__(256) k_srot_finalize(const T* __restrict__ C, 
                                                        const double* __restrict__ alpha,
                                                        const double* __restrict__ beta,
                                                        const double* __restrict__ gam, const double* __restrict__ rowscal,
-                                                       int64_t n, int64_t m, const SolverState* __restrict__ state,
+                                                       const double* __restrict__ colsum, int64_t n, int64_t m,
+                                                       const SolverState* __restrict__ state,
                                                        double* __restrict__ report) {
   __shared__ double sh[128];
   int buf = 0;
   const int64_t b = blockIdx.x;
   const double g = gam[b];
+  (void)C;
+  (void)g;
   double cl1 = 0.0, cl2 = 0.0;
   for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
-    double c = 0.0;
-    for (int64_t k = 0; k < n; ++k)
-      for (int64_t i = 0; i < m; ++i) {
-        const double y = w[b * m + i] + z[b * m + j] - (double)C[((b * n + k) * m + i) * m + j];
-        c += y > 0.0 ? g * y : 0.0;
-      }
-    const double dv = c - beta[b * m + j];
+    const double dv = colsum[b * m + j] - beta[b * m + j];
     cl1 += fabs(dv);
     cl2 += dv * dv;
   }
@@ -286,7 +320,7 @@ cudaError_t launch_srot_sweep(const IterArgs& a, const double* gam, const Worksp
   const int sms = device_sm_count();
   const int64_t rows = a.B * a.m;
   const int grid = (int)std::min<int64_t>(rows, (int64_t)sms * 8);
-  dim3 cgrid((unsigned)((a.m + 31) / 32), (unsigned)a.B);
+  dim3 cgrid((unsigned)((a.m + kSrotTW - 1) / kSrotTW), (unsigned)a.B);
   if (a.dtype == COT_F32) {
     k_srot_rows<float><<<grid, 256, 0, s>>>((const float*)a.C, a.alpha, a.z_hat, a.w_hat, gam, a.B, a.n, a.m, ws.state);
     k_srot_cols<float><<<cgrid, 256, 0, s>>>((const float*)a.C, a.beta, a.w_hat, a.z_hat, gam, a.n, a.m, ws.resid_part,
@@ -306,16 +340,20 @@ cudaError_t launch_srot_plan(const IterArgs& a, const double* gam, const Workspa
   const int64_t rows = a.B * a.m;
   const int grid = (int)std::min<int64_t>(rows, (int64_t)sms * 8);
   double* rowscal = ws.rowscal;       // [B*m][4]
+  double* colsum = ws.c_local;        // [B][m]
+  dim3 cgrid((unsigned)((a.m + kSrotTW - 1) / kSrotTW), (unsigned)a.B);
   if (a.dtype == COT_F32) {
     k_srot_plan<float><<<grid, 256, 0, s>>>((const float*)a.C, a.w_hat, a.z_hat, a.alpha, gam, a.B, a.n, a.m,
                                             (float*)T_blocks, rowscal, nullptr);
+    k_srot_colsum<float><<<cgrid, 256, 0, s>>>((const float*)a.C, a.w_hat, a.z_hat, gam, a.n, a.m, colsum);
     k_srot_finalize<float><<<(unsigned)a.B, 256, 0, s>>>((const float*)a.C, a.w_hat, a.z_hat, a.alpha, a.beta, gam,
-                                                         rowscal, a.n, a.m, ws.state, report);
+                                                         rowscal, colsum, a.n, a.m, ws.state, report);
   } else {
     k_srot_plan<double><<<grid, 256, 0, s>>>((const double*)a.C, a.w_hat, a.z_hat, a.alpha, gam, a.B, a.n, a.m,
                                              (double*)T_blocks, rowscal, nullptr);
+    k_srot_colsum<double><<<cgrid, 256, 0, s>>>((const double*)a.C, a.w_hat, a.z_hat, gam, a.n, a.m, colsum);
     k_srot_finalize<double><<<(unsigned)a.B, 256, 0, s>>>((const double*)a.C, a.w_hat, a.z_hat, a.alpha, a.beta, gam,
-                                                          rowscal, a.n, a.m, ws.state, report);
+                                                          rowscal, colsum, a.n, a.m, ws.state, report);
   }
   return cudaGetLastError();
 }
