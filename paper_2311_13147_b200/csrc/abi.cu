@@ -62,8 +62,8 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, i
   w.grid_bar = reinterpret_cast<unsigned*>(take(16));
   w.nonfinite = reinterpret_cast<int32_t*>(take(4));
   w.report = reinterpret_cast<double*>(take((size_t)B * kReportDoubles * 8));
-  // monitor partials: per 32-column tile (k_cols, k_zupdate) or per 8-column tile (C-SROT z-step)
-  w.resid_part = reinterpret_cast<double*>(take((size_t)std::max<int64_t>(B * ((m + 7) / 8), sm_count) * 8));
+  // monitor partials: per 32-column tile (k_cols, k_zupdate) or per 4-column tile (C-SROT z-step)
+  w.resid_part = reinterpret_cast<double*>(take((size_t)std::max<int64_t>(B * ((m + 3) / 4), sm_count) * 8));
   if (B == 1) {   // LL lines of the persistent kernel
     const size_t o0 = off;
     w.lepoch = reinterpret_cast<unsigned long long*>(take(256));

@@ -52,31 +52,36 @@ __global__ void __launch_bounds__(256) k_srot_rows(const T* __restrict__ C, cons
                                                    const double* __restrict__ gam, int64_t B, int64_t n, int64_t m,
                                                    const SolverState* __restrict__ state) {
   __shared__ double sh[128];
+  extern __shared__ double zs[];   // [m] z of the current problem
   int buf = 0;
+  int64_t zb = -1;
   for (int64_t u = blockIdx.x; u < B * m; u += gridDim.x) {
     const int64_t b = u / m, i = u - b * m;
     if (!state[b].active) continue;
+    if (b != zb) {   // block-uniform
+      __syncthreads();
+      for (int64_t j = threadIdx.x; j < m; j += blockDim.x) zs[j] = z[b * m + j];
+      __syncthreads();
+      zb = b;
+    }
     const double g = gam[b];
     const double A = alpha[b * m + i] / g;
     const T* Cb = C + b * n * m * m + i * m;                       // C[b][k][i][j] = Cb[k*m*m + j]
-    const int64_t L = n * m;
     double lmin = INFINITY;
-    for (int64_t l = threadIdx.x; l < L; l += blockDim.x) {
-      const int64_t k = l / m, j = l - k * m;
-      lmin = fmin(lmin, (double)Cb[k * m * m + j] - z[b * m + j]);
-    }
+    for (int64_t k = 0; k < n; ++k)
+      for (int64_t j = threadIdx.x; j < m; j += blockDim.x) lmin = fmin(lmin, (double)Cb[k * m * m + j] - zs[j]);
     const double bmin = blk_min(lmin, sh, buf);
     double x = bmin + A;                                           // right of the root
     for (int it = 0; it < 200; ++it) {
       double S = 0.0, N = 0.0;
-      for (int64_t l = threadIdx.x; l < L; l += blockDim.x) {
-        const int64_t k = l / m, j = l - k * m;
-        const double d = x - ((double)Cb[k * m * m + j] - z[b * m + j]);
-        if (d > 0.0) {
-          S += d;
-          N += 1.0;
+      for (int64_t k = 0; k < n; ++k)
+        for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+          const double d = x - ((double)Cb[k * m * m + j] - zs[j]);
+          if (d > 0.0) {
+            S += d;
+            N += 1.0;
+          }
         }
-      }
       blk_sum2(S, N, sh, buf);
       const double F = S - A;                                      // >= 0 (convex, from the right)
       if (F <= 1e-14 * A || N == 0.0) break;
@@ -86,11 +91,11 @@ __global__ void __launch_bounds__(256) k_srot_rows(const T* __restrict__ C, cons
   }
 }
 
-// z-step: a block owns TW = 8 consecutive columns; thread t handles column t % TW and the (k, i) pairs
-// (t / TW) + q * (256 / TW) -- 32 partial sums per column, combined in a fixed order (deterministic). All
+// z-step: a block owns TW = 4 consecutive columns; thread t handles column t % TW and the (k, i) pairs
+// (t / TW) + q * (256 / TW) -- 64 partial sums per column, combined in a fixed order (deterministic). All
 // columns of the tile iterate their Newton steps together. The first evaluation at the old z gives the plan's
 // column sums c_j (monitor). grid = (ceil(m / TW), B).
-constexpr int kSrotTW = 8;
+constexpr int kSrotTW = 4;
 template <typename T>
 __global__ void __launch_bounds__(256) k_srot_cols(const T* __restrict__ C, const double* __restrict__ beta,
                                                    const double* __restrict__ w, double* __restrict__ z,
@@ -110,7 +115,6 @@ __global__ void __launch_bounds__(256) k_srot_cols(const T* __restrict__ C, cons
   const double g = gam[b];
   const double Bt = ok ? beta[b * m + j] / g : 0.0;
   const T* Cb = C + b * n * m * m;
-  const int64_t L = n * m;   // (k, i) pairs
   auto reduce = [&](double& S, double& N, bool is_min) {
     sS[grp][c] = S;
     sN[grp][c] = N;
@@ -124,16 +128,35 @@ __global__ void __launch_bounds__(256) k_srot_cols(const T* __restrict__ C, cons
     S = a0;
     N = a1;
   };
+  extern __shared__ double ws_[];   // [m] w of this problem
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) ws_[i] = w[b * m + i];
+  __syncthreads();
   auto pass = [&](double x, double& S, double& N) {
     S = 0.0;
     N = 0.0;
     if (ok)
-      for (int64_t l = grp; l < L; l += NG) {
-        const int64_t k = l / m, i = l - k * m;
-        const double d = x - ((double)Cb[(k * m + i) * m + j] - w[b * m + i]);
-        if (d > 0.0) {
-          S += d;
-          N += 1.0;
+      for (int64_t k = 0; k < n; ++k) {
+        const T* Ck = Cb + k * m * m + j;
+        int64_t i = grp;
+        for (; i + 3 * NG < m; i += 4 * NG) {   // 4 loads in flight
+          T cv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cv[q] = Ck[(i + q * NG) * m];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double d = x - ((double)cv[q] - ws_[i + q * NG]);
+            if (d > 0.0) {
+              S += d;
+              N += 1.0;
+            }
+          }
+        }
+        for (; i < m; i += NG) {
+          const double d = x - ((double)Ck[i * m] - ws_[i]);
+          if (d > 0.0) {
+            S += d;
+            N += 1.0;
+          }
         }
       }
     reduce(S, N, false);
@@ -147,10 +170,8 @@ __global__ void __launch_bounds__(256) k_srot_cols(const T* __restrict__ C, cons
   // minimum breakpoint of this column
   double lmin = INFINITY, dummy = 0.0;
   if (ok)
-    for (int64_t l = grp; l < L; l += NG) {
-      const int64_t k = l / m, i = l - k * m;
-      lmin = fmin(lmin, (double)Cb[(k * m + i) * m + j] - w[b * m + i]);
-    }
+    for (int64_t k = 0; k < n; ++k)
+      for (int64_t i = grp; i < m; i += NG) lmin = fmin(lmin, (double)Cb[(k * m + i) * m + j] - ws_[i]);
   reduce(lmin, dummy, true);
   double x = lmin + Bt;
   bool act = ok;
@@ -321,14 +342,16 @@ cudaError_t launch_srot_sweep(const IterArgs& a, const double* gam, const Worksp
   const int64_t rows = a.B * a.m;
   const int grid = (int)std::min<int64_t>(rows, (int64_t)sms * 8);
   dim3 cgrid((unsigned)((a.m + kSrotTW - 1) / kSrotTW), (unsigned)a.B);
+  const size_t zbytes = (size_t)a.m * 8;   // z (w-step) or w (z-step) of one problem in shared memory
+  if (zbytes > 48 * 1024) return cudaErrorInvalidValue;
   if (a.dtype == COT_F32) {
-    k_srot_rows<float><<<grid, 256, 0, s>>>((const float*)a.C, a.alpha, a.z_hat, a.w_hat, gam, a.B, a.n, a.m, ws.state);
-    k_srot_cols<float><<<cgrid, 256, 0, s>>>((const float*)a.C, a.beta, a.w_hat, a.z_hat, gam, a.n, a.m, ws.resid_part,
+    k_srot_rows<float><<<grid, 256, zbytes, s>>>((const float*)a.C, a.alpha, a.z_hat, a.w_hat, gam, a.B, a.n, a.m, ws.state);
+    k_srot_cols<float><<<cgrid, 256, zbytes, s>>>((const float*)a.C, a.beta, a.w_hat, a.z_hat, gam, a.n, a.m, ws.resid_part,
                                              ws.state, ws.counters, a.tol, a.check_every);
   } else {
-    k_srot_rows<double><<<grid, 256, 0, s>>>((const double*)a.C, a.alpha, a.z_hat, a.w_hat, gam, a.B, a.n, a.m,
+    k_srot_rows<double><<<grid, 256, zbytes, s>>>((const double*)a.C, a.alpha, a.z_hat, a.w_hat, gam, a.B, a.n, a.m,
                                              ws.state);
-    k_srot_cols<double><<<cgrid, 256, 0, s>>>((const double*)a.C, a.beta, a.w_hat, a.z_hat, gam, a.n, a.m,
+    k_srot_cols<double><<<cgrid, 256, zbytes, s>>>((const double*)a.C, a.beta, a.w_hat, a.z_hat, gam, a.n, a.m,
                                               ws.resid_part, ws.state, ws.counters, a.tol, a.check_every);
   }
   return cudaGetLastError();
