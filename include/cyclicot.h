@@ -59,6 +59,8 @@ typedef enum {
                                  z_hat is a warm start                                                  */
 #define COT_FORCE_LDG  0x2u   /* use the generic LDG row kernels even where the TMA (large problems)  */
                               /* or cluster-resident (small problems) kernels apply                    */
+#define COT_FORCE_TMA  0x8u   /* B == 1 fp32 problems that would run cluster-resident use the persistent  */
+                              /* TMA-streaming kernel instead (tests of that kernel on small shapes)     */
 #define COT_PRECOMPUTED 0x4u  /* NEXT-1: `C` is S from cerot_precompute ([B][1][m][m], pass n = 1); the  */
                               /* row pass uses s_ij = S_ij instead of re-streaming the n blocks          */
 /* Diagnostic flags (results are NOT valid with them; used by scripts/ubench_iter.py only):          */

@@ -358,7 +358,8 @@ static size_t batch_smem_bytes(int n, int m, int RB, int nwarps) {
 }
 
 bool batch_cluster_eligible(const IterArgs& a) {
-  if (a.dtype != COT_F32 || a.m % 4 != 0 || a.m > 256 || a.m < kNCL || a.R != a.m || (a.flags & COT_FORCE_LDG))
+  if (a.dtype != COT_F32 || a.m % 4 != 0 || a.m > 256 || a.m < kNCL || a.R != a.m ||
+      (a.flags & (COT_FORCE_LDG | COT_FORCE_TMA)))
     return false;
   const int RB = (int)((a.m + kNCL - 1) / kNCL);
   if (RB > 32) return false;

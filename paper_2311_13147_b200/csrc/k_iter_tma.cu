@@ -1092,7 +1092,8 @@ void trace_end(const unsigned long long* trace, int grid, int iters, cudaStream_
 
 cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, bool rows_only, int parity,
                             cudaStream_t s) {
-  const int sms = device_sm_count();
+  int sms = device_sm_count();
+  if (const char* ev = getenv("COT_MAX_CTAS")) sms = std::max(1, std::min(sms, atoi(ev)));   // experiments
   TmaParams p;
   TmaCfg cfg;
   cudaError_t e = tma_config(a, ws, iters, rows_only, parity, sms, &p, &cfg);

@@ -361,3 +361,20 @@ def test_c5_full_batch_in_the_bench_launch_configuration_sampled():
         assert np.array_equal(Tfull[b].cpu().numpy(), oracle.expand_plan(Tb))
     del Tfull, T, C, prob
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n,m,R_seed", [(1, 4, 1), (3, 12, 2), (5, 64, 3), (17, 132, 4), (33, 256, 5), (2, 1020, 6),
+                                        (40, 512, 7)])
+def test_tma_kernel_shapes(n, m, R_seed):
+    """The persistent TMA kernel (forced on shapes the cluster kernel would take) on ragged shapes: n = 1, n not a
+    multiple of the slot's k-rows, m not a multiple of the warp width, m up to 1020; 25 iterations against the
+    oracle, and a second launch continuing from the first (the epoch / reference hand-over across launches)."""
+    p = synthetic.random_cyclic(seed=100 + R_seed, n=n, m=m, dtype=np.float32, eps=0.05)
+    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps)).init()
+    prob.iterate(15, flags=cot.COT_FORCE_TMA)
+    prob.iterate(10, flags=cot.COT_FORCE_TMA)
+    T, rep = prob.plan(T_blocks=True)
+    w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, 0.05, 25, form="kernel")
+    _compare(p, rep.cpu().numpy()[0], T.cpu().numpy(), w, z)
+    it, _, _ = prob.state()
+    assert it[0] == 25
