@@ -278,6 +278,27 @@ class ShardedRunner:
         self.sh = cdist.ShardedCerot(torch.as_tensor(Cl, device=dev), torch.as_tensor(p.alpha, device=dev),
                                      torch.as_tensor(p.beta, device=dev), float(p.eps[0]), self.row_begin, p.m,
                                      comm=self.comm, stream=stream)
+        if self.fused:
+            # probe: a few fused iterations must complete on every rank (peer stores visible, no COT_E_PEER)
+            # before the bench relies on the path; otherwise every rank falls back to the NCCL baseline
+            ok, err = 1, ""
+            try:
+                with stdout_to_stderr():
+                    self.sh.init().iterate_fused(self.xchg, 3)
+                    if self.sh.state()[0] != 3:
+                        ok, err = 0, "probe iterations incomplete"
+            except Exception as e:
+                ok, err = 0, str(e)
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+            import torch.distributed as tdist
+            if tdist.is_initialized():
+                tdist.all_reduce(flag, op=tdist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                self.xchg.close()
+                self.xchg = None
+                self.fused = False
+                self.fused_note = f"fused exchange probe failed ({err or 'on another rank'}): NCCL baseline"
+                print(f"[bench] {self.fused_note}", file=sys.stderr)
         d = p.n * p.m
         self.Tl = torch.empty_like(self.sh.C)
         self.Trows = torch.empty((p.n, self.R, d), dtype=self.sh.C.dtype, device=dev)

@@ -173,17 +173,26 @@ __device__ __forceinline__ double cblk_sum1(double v, double* red2, int& buf, in
   return v;
 }
 
-// s * e^d for d in fp64 and s in fp32: 2^round(d log2e) built exactly in the exponent bits (the round by the
-// 1.5*2^52 trick, valid for |d| < 1e15), times s * 2^frac (|frac| <= 1/2) in fp32 with MUFU.EX2, so the
-// rounding of the argument costs < 3e-8 relative regardless of |d|. The exponent is clamped to
-// [-1022, 1000]: terms below 2^-1022 come out ~1e-308 (negligible), terms above 2^1000 make the caller's
-// row-sum range check redo the row exactly. Two conversions, no branch.
-__device__ __forceinline__ double exp_scaled(double d, float s) {
-  const double a = d * COT_LOG2E;
-  const double big = a + 6755399441055744.0;
-  const int ai = min(max(__double2loint(big), -1022), 1000);
-  const float f = (float)(a - (big - 6755399441055744.0));
-  return (double)(s * ex2(f)) * __hiloint2double((ai + 1023) << 20, 0);
+// The epilogue's exponentials in split form. Every term is t_ij = s'_ij 2^{zL_j - kM_i - a_ij} with
+// s'_ij = sum_k 2^{a_ij - C_ijk log2e/eps} from the k-sum warps (a_ij = round(G_ij log2e/eps), an integer, so
+// s'_ij lies in [2^-1/2, 1.42 n]), zL_j = z_j log2e and kM_i an integer row shift (the rounded log2 of the
+// previous iteration's row log-sum-exp). zL_j is split once per column per iteration into an integer kz_j and
+// Fz_j = 2^{zL_j - kz_j} in fp64 (split_pow2_fp64); per element that leaves an integer exponent
+// e = kz_j - kM_i - a_ij assembled into the fp64 bits of s'_ij (ldexp_pos, no conversion) and one fp64
+// product by Fz_j. The only per-element rounding is the fp32 k-sum's (random across i, averaged in the
+// column sums); no factor common to a row or a column is rounded below fp64.
+__device__ __forceinline__ double split_pow2_fp64(double x, int& k) {
+  const double big = x + 6755399441055744.0;   // 1.5 * 2^52: round to an integer in the low word
+  k = __double2loint(big);
+  return exp2(x - (big - 6755399441055744.0));
+}
+// f * 2^e, exactly, for f in [2^-22, 2^23) (here f = s'_ij in [0.7, 1.42 n]) and e clamped to [-1000, 1000]:
+// terms below 2^-1000 come out ~1e-301 (negligible), terms above 2^1000 make the caller's row-sum range check
+// redo the row exactly. Integer operations only.
+__device__ __forceinline__ double ldexp_pos(float f, int e) {
+  const unsigned b = __float_as_uint(f);
+  e = min(max(e, -1000), 1000);
+  return __hiloint2double((int)((b >> 3) + ((unsigned)(e + 896) << 20)), (int)(b << 29));
 }
 
 // One-barrier block reductions of N values over the epilogue warps (<= 8 warps; double-buffered scratch).
@@ -253,8 +262,8 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
   // ---- shared memory layout
   float* ring = reinterpret_cast<float*>(smem);
   float* queue = reinterpret_cast<float*>(smem + (size_t)p.nslot * slot_floats * 4 + 1024);   // [QN][m]
-  double* gsh = reinterpret_cast<double*>(queue + (size_t)QN * m);      // [rpu][m] -G/eps in fp64 if p.gsh
-  double* rowstat = gsh + (p.gsh ? (size_t)rpu * m : 0);                 // [rpu][RS]
+  int* gsh = reinterpret_cast<int*>(queue + (size_t)QN * m);            // [rpu][m] a_ij = round(G_ij log2e/eps)
+  double* rowstat = reinterpret_cast<double*>(gsh + (size_t)rpu * m);    // [rpu][RS] (rpu * m even: m % 4 == 0)
   double* xs = rowstat + (size_t)rpu * RS;                               // [kColScratch] column-pass scratch
   uint64_t* full = reinterpret_cast<uint64_t*>(xs + kColScratch);
   uint64_t* empty = full + p.nslot;
@@ -280,12 +289,13 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
     fence_mbar_init();
   }
   const double inv_eps = 1.0 / p.eps[0];
-  if (p.gsh) {   // this CTA's rows of -G/eps in fp64, read by the epilogue warps every iteration
+  const float c2 = (float)(COT_LOG2E * inv_eps);
+  {   // this CTA's rows of the integer shifts a_ij, computed exactly as the k-sum warps compute them
     const VT* src = reinterpret_cast<const VT*>(p.G + (size_t)i0 * m);
     for (int idx = threadIdx.x; idx < nrows * mv; idx += blockDim.x) {
       const float4 g4 = __ldg(src + idx);
-      reinterpret_cast<double2*>(gsh)[2 * idx] = make_double2(-(double)g4.x * inv_eps, -(double)g4.y * inv_eps);
-      reinterpret_cast<double2*>(gsh)[2 * idx + 1] = make_double2(-(double)g4.z * inv_eps, -(double)g4.w * inv_eps);
+      reinterpret_cast<int4*>(gsh)[idx] = make_int4(__float2int_rn(g4.x * c2), __float2int_rn(g4.y * c2),
+                                                    __float2int_rn(g4.z * c2), __float2int_rn(g4.w * c2));
     }
   }
   __syncthreads();
@@ -341,7 +351,6 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
     // queue; never waits for the potentials. Threads past the last column compute (in-bounds) garbage that
     // the epilogue masks out, so the slot body has no per-column branches.
     const int kt = threadIdx.x;
-    const float c2 = (float)(COT_LOG2E * inv_eps);
     uint32_t slot = 0, phase = 0, qs = 0, qph = 0;
     unsigned consumed = 0, produced = 0;
     long long c_ksum = 0, c_kqw = 0;
@@ -373,15 +382,19 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       asm volatile("bar.sync 3, %0;" ::"r"(nkt) : "memory");
       if (halt) break;
       const int r = rr % nrows;
-      float gc[CPT][VEC], s[CPT][VEC];
+      // the row's integer shifts a_ij = round(G_ij log2e/eps): s'_ij = sum_k 2^{a_ij - C_ijk log2e/eps}, one
+      // rounding per term (the product is exact inside the FMA); the G-shifted S_ij of the precomputed mode is
+      // rescaled by 2^{a_ij - G_ij log2e/eps} (|.| <= 1/2) to the same convention
+      float gc[CPT][VEC], s[CPT][VEC], pf[CPT][VEC];
 #pragma unroll
       for (int q = 0; q < CPT; ++q) {
-        gc[q][0] = gnext[q].x * c2;
-        gc[q][1] = gnext[q].y * c2;
-        gc[q][2] = gnext[q].z * c2;
-        gc[q][3] = gnext[q].w * c2;
+        const float gv[VEC] = {gnext[q].x, gnext[q].y, gnext[q].z, gnext[q].w};
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) s[q][v] = 0.f;
+        for (int v = 0; v < VEC; ++v) {
+          gc[q][v] = (float)__float2int_rn(gv[v] * c2);
+          pf[q][v] = p.pre ? ex2(fmaf(-gv[v], c2, gc[q][v])) : 1.f;
+          s[q][v] = 0.f;
+        }
       }
       load_g(r + 1 < nrows ? i0 + r + 1 : i0);
       const long long tk0 = p.trace ? clock64() : 0;
@@ -393,10 +406,10 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
 #pragma unroll
           for (int q = 0; q < CPT; ++q) {
             const float4 c = sb[q * nkt + kt];
-            s[q][0] = c.x;
-            s[q][1] = c.y;
-            s[q][2] = c.z;
-            s[q][3] = c.w;
+            s[q][0] = c.x * pf[q][0];
+            s[q][1] = c.y * pf[q][1];
+            s[q][2] = c.z * pf[q][2];
+            s[q][3] = c.w * pf[q][3];
           }
         } else if (!(p.diag & COT_DIAG_NO_COMPUTE)) {
 #pragma unroll
@@ -512,13 +525,15 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
     asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
     SolverState st = p.state[0];
     const long long iters0 = st.iters;
-    double z[EPT][VEC], P[EPT][VEC];
+    double P[EPT][VEC];
+    int kz[EPT][VEC];     // z_j log2e = kz_j + f_j, Fz_j = 2^{f_j} (fp64): once per column per iteration
+    double Fz[EPT][VEC];
 #pragma unroll
     for (int q = 0; q < EPT; ++q)
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         const int jv = q * net + et;
-        z[q][v] = jv < mv ? __ldcg(p.z_hat + VEC * jv + v) : 0.0;
+        Fz[q][v] = split_pow2_fp64((jv < mv ? __ldcg(p.z_hat + VEC * jv + v) : 0.0) * COT_LOG2E, kz[q][v]);
         P[q][v] = 0.0;
       }
     auto need_resid = [&](int t) {
@@ -568,7 +583,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
               }
             }
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) z[q][v] = ll_value(zl[v]);
+            for (int v = 0; v < VEC; ++v) Fz[q][v] = split_pow2_fp64(ll_value(zl[v]) * COT_LOG2E, kz[q][v]);
           }
         }
         if (need_resid(t - 1)) st.residual = read_resid(g) * (double)n;
@@ -634,18 +649,18 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
               continue;
             }
             const int rb = r0 + (b < nb ? b : 0);
+            const int kM = __double2int_rn(Mref[b] * COT_LOG2E);   // integer row shift (exact: no rounded factor)
 #pragma unroll
             for (int q = 0; q < EPT; ++q) {
               const int jv = q * net + et;
               const bool ok = use && jv < mv && b < nb;
               const int jc = jv < mv ? jv : 0;
               const float4 s4 = reinterpret_cast<const VT*>(queue + (size_t)qsb[b] * m)[jc];
-              const double2* g2 = reinterpret_cast<const double2*>(gsh + (size_t)rb * m) + 2 * jc;
-              const double2 ga = g2[0], gb = g2[1];
-              const double t0 = exp_scaled(z[q][0] + ga.x - Mref[b], s4.x);
-              const double t1 = exp_scaled(z[q][1] + ga.y - Mref[b], s4.y);
-              const double t2 = exp_scaled(z[q][2] + gb.x - Mref[b], s4.z);
-              const double t3 = exp_scaled(z[q][3] + gb.y - Mref[b], s4.w);
+              const int4 a4 = reinterpret_cast<const int4*>(gsh + (size_t)rb * m)[jc];
+              const double t0 = ldexp_pos(s4.x, kz[q][0] - kM - a4.x) * Fz[q][0];
+              const double t1 = ldexp_pos(s4.y, kz[q][1] - kM - a4.y) * Fz[q][1];
+              const double t2 = ldexp_pos(s4.z, kz[q][2] - kM - a4.z) * Fz[q][2];
+              const double t3 = ldexp_pos(s4.w, kz[q][3] - kM - a4.w) * Fz[q][3];
               tt[b][q][0] = ok ? t0 : 0.0;
               tt[b][q][1] = ok ? t1 : 0.0;
               tt[b][q][2] = ok ? t2 : 0.0;
@@ -675,13 +690,14 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
 #pragma unroll
               for (int v = 0; v < VEC; ++v) {
                 const int jv = q * net + et;
-                if (jv < mv && b < nb) mx[b] = fmax(mx[b], z[q][v] + gsh[(size_t)rb * m + VEC * jv + v]);
+                if (jv < mv && b < nb)   // the largest kz_j - a_ij: every term <= 2^{1/2} s'_ij, the largest >= 1/2
+                  mx[b] = fmax(mx[b], (double)(kz[q][v] - gsh[(size_t)rb * m + VEC * jv + v]));
               }
           }
           cblk_maxN<RB>(mx, red2, rbuf, net, nk);
 #pragma unroll
           for (int b = 0; b < RB; ++b) {
-            Mref[b] = b < nb ? mx[b] : 0.0;
+            Mref[b] = b < nb ? mx[b] * COT_LN2 : 0.0;
             sm[b] = 0.0;
           }
           batch_terms(true);
@@ -708,8 +724,10 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
           rinv = rinv * fma(-rsum, rinv, 2.0);
           rinv = rinv * fma(-rsum, rinv, 2.0);
           const double rho = rowstat[r * RS + 4] * rinv;
-          if (et == 0) {
-            rowstat[r * RS + 1] = Mref[b];           // shift used for r_i
+          if (et == 0) {   // the shift used for r_i, r_i, and the next iteration's shift: kM + floor(log2 r_i)
+            const int kM = __double2int_rn(Mref[b] * COT_LOG2E);
+            rowstat[r * RS + 0] = (double)(kM + ((__double2hiint(rsum) >> 20) - 1023)) * COT_LN2;
+            rowstat[r * RS + 1] = (double)kM * COT_LN2;
             rowstat[r * RS + 2] = rsum;
           }
 #pragma unroll
@@ -719,14 +737,17 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         }
         if (p.trace) c_epi += clock64() - te0;
       }
-      // ---- w_hat of this CTA's rows (parallel logs)
-      asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
-      for (int r = et; r < nrows; r += net) {   // LSE_i = Mref_i + log r_i: w_hat_i and the next reference
-        const double lse = rowstat[r * RS + 1] + log(rowstat[r * RS + 2]);
-        p.w_hat[p.row_begin + i0 + r] = rowstat[r * RS + 3] - lse;
-        rowstat[r * RS + 0] = lse;
-      }
+      // ---- w_hat of this CTA's rows, LSE_i = shift_i + log r_i, by the warp of the thread that wrote the row
+      // statistics (no block barrier); off the critical path in the iterated launch (after the partial lines are out)
+      auto write_w_hat = [&]() {
+        if (et < 32) {   // the writer's warp (__syncwarp orders its shared-memory writes for the lanes)
+          __syncwarp();
+          for (int r = et; r < nrows; r += 32)
+            p.w_hat[p.row_begin + i0 + r] = rowstat[r * RS + 3] - (rowstat[r * RS + 1] + log(rowstat[r * RS + 2]));
+        }
+      };
       if (p.rows_only) {   // cerot_rows: the plain fp64 partial, no device-wide step
+        write_w_hat();
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
           const int jv = q * net + et;
@@ -737,6 +758,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         break;
       }
       if (!sync) {   // diagnostics (COT_DIAG_NO_SYNC): no column pass, z_hat unchanged
+        write_w_hat();
 #pragma unroll
         for (int q = 0; q < EPT; ++q)
 #pragma unroll
@@ -761,6 +783,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
           for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
         }
       }
+      write_w_hat();
       // ---- column pass of this CTA's slice: c_j = sum_u P_uj in unit order; q-update; z lines
       const long long tc0 = p.trace ? clock64() : 0;
       if (p.trace) c_pub += tc0 - tp0;
@@ -939,8 +962,8 @@ __global__ void __launch_bounds__(416, 1) k_iter_tma_emu(const __grid_constant__
 // ------------------------------------------------------------------------------------------ launcher
 bool tma_eligible(const IterArgs& a, int sms) {
   if (sms <= 0) sms = device_sm_count();
-  const int64_t rpu = unit_plan(1, a.R, sms).rpu;   // -G/eps of a CTA's rows (fp64) is staged in <= 64 KB
-  return a.dtype == COT_F32 && a.B == 1 && a.m % 4 == 0 && a.m <= 1024 && rpu * a.m * 8 <= 65536 &&
+  const int64_t rpu = unit_plan(1, a.R, sms).rpu;   // the shifts a_ij of a CTA's rows (int32) fit in <= 64 KB
+  return a.dtype == COT_F32 && a.B == 1 && a.m % 4 == 0 && a.m <= 1024 && rpu * a.m * 4 <= 65536 &&
          !(a.flags & COT_FORCE_LDG);
 }
 
@@ -998,7 +1021,7 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
   p.qn = std::max(1, std::min(p.rpu, 8));
   if (const char* ev = getenv("COT_QN")) p.qn = std::max(1, atoi(ev));
   p.qn = std::max(p.qn, std::min(p.rpu, 4));   // the epilogue holds up to one batch (<= 4 rows) of queue slots
-  const size_t gsh_bytes = (size_t)p.rpu * m * 8;   // -G/eps in fp64
+  const size_t gsh_bytes = (size_t)p.rpu * m * 4;   // the integer shifts a_ij
   p.gsh = 1;
   if (gsh_bytes > 64 * 1024) return cudaErrorInvalidConfiguration;   // see tma_eligible
   const size_t queue_bytes = (size_t)p.qn * row_bytes + (p.gsh ? gsh_bytes : 0) + (size_t)p.rpu * 6 * 8 +
