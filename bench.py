@@ -442,7 +442,7 @@ def run_ours(args, rank, world, local_rank):
                   (f" [{R.fused_note}]" if R.fused_note else ""))
     else:
         kernel = {1: "k_iter_tma (persistent: all iterations in one launch)",
-                  2: "k_batch_cluster (8-CTA cluster per problem, all iterations in one launch, on chip)"}.get(
+                  2: "k_batch_cluster (one thread-block cluster per problem: 8 CTAs while the batch fits one wave, else 6; all iterations in one launch, on chip)"}.get(
                       getattr(R, "path", 0), "k_rows_ldg + k_cols (one launch pair per iteration)")
     trf = _ncu_traffic_per_iter(args.workload) if world == 1 else None
     metric = _metric()

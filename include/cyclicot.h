@@ -66,6 +66,8 @@ typedef enum {
 /* Diagnostic flags (results are NOT valid with them; used by scripts/ubench_iter.py only):          */
 #define COT_DIAG_NO_COMPUTE 0x100u  /* TMA kernel: consumers only acknowledge slots (pure HBM stream)    */
 #define COT_DIAG_NO_SYNC    0x200u  /* TMA kernel: skip the column pass and device-wide barriers        */
+#define COT_DIAG_NO_STREAM  0x400u  /* TMA kernel: stream C in the first iteration only (later k-sums    */
+                                    /* read stale slots: wrong results; isolates the sync chain)         */
 
 /* Layout of one problem's report (HOST struct; the device report is the same 8 doubles + 2 ints). */
 typedef struct {

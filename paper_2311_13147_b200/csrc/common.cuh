@@ -18,6 +18,22 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x = 2^k * 2^f with k = round(x) an integer and 2^f (|f| <= 1/2) in fp64 (the 1.5 * 2^52 rounding trick,
+// valid for |x| < 2^31).
+__device__ __forceinline__ double split_pow2_fp64(double x, int& k) {
+  const double big = x + 6755399441055744.0;   // 1.5 * 2^52: round to an integer in the low word
+  k = __double2loint(big);
+  return exp2(x - (big - 6755399441055744.0));
+}
+// f * 2^e, exactly, for f in [2^-22, 2^23) (the k-sums s'_ij lie in [0.7, 1.42 n]) and e clamped to
+// [-1000, 1000]: terms below 2^-1000 come out ~1e-301 (negligible); callers whose exponents can exceed 1000
+// check the sums' range. Integer operations only.
+__device__ __forceinline__ double ldexp_pos(float f, int e) {
+  const unsigned b = __float_as_uint(f);
+  e = min(max(e, -1000), 1000);
+  return __hiloint2double((int)((b >> 3) + ((unsigned)(e + 896) << 20)), (int)(b << 29));
+}
+
 __device__ __forceinline__ bool finite_f(float x) { return fabsf(x) <= 3.402823466e38f; }
 __device__ __forceinline__ bool finite_f(double x) { return fabs(x) <= 1.7976931348623157e308; }
 

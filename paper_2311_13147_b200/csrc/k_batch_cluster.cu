@@ -4,10 +4,13 @@
 // One thread-block cluster of NCL = 8 CTAs per problem. CTA c holds rows [c*RB, (c+1)*RB) of every cost
 // block in shared memory (RB*n*m fp32; 128 KiB for C5), loaded once with TMA bulk copies, plus its G rows
 // and a replica of z_hat. One warp per row, VEC = 4 columns per lane (x VPL):
-//   k-sum       s_ij = sum_k exp2((G_ij - C_ijk) log2e/eps) from shared memory (FFMA + MUFU.EX2 + FADD);
-//   epilogue    x_ij = z_hat_j - G_ij/eps (fp64), M_i = max_j x_ij and r_i by warp shuffles (no block
-//               barrier: a row lives in one warp), w_hat_i = log alpha_i - M_i - log r_i,
-//               column terms (alpha_i / r_i) s_ij exp(x_ij - M_i) accumulated per warp in fp64;
+//   k-sum       s'_ij = sum_k exp2(a_ij - C_ijk log2e/eps) from shared memory (FFMA + MUFU.EX2 + FADD), with
+//               the integer shift a_ij = round(G_ij log2e/eps) (s'_ij in [0.7, 1.42 n]);
+//   epilogue    t_ij = s'_ij 2^{kz_j - a_ij - kM_i} Fz_j with z_hat_j log2e = kz_j + log2 Fz_j split once per
+//               column per iteration (kept in the replica next to z_hat) and kM_i = max_j (kz_j - a_ij) by one
+//               integer warp reduction: the exponent goes into the fp64 bits, one fp64 product, no MUFU and
+//               no conversion per element. r_i by warp shuffles (no block barrier: a row lives in one warp),
+//               w_hat_i = log alpha_i - kM_i ln2 - log r_i, column terms (alpha_i / r_i) t_ij in fp64;
 //   columns     per-CTA column partials in shared memory; after a cluster barrier CTA c sums the 8 CTAs'
 //               partials of its column slice through DSMEM in CTA order (deterministic), applies the
 //               q-update z_hat_j += log beta_j - log c_j and writes z_hat_j into every CTA's replica (DSMEM);
@@ -29,7 +32,7 @@ namespace cg = cooperative_groups;
 
 namespace cot {
 
-constexpr int kNCL = 8;   // CTAs per cluster (portable maximum)
+constexpr int kMaxNCL = 16;   // CTAs per cluster: up to the non-portable maximum
 
 struct BatchParams {
   const float* C;        // [B][n][m][m]
@@ -45,28 +48,35 @@ struct BatchParams {
   double tol;
   long long check_every;
   int pre;               // precomputed mode (NEXT-1): C is S [B][1][m][m], s_ij = S_ij
+  int ncl;               // CTAs per cluster (one problem per cluster)
+  int gs_log;            // log2 of the column-pass group (a power of two >= ncl: 8 or 16 lanes)
   unsigned long long* trace;   // diagnostics (COT_TRACE=1): [grid][8] cycle counters, or nullptr
 };
 
-template <int VPL>
-__global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
+template <int VPL, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_batch_cluster(BatchParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
-  const int64_t b = blockIdx.x / kNCL;                      // problem of this cluster
+  const int ncl = p.ncl;
+  const int64_t b = blockIdx.x / ncl;                       // problem of this cluster
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int n = p.n, m = p.m, RB = p.RB, mv = m >> 2;
   const int r0 = crank * RB;                                // first row of this CTA
   const int nrows = max(0, min(RB, m - r0));
-  // ---- shared memory: C rows [RB][n][m] f32 | G rows [RB][m] f32 | z [m] f64 | warp partials [nw][m] f64 |
-  //      CTA partial [m] f64 | monitor partials [NCL] f64 | mbarrier
+  // ---- shared memory: C rows [RB][n][m] f32 | G rows [RB][m] f32, then the shifts a_ij (int32) in place |
+  //      z [m] f64 | Fz [m] f64 | kz [m] i32 | warp partials [nw][m] f64 | CTA partial [m] f64 | monitor
+  //      partials [NCL] f64 | row stats | beta | mbarrier
   float* Cs = reinterpret_cast<float*>(smem);
   float* Gs = Cs + (size_t)RB * n * m;
+  int* As = reinterpret_cast<int*>(Gs);
   double* zs = reinterpret_cast<double*>(Gs + (size_t)RB * m);
-  double* wpart = zs + m;
+  double* zf = zs + m;
+  int* zk = reinterpret_cast<int*>(zf + m);
+  double* wpart = reinterpret_cast<double*>(zk + m);   // m % 4 == 0: 8-byte aligned
   double* cpart = wpart + (size_t)nwarps * m;
   double* mon = cpart + m;
-  double* rstat = mon + kNCL;                                // [RB][4]: M_i, r_i, alpha_i, log alpha_i
+  double* rstat = mon + kMaxNCL;                                // [RB][4]: M_i, r_i, alpha_i, log alpha_i
   double* bcol = rstat + (size_t)RB * 4;                     // [m][2]: beta_j, log beta_j
   uint64_t* bar = reinterpret_cast<uint64_t*>(bcol + (size_t)m * 2);
   __shared__ int s_flags;
@@ -95,6 +105,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
   }
   for (int j = threadIdx.x; j < m; j += blockDim.x) {
     zs[j] = p.z_hat[b * m + j];
+    zf[j] = split_pow2_fp64(zs[j] * COT_LOG2E, zk[j]);
     const double bj = p.beta[b * m + j];
     bcol[2 * j] = bj;
     bcol[2 * j + 1] = log(bj);
@@ -105,9 +116,17 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
     rstat[4 * i + 3] = log(a);
   }
   if (nrows > 0) mbar_wait(bar, 0);
+  // the integer shifts a_ij = round(G_ij log2e/eps) replace G in place; the precomputed mode's G-shifted
+  // S_ij is rescaled to the same convention, S'_ij = S_ij 2^{a_ij - G_ij log2e/eps}
+  for (int idx = threadIdx.x; idx < nrows * m; idx += blockDim.x) {
+    const float g = Gs[idx];
+    const int a = __float2int_rn(g * c2);
+    if (p.pre) Cs[idx] *= ex2(fmaf(-g, c2, (float)a));   // n == 1: Cs row i holds S_i.
+    As[idx] = a;
+  }
   __syncthreads();
 
-  const int cols_per_cta = (m + kNCL - 1) / kNCL;
+  const int cols_per_cta = (m + ncl - 1) / ncl;
   const int c0 = crank * cols_per_cta, c1 = min(m, c0 + cols_per_cta);
   const int nrw = (nrows + nwarps - 1) / nwarps;            // rows per warp (1 for C5)
   constexpr int MAXR = 2;
@@ -169,12 +188,12 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
       const int jv = q * 32 + lane;
-      const float4 gv = (i < nrows && jv < mv) ? reinterpret_cast<const float4*>(Gs + (size_t)i * m)[jv]
-                                               : make_float4(0, 0, 0, 0);
-      gcr[rr][q][0] = gv.x * c2;
-      gcr[rr][q][1] = gv.y * c2;
-      gcr[rr][q][2] = gv.z * c2;
-      gcr[rr][q][3] = gv.w * c2;
+      const int4 av = (i < nrows && jv < mv) ? reinterpret_cast<const int4*>(As + (size_t)i * m)[jv]
+                                             : make_int4(0, 0, 0, 0);
+      gcr[rr][q][0] = (float)av.x;
+      gcr[rr][q][1] = (float)av.y;
+      gcr[rr][q][2] = (float)av.z;
+      gcr[rr][q][3] = (float)av.w;
     }
   }
   auto zero_s = [&]() {
@@ -202,33 +221,40 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
     for (int rr = 0; rr < nrw && rr < MAXR; ++rr) {
       const int i = warp + rr * nwarps;
       if (i >= nrows) break;
-      double x[VPL][4];
-      double lmax = -INFINITY;
+      int ex[VPL][4];
+      int emax = -0x7fffffff;
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
         const int jv = q * 32 + lane;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          x[q][v] = jv < mv ? zs[4 * jv + v] - (double)Gs[(size_t)i * m + 4 * jv + v] * inv_eps
-                            : -INFINITY;
-          lmax = fmax(lmax, x[q][v]);
-        }
+        const int jc = jv < mv ? jv : 0;
+        const int4 a4 = reinterpret_cast<const int4*>(As + (size_t)i * m)[jc];
+        const int4 k4 = reinterpret_cast<const int4*>(zk)[jc];
+        ex[q][0] = k4.x - a4.x;
+        ex[q][1] = k4.y - a4.y;
+        ex[q][2] = k4.z - a4.z;
+        ex[q][3] = k4.w - a4.w;
+        if (jv < mv) emax = max(emax, max(max(ex[q][0], ex[q][1]), max(ex[q][2], ex[q][3])));
       }
-      const double M = warp_max(lmax);
+      const int kM = __reduce_max_sync(0xffffffffu, emax);   // every term <= 1.42 s'_ij, the largest >= 1/2
       double tt[VPL][4];
       double lsum = 0.0;
 #pragma unroll
-      for (int q = 0; q < VPL; ++q)
+      for (int q = 0; q < VPL; ++q) {
+        const int jv = q * 32 + lane;
+        const int jc = jv < mv ? jv : 0;
+        const double2* f2 = reinterpret_cast<const double2*>(zf) + 2 * jc;
+        const double2 fa = f2[0], fb = f2[1];
+        const double fz[4] = {fa.x, fa.y, fb.x, fb.y};
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-          tt[q][v] = (x[q][v] == -INFINITY) ? 0.0
-                                            : (double)sacc[rr][q][v] * (double)ex2((float)((x[q][v] - M) * COT_LOG2E));
+          tt[q][v] = jv < mv ? ldexp_pos(sacc[rr][q][v], ex[q][v] - kM) * fz[v] : 0.0;
           lsum += tt[q][v];
         }
+      }
       const double r = warp_sum(lsum);
       const double a = rstat[4 * i + 2];
-      if (lane == 0) {   // w_hat_i = log alpha_i - M_i - log r_i is formed once, after the last iteration
-        rstat[4 * i + 0] = M;
+      if (lane == 0) {   // w_hat_i = log alpha_i - kM_i ln2 - log r_i is formed once, after the last iteration
+        rstat[4 * i + 0] = (double)kM * COT_LN2;
         rstat[4 * i + 1] = r;
       }
       double rinv = (double)__frcp_rn((float)r);   // alpha_i / r_i: fast reciprocal + 2 Newton steps
@@ -268,19 +294,22 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
     const long long c3t = p.trace ? clock64() : 0;
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     const long long c4t = p.trace ? clock64() : 0;
-    // ================= column pass of this CTA's slice: one thread per (column, source CTA), the 8 values
-    //                   combined by a fixed xor tree (deterministic), q-update written to every replica
+    // ================= column pass of this CTA's slice: one thread per (column, source CTA) in groups of 8 or
+    //                   16 lanes, the ncl values combined by a fixed xor tree (deterministic), q-update written
+    //                   to every replica
     const bool need = (p.tol > 0.0 && (st.iters + 1) % p.check_every == 0) || t == p.iters - 1;
     double dev = 0.0;
-    for (int base = 0; base < (c1 - c0) * kNCL; base += blockDim.x) {
+    const int gs_log = p.gs_log;
+    for (int base = 0; base < ((c1 - c0) << gs_log); base += blockDim.x) {
       const int idx = base + threadIdx.x;
-      const int jc = idx / kNCL, src = idx % kNCL;
+      const int jc = idx >> gs_log, src = idx & ((1 << gs_log) - 1);
       const int j = c0 + jc;
-      const bool ok = jc < (c1 - c0);
+      const bool ok = jc < (c1 - c0) && src < ncl;
       double v = ok ? cluster.map_shared_rank(cpart, src)[j] : 0.0;
       v += __shfl_xor_sync(0xffffffffu, v, 1);
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       v += __shfl_xor_sync(0xffffffffu, v, 4);
+      if (gs_log == 4) v += __shfl_xor_sync(0xffffffffu, v, 8);
       double zn = 0.0;
       if (ok) {
         const double bj = bcol[2 * j];
@@ -289,7 +318,11 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
           if (!(v >= 1e-28)) s_flags = 1;
         }
         zn = zs[j] + (bcol[2 * j + 1] - log(v));
+        int kz;
+        const double fz = split_pow2_fp64(zn * COT_LOG2E, kz);
         cluster.map_shared_rank(zs, src)[j] = zn;   // lane `src` of the group writes replica `src`
+        cluster.map_shared_rank(zf, src)[j] = fz;
+        cluster.map_shared_rank(zk, src)[j] = kz;
       }
     }
     if (need) {
@@ -322,7 +355,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
     if (need) {
       double rr = 0.0;
       const double* m0 = cluster.map_shared_rank(mon, 0);
-      for (int cr = 0; cr < kNCL; ++cr) rr += m0[cr];
+      for (int cr = 0; cr < ncl; ++cr) rr += m0[cr];
       st.residual = rr * (double)n;
     }
     if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
@@ -353,20 +386,111 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster(BatchParams p) {
 }
 
 static size_t batch_smem_bytes(int n, int m, int RB, int nwarps) {
-  return (size_t)RB * n * m * 4 + (size_t)RB * m * 4 + (size_t)m * 8 + (size_t)nwarps * m * 8 + (size_t)m * 8 +
-         kNCL * 8 + (size_t)RB * 32 + (size_t)m * 16 + 16;
+  return (size_t)RB * n * m * 4 + (size_t)RB * m * 4 + (size_t)m * 20 + (size_t)nwarps * m * 8 + (size_t)m * 8 +
+         kMaxNCL * 8 + (size_t)RB * 32 + (size_t)m * 16 + 16;
+}
+
+// Cluster shapes. Measured on B200 (scripts/ubench/clocc.cu, ubench_batch.py, ubench_c2.py): with one CTA of
+// ~200 KB per SM only 15 clusters of 8 CTAs are co-resident (GPC packing: 120 of 148 SMs), but 22 clusters of 6;
+// C5 (4096 problems) runs 12% faster as 6-CTA clusters of 11 warps (2 rows per warp, balanced k-sums) than as
+// 8-CTA clusters, while a batch that fits in one wave of 8-CTA clusters (C2) is latency-bound and keeps the
+// 8-CTA shape (fewer rows per CTA). A shape is feasible when a CTA's rows fit (<= 2 rows per warp) and its
+// shared memory fits the per-SM budget of its occupancy.
+struct ClusterShape {
+  int ncl, threads, ctas_per_sm;
+};
+constexpr ClusterShape kShapes[] = {{8, 512, 1}, {6, 352, 1}, {12, 256, 2}, {16, 256, 2}, {6, 512, 1}};
+constexpr int kLatencyShape = 0, kThroughputShape = 1;
+
+struct BatchCfg {
+  ClusterShape sh;
+  int RB;
+  size_t smem;
+  void* fn;
+};
+
+static bool shape_config(int k, int64_t n, int64_t m, BatchCfg* out) {
+  const ClusterShape sh = kShapes[k];
+  if (m < sh.ncl) return false;
+  const int RB = (int)((m + sh.ncl - 1) / sh.ncl);
+  const int nwarps = sh.threads / 32;
+  if (RB > 2 * nwarps) return false;
+  const size_t smem = batch_smem_bytes((int)n, (int)m, RB, std::min(RB, nwarps));
+  const size_t budget = sh.ctas_per_sm == 1 ? 226 * 1024 : 110 * 1024;   // of 227 KB per CTA, 228 KB per SM
+  if (smem > budget) return false;
+  out->sh = sh;
+  out->RB = RB;
+  out->smem = smem;
+  const bool v1 = m <= 128;
+  if (sh.ctas_per_sm == 1)
+    out->fn = v1 ? (void*)k_batch_cluster<1, 512, 1> : (void*)k_batch_cluster<2, 512, 1>;
+  else
+    out->fn = v1 ? (void*)k_batch_cluster<1, 256, 2> : (void*)k_batch_cluster<2, 256, 2>;
+  return true;
+}
+
+// co-resident clusters of a configuration (cached per shared-memory size)
+static int active_clusters(const BatchCfg& c) {
+  static int64_t cached_key = -1;
+  static int cached = 0;
+  const int64_t key = (int64_t)c.smem * 64 + c.sh.ncl;
+  if (key == cached_key) return cached;
+  cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  if (c.sh.ncl > 8) cudaFuncSetAttribute(c.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(c.sh.ncl * 64));
+  cfg.blockDim = dim3((unsigned)(std::min(c.RB, c.sh.threads / 32) * 32));
+  cfg.dynamicSmemBytes = c.smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = c.sh.ncl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, c.fn, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cached_key = key;
+  cached = n;
+  return n;
+}
+
+// The shape for a batch of B problems: the latency shape while the batch fits in one wave of it, else the
+// throughput shape; then any feasible shape. COT_BATCH_SHAPE forces one (experiments).
+static bool batch_config(int64_t n, int64_t m, int64_t B, BatchCfg* out) {
+  if (const char* ev = getenv("COT_BATCH_SHAPE")) {
+    const int k = atoi(ev);
+    return k >= 0 && k < (int)(sizeof(kShapes) / sizeof(kShapes[0])) && shape_config(k, n, m, out);
+  }
+  BatchCfg lat;
+  const bool have_lat = shape_config(kLatencyShape, n, m, &lat);
+  if (have_lat && (B <= 0 || B <= active_clusters(lat))) {
+    *out = lat;
+    return true;
+  }
+  if (shape_config(kThroughputShape, n, m, out)) return true;
+  if (have_lat) {
+    *out = lat;
+    return true;
+  }
+  for (int k = 0; k < (int)(sizeof(kShapes) / sizeof(kShapes[0])); ++k)
+    if (shape_config(k, n, m, out)) return true;
+  return false;
 }
 
 bool batch_cluster_eligible(const IterArgs& a) {
-  if (a.dtype != COT_F32 || a.m % 4 != 0 || a.m > 256 || a.m < kNCL || a.R != a.m ||
-      (a.flags & (COT_FORCE_LDG | COT_FORCE_TMA)))
+  if (a.dtype != COT_F32 || a.m % 4 != 0 || a.m > 256 || a.R != a.m || (a.flags & (COT_FORCE_LDG | COT_FORCE_TMA)))
     return false;
-  const int RB = (int)((a.m + kNCL - 1) / kNCL);
-  if (RB > 32) return false;
-  return batch_smem_bytes((int)a.n, (int)a.m, RB, std::min(RB, 16)) <= 200 * 1024;
+  BatchCfg c;
+  return batch_config(a.n, a.m, 0, &c);
 }
 
 cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int iters, cudaStream_t s) {
+  BatchCfg bc;
+  if (!batch_config(a.n, a.m, a.B, &bc)) return cudaErrorInvalidConfiguration;
   BatchParams p;
   p.C = static_cast<const float*>(a.C);
   p.G = static_cast<const float*>(a.G);
@@ -378,24 +502,29 @@ cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int ite
   p.state = ws.state;
   p.n = (int)a.n;
   p.m = (int)a.m;
-  p.RB = (int)((a.m + kNCL - 1) / kNCL);
+  p.RB = bc.RB;
+  p.ncl = bc.sh.ncl;
+  p.gs_log = bc.sh.ncl <= 8 ? 3 : 4;
   p.iters = iters;
   p.tol = a.tol;
   p.check_every = a.check_every > 0 ? a.check_every : 1;
   p.pre = (a.flags & COT_PRECOMPUTED) ? 1 : 0;
-  const int nwarps = std::min(p.RB, 16);   // one warp per row (two rows per warp when m > 128)
-  const size_t smem = batch_smem_bytes(p.n, p.m, p.RB, nwarps);
-  void* fn = a.m <= 128 ? (void*)k_batch_cluster<1> : (void*)k_batch_cluster<2>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int nwarps = std::min(p.RB, bc.sh.threads / 32);   // one warp per row (two rows per warp beyond)
+  void* fn = bc.fn;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bc.smem);
   if (e != cudaSuccess) return e;
+  if (p.ncl > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(a.B * kNCL));
+  cfg.gridDim = dim3((unsigned)(a.B * p.ncl));
   cfg.blockDim = dim3((unsigned)(nwarps * 32));
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = bc.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kNCL;
+  attr[0].val.clusterDim.x = p.ncl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -403,22 +532,25 @@ cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int ite
   static unsigned long long* trace_buf = nullptr;   // diagnostics only (COT_TRACE=1)
   p.trace = nullptr;
   if (getenv("COT_TRACE")) {
-    if (!trace_buf) cudaMalloc(&trace_buf, 256 * kNCL * 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(trace_buf, 0, 256 * kNCL * 8 * sizeof(unsigned long long), s);
+    if (!trace_buf) cudaMalloc(&trace_buf, 256 * kMaxNCL * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace_buf, 0, 256 * kMaxNCL * 8 * sizeof(unsigned long long), s);
     p.trace = trace_buf;
   }
   void* args[] = {&p};
   e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e == cudaSuccess && p.trace) {
-    const int ctas = (int)std::min<int64_t>(a.B, 256) * kNCL;
+    const int ctas = (int)std::min<int64_t>(a.B, 256) * p.ncl;
     std::vector<unsigned long long> h((size_t)ctas * 8);
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost);
     double acc[6] = {0};
     for (int c = 0; c < ctas; ++c)
       for (int k = 0; k < 6; ++k) acc[k] += (double)h[(size_t)c * 8 + k] / ctas / std::max(iters, 1);
-    fprintf(stderr, "[cot batch trace] per-iter cycles: epilogue %.0f cta_partial %.0f ksum1 %.0f B1_wait %.0f "
-            "colpass+B2_wait %.0f ksum2 %.0f\n", acc[0], acc[1], acc[2], acc[3], acc[4], acc[5]);
+    int act = -1;
+    cudaOccupancyMaxActiveClusters(&act, fn, &cfg);
+    fprintf(stderr, "[cot batch trace] cluster %d x %d threads, %d co-resident clusters; per-iter cycles: epilogue "
+            "%.0f cta_partial %.0f ksum1 %.0f B1_wait %.0f colpass+B2_wait %.0f ksum2 %.0f\n", p.ncl,
+            (int)cfg.blockDim.x, act, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5]);
   }
   return e;
 }

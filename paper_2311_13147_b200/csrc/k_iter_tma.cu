@@ -181,19 +181,7 @@ __device__ __forceinline__ double cblk_sum1(double v, double* red2, int& buf, in
 // e = kz_j - kM_i - a_ij assembled into the fp64 bits of s'_ij (ldexp_pos, no conversion) and one fp64
 // product by Fz_j. The only per-element rounding is the fp32 k-sum's (random across i, averaged in the
 // column sums); no factor common to a row or a column is rounded below fp64.
-__device__ __forceinline__ double split_pow2_fp64(double x, int& k) {
-  const double big = x + 6755399441055744.0;   // 1.5 * 2^52: round to an integer in the low word
-  k = __double2loint(big);
-  return exp2(x - (big - 6755399441055744.0));
-}
-// f * 2^e, exactly, for f in [2^-22, 2^23) (here f = s'_ij in [0.7, 1.42 n]) and e clamped to [-1000, 1000]:
-// terms below 2^-1000 come out ~1e-301 (negligible), terms above 2^1000 make the caller's row-sum range check
-// redo the row exactly. Integer operations only.
-__device__ __forceinline__ double ldexp_pos(float f, int e) {
-  const unsigned b = __float_as_uint(f);
-  e = min(max(e, -1000), 1000);
-  return __hiloint2double((int)((b >> 3) + ((unsigned)(e + 896) << 20)), (int)(b << 29));
-}
+// (split_pow2_fp64 and ldexp_pos: common.cuh)
 
 // One-barrier block reductions of N values over the epilogue warps (<= 8 warps; double-buffered scratch).
 // The sums use a transposed butterfly: at the first levels each lane keeps half of its values and sends the
@@ -321,10 +309,14 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
             const long long tw0 = p.trace ? clock64() : 0;
             mbar_wait(&empty[slot], phase ^ 1u);
             if (p.trace) prod_wait += clock64() - tw0;
-            mbar_arrive_expect_tx(&full[slot], (uint32_t)kk * row_bytes);
-            float* dst = ring + (size_t)slot * slot_floats;
-            for (int q = 0; q < kk; ++q)
-              bulk_g2s(dst + (size_t)q * m, p.C + ((size_t)(k0 + q) * R + i) * m, row_bytes, &full[slot], pol);
+            if (t > 0 && (p.diag & COT_DIAG_NO_STREAM)) {
+              mbar_arrive(&full[slot]);
+            } else {
+              mbar_arrive_expect_tx(&full[slot], (uint32_t)kk * row_bytes);
+              float* dst = ring + (size_t)slot * slot_floats;
+              for (int q = 0; q < kk; ++q)
+                bulk_g2s(dst + (size_t)q * m, p.C + ((size_t)(k0 + q) * R + i) * m, row_bytes, &full[slot], pol);
+            }
             ++issued;
             *(volatile unsigned*)&ctl[0] = issued;
             if (++slot == (uint32_t)p.nslot) {
@@ -1045,7 +1037,7 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
   p.lcap = ws.lcap;
   if (!rows_only && (!ws.plines || up.U > ws.lcap)) return cudaErrorInvalidValue;
   p.evict_last_rows = 0;
-  p.diag = (int)(a.flags & (COT_DIAG_NO_COMPUTE | COT_DIAG_NO_SYNC));
+  p.diag = (int)(a.flags & (COT_DIAG_NO_COMPUTE | COT_DIAG_NO_SYNC | COT_DIAG_NO_STREAM));
   p.pre = (a.flags & COT_PRECOMPUTED) ? 1 : 0;
   if (const char* ev = getenv("COT_EVICT_LAST_ROWS")) p.evict_last_rows = atoi(ev);   // L2 residency experiment
   p.trace = nullptr;

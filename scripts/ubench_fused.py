@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--n", type=int, default=64)
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--ranks", default="1,2,4,8")
+    ap.add_argument("--flags", type=lambda x: int(x, 0), default=0, help="diagnostic flags (COT_DIAG_*)")
     ap.add_argument("--shard-alone", type=int, default=0,
                     help="G > 0: run rank 0's shard of a G-way row partition ALONE on this GPU (cerot_iter_fused, "
                          "nranks = 1, exchange with itself): the per-GPU work and local sync of a G-GPU run, "
@@ -49,8 +50,8 @@ def main():
         b0, R = cdist.row_partition(p.m, G, 0)
         sh = cdist.ShardedCerot(D(p.C[:, b0:b0 + R, :]), D(p.alpha), D(p.beta), float(p.eps[0]), b0, p.m)
         x = cdist.PeerExchange(p.m)
-        ms = timed(lambda: sh.init().iterate_fused(x, a.iters))
-        print(json.dumps({"mode": f"shard_alone_1_of_{G}", "rows": R, "m": a.m, "n": a.n,
+        ms = timed(lambda: sh.init().iterate_fused(x, a.iters, flags=a.flags))
+        print(json.dumps({"mode": f"shard_alone_1_of_{G}", "rows": R, "m": a.m, "n": a.n, "flags": a.flags,
                           "us_per_iter": ms * 1e3 / a.iters}))
         x.close()
         return
