@@ -34,6 +34,17 @@ __device__ __forceinline__ double ldexp_pos(float f, int e) {
   return __hiloint2double((int)((b >> 3) + ((unsigned)(e + 896) << 20)), (int)(b << 29));
 }
 
+// 1/r for a positive normal fp64 r without the MUFU pipe (kernels whose k-sum warps keep MUFU.EX2 saturated
+// would otherwise queue the epilogue's MUFU.RCP behind them): exponent-negation estimate (relative error
+// <= 5.1%) and four Newton steps (quadratic: 2.6e-3, 6.5e-6, 4.2e-11, rounding level; checked on 4e4 samples
+// over [1e-280, 1e280]).
+__device__ __forceinline__ double rcp_nomufu(double r) {
+  double y = __hiloint2double(0x7FDE6239 - __double2hiint(r), 0);
+#pragma unroll
+  for (int s = 0; s < 4; ++s) y = fma(y, fma(-r, y, 1.0), y);
+  return y;
+}
+
 __device__ __forceinline__ bool finite_f(float x) { return fabsf(x) <= 3.402823466e38f; }
 __device__ __forceinline__ bool finite_f(double x) { return fabs(x) <= 1.7976931348623157e308; }
 

@@ -154,20 +154,26 @@ __global__ void __launch_bounds__(NT, MINB) k_batch_cluster(BatchParams p) {
         continue;
       }
       int k = k_lo;
+      // blocks of 4 k: the 16 (x VPL) MUFU.EX2 of a block are independent and issued back to back, then
+      // summed in a fixed pairwise order (in-order issue would otherwise stall on each MUFU result)
       for (; k + 4 <= k_hi; k += 4) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
+        for (int q = 0; q < VPL; ++q) {
+          const int jv = q * 32 + lane;
+          if (jv < mv) {
+            float e[4][4];
 #pragma unroll
-          for (int q = 0; q < VPL; ++q) {
-            const int jv = q * 32 + lane;
-            if (jv < mv) {
+            for (int kk = 0; kk < 4; ++kk) {
               const float4 c = crow[(size_t)(k + kk) * mv + jv];
-              sacc[rr][q][0] += ex2(fmaf(-c.x, c2, gcr[rr][q][0]));
-              sacc[rr][q][1] += ex2(fmaf(-c.y, c2, gcr[rr][q][1]));
-              sacc[rr][q][2] += ex2(fmaf(-c.z, c2, gcr[rr][q][2]));
-              sacc[rr][q][3] += ex2(fmaf(-c.w, c2, gcr[rr][q][3]));
+              e[kk][0] = ex2(fmaf(-c.x, c2, gcr[rr][q][0]));
+              e[kk][1] = ex2(fmaf(-c.y, c2, gcr[rr][q][1]));
+              e[kk][2] = ex2(fmaf(-c.z, c2, gcr[rr][q][2]));
+              e[kk][3] = ex2(fmaf(-c.w, c2, gcr[rr][q][3]));
             }
+#pragma unroll
+            for (int v = 0; v < 4; ++v) sacc[rr][q][v] += (e[0][v] + e[1][v]) + (e[2][v] + e[3][v]);
           }
+        }
       }
       for (; k < k_hi; ++k)
 #pragma unroll
@@ -257,9 +263,7 @@ __global__ void __launch_bounds__(NT, MINB) k_batch_cluster(BatchParams p) {
         rstat[4 * i + 0] = (double)kM * COT_LN2;
         rstat[4 * i + 1] = r;
       }
-      double rinv = (double)__frcp_rn((float)r);   // alpha_i / r_i: fast reciprocal + 2 Newton steps
-      rinv = rinv * fma(-r, rinv, 2.0);
-      rinv = rinv * fma(-r, rinv, 2.0);
+      const double rinv = rcp_nomufu(r);   // alpha_i / r_i
       const double rho = a * rinv;
 #pragma unroll
       for (int q = 0; q < VPL; ++q)
@@ -385,6 +389,334 @@ __global__ void __launch_bounds__(NT, MINB) k_batch_cluster(BatchParams p) {
   cluster.sync();   // no CTA leaves while others may still read its shared memory
 }
 
+// Warp-specialised variant (8-CTA clusters, m <= 128: at most 16 rows per CTA, 8 + 8 warps). The k-sums are
+// iterate-independent, so 8 K warps compute iteration t+1's s'_ij (rows w and w + 8) while the 8 E warps run
+// iteration t's chain (epilogues, CTA partial, cluster barrier, column pass, cluster barrier): the MUFU work
+// overlaps the latency-bound chain instead of following it. Hand-off through a double-buffered shared-memory
+// row buffer and named barrier 1 (K arrive, E sync); the E warps' block-level steps use named barrier 2. The
+// arithmetic (and every sum order) is that of k_batch_cluster; only the schedule differs.
+constexpr int kWsE = 8;   // epilogue warps (= k-sum warps)
+
+__global__ void __launch_bounds__(512, 1) k_batch_cluster_ws(BatchParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int ncl = p.ncl;
+  const int64_t b = blockIdx.x / ncl;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = p.n, m = p.m, RB = p.RB, mv = m >> 2;
+  const int r0 = crank * RB;
+  const int nrows = max(0, min(RB, m - r0));
+  constexpr int NE = kWsE, NET = NE * 32;
+  float* Cs = reinterpret_cast<float*>(smem);
+  float* Gs = Cs + (size_t)RB * n * m;
+  int* As = reinterpret_cast<int*>(Gs);
+  double* zs = reinterpret_cast<double*>(Gs + (size_t)RB * m);
+  double* zf = zs + m;
+  int* zk = reinterpret_cast<int*>(zf + m);
+  double* wpart = reinterpret_cast<double*>(zk + m);
+  double* cpart = wpart + (size_t)NE * m;
+  double* mon = cpart + m;
+  double* rstat = mon + kMaxNCL;
+  double* bcol = rstat + (size_t)RB * 4;
+  float* sbuf = reinterpret_cast<float*>(bcol + (size_t)m * 2);      // [2][RB][m] s'_ij of iterations t, t+1
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)2 * RB * m);
+  __shared__ int s_flags;
+  __shared__ double wdev[NE];
+
+  SolverState st = p.state[b];
+  if (!st.active) return;
+  const double inv_eps = 1.0 / p.eps[b];
+  const float c2 = (float)(COT_LOG2E * inv_eps);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    s_flags = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && nrows > 0) {
+    const uint32_t row_bytes = (uint32_t)m * 4u;
+    mbar_arrive_expect_tx(bar, (uint32_t)nrows * (uint32_t)(n + 1) * row_bytes);
+    const uint64_t pol = policy_evict_first();
+    for (int i = 0; i < nrows; ++i) {
+      for (int k = 0; k < n; ++k)
+        bulk_g2s(Cs + ((size_t)i * n + k) * m, p.C + (((size_t)b * n + k) * m + r0 + i) * m, row_bytes, bar, pol);
+      bulk_g2s(Gs + (size_t)i * m, p.G + ((size_t)b * m + r0 + i) * m, row_bytes, bar, pol);
+    }
+  }
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    zs[j] = p.z_hat[b * m + j];
+    zf[j] = split_pow2_fp64(zs[j] * COT_LOG2E, zk[j]);
+    const double bj = p.beta[b * m + j];
+    bcol[2 * j] = bj;
+    bcol[2 * j + 1] = log(bj);
+  }
+  for (int i = threadIdx.x; i < nrows; i += blockDim.x) {
+    const double a = p.alpha[b * m + r0 + i];
+    rstat[4 * i + 2] = a;
+    rstat[4 * i + 3] = log(a);
+  }
+  if (nrows > 0) mbar_wait(bar, 0);
+  for (int idx = threadIdx.x; idx < nrows * m; idx += blockDim.x) {
+    const float g = Gs[idx];
+    const int a = __float2int_rn(g * c2);
+    if (p.pre) Cs[idx] *= ex2(fmaf(-g, c2, (float)a));
+    As[idx] = a;
+  }
+  __syncthreads();
+
+  const int cols_per_cta = (m + ncl - 1) / ncl;
+  const int c0 = crank * cols_per_cta, c1 = min(m, c0 + cols_per_cta);
+  const int kmid = n / 2;
+  long long tr[6] = {0, 0, 0, 0, 0, 0};
+  int t = 0;
+  bool stop = false;
+  // the monitor of iteration t and the freeze rule, identical in every thread (read after the second barrier)
+  auto monitor = [&](bool need) {
+    st.iters += 1;
+    if (need) {
+      double rr = 0.0;
+      const double* m0 = cluster.map_shared_rank(mon, 0);
+      for (int cr = 0; cr < ncl; ++cr) rr += m0[cr];
+      st.residual = rr * (double)n;
+    }
+    if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
+      st.active = 0;
+      st.converged = 1;
+      stop = true;
+    }
+  };
+  if (warp >= NE) {
+    // ============================================================== K warps: s'_ij of the next iteration
+    const int w = warp - NE;
+    float gcr[2][4], s[2][4];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int i = w + rr * NE;
+      const int4 av = (i < nrows && lane < mv) ? reinterpret_cast<const int4*>(As + (size_t)i * m)[lane]
+                                               : make_int4(0, 0, 0, 0);
+      gcr[rr][0] = (float)av.x;
+      gcr[rr][1] = (float)av.y;
+      gcr[rr][2] = (float)av.z;
+      gcr[rr][3] = (float)av.w;
+    }
+    auto zero = [&]() {
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) s[rr][v] = 0.f;
+    };
+    auto ksum = [&](int k_lo, int k_hi) {
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int i = w + rr * NE;
+        if (i >= nrows || lane >= mv) continue;
+        const float4* crow = reinterpret_cast<const float4*>(Cs + (size_t)i * n * m);
+        if (p.pre) {
+          if (k_lo < k_hi) {
+            const float4 c = crow[lane];
+            s[rr][0] = c.x;
+            s[rr][1] = c.y;
+            s[rr][2] = c.z;
+            s[rr][3] = c.w;
+          }
+          continue;
+        }
+        int k = k_lo;
+        for (; k + 4 <= k_hi; k += 4) {
+          float e[4][4];
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const float4 c = crow[(size_t)(k + kk) * mv + lane];
+            e[kk][0] = ex2(fmaf(-c.x, c2, gcr[rr][0]));
+            e[kk][1] = ex2(fmaf(-c.y, c2, gcr[rr][1]));
+            e[kk][2] = ex2(fmaf(-c.z, c2, gcr[rr][2]));
+            e[kk][3] = ex2(fmaf(-c.w, c2, gcr[rr][3]));
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) s[rr][v] += (e[0][v] + e[1][v]) + (e[2][v] + e[3][v]);
+        }
+        for (; k < k_hi; ++k) {
+          const float4 c = crow[(size_t)k * mv + lane];
+          s[rr][0] += ex2(fmaf(-c.x, c2, gcr[rr][0]));
+          s[rr][1] += ex2(fmaf(-c.y, c2, gcr[rr][1]));
+          s[rr][2] += ex2(fmaf(-c.z, c2, gcr[rr][2]));
+          s[rr][3] += ex2(fmaf(-c.w, c2, gcr[rr][3]));
+        }
+      }
+    };
+    auto publish = [&](int buf) {   // s' rows into sbuf[buf], then named barrier 1 (arrive: no wait)
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int i = w + rr * NE;
+        if (i < nrows && lane < mv)
+          reinterpret_cast<float4*>(sbuf + ((size_t)buf * RB + i) * m)[lane] = make_float4(s[rr][0], s[rr][1], s[rr][2], s[rr][3]);
+      }
+      __threadfence_block();
+      asm volatile("bar.arrive 1, %0;" ::"r"(512) : "memory");
+    };
+    zero();
+    ksum(0, n);
+    publish(0);
+    for (; t < p.iters && !stop; ++t) {
+      const bool more = t + 1 < p.iters;
+      const bool need = (p.tol > 0.0 && (st.iters + 1) % p.check_every == 0) || t == p.iters - 1;
+      const long long k0 = p.trace ? clock64() : 0;
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      zero();
+      if (more) ksum(0, kmid);
+      const long long k1 = p.trace ? clock64() : 0;
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      const long long k2 = p.trace ? clock64() : 0;
+      if (more) ksum(kmid, n);
+      const long long k3 = p.trace ? clock64() : 0;
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      monitor(need);
+      if (more && !stop) publish((t + 1) & 1);
+      if (p.trace) {
+        tr[2] += k1 - k0;
+        tr[5] += k3 - k2;
+      }
+    }
+  } else {
+    // ============================================================== E warps: the iteration chain
+    const int et = threadIdx.x;
+    for (; t < p.iters && !stop; ++t) {
+      const bool need = (p.tol > 0.0 && (st.iters + 1) % p.check_every == 0) || t == p.iters - 1;
+      asm volatile("bar.sync 1, %0;" ::"r"(512) : "memory");   // s'(t) is in sbuf[t & 1]
+      const long long c0t = p.trace ? clock64() : 0;
+      const float* sb = sbuf + (size_t)(t & 1) * RB * m;
+      double P[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int i = warp + rr * NE;
+        if (i >= nrows) break;
+        const int jc = lane < mv ? lane : 0;
+        const int4 a4 = reinterpret_cast<const int4*>(As + (size_t)i * m)[jc];
+        const int4 k4 = reinterpret_cast<const int4*>(zk)[jc];
+        const int ex[4] = {k4.x - a4.x, k4.y - a4.y, k4.z - a4.z, k4.w - a4.w};
+        const int emax = lane < mv ? max(max(ex[0], ex[1]), max(ex[2], ex[3])) : -0x7fffffff;
+        const int kM = __reduce_max_sync(0xffffffffu, emax);
+        const float4 s4 = reinterpret_cast<const float4*>(sb + (size_t)i * m)[jc];
+        const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+        const double2* f2 = reinterpret_cast<const double2*>(zf) + 2 * jc;
+        const double2 fa = f2[0], fb = f2[1];
+        const double fz[4] = {fa.x, fa.y, fb.x, fb.y};
+        double tt[4], lsum = 0.0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          tt[v] = lane < mv ? ldexp_pos(sv[v], ex[v] - kM) * fz[v] : 0.0;
+          lsum += tt[v];
+        }
+        const double r = warp_sum(lsum);
+        const double a = rstat[4 * i + 2];
+        if (lane == 0) {
+          rstat[4 * i + 0] = (double)kM * COT_LN2;
+          rstat[4 * i + 1] = r;
+        }
+        const double rinv = rcp_nomufu(r);
+        const double rho = a * rinv;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) P[v] = fma(rho, tt[v], P[v]);
+      }
+      if (lane < mv)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) wpart[(size_t)warp * m + 4 * lane + v] = P[v];
+      const long long c1t = p.trace ? clock64() : 0;
+      asm volatile("bar.sync 2, %0;" ::"r"(NET) : "memory");
+      for (int j = et; j < m; j += NET) {   // CTA partial: the 8 warps in a fixed pairwise tree
+        double v8[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v8[w] = wpart[(size_t)w * m + j];
+#pragma unroll
+        for (int h = 4; h >= 1; h >>= 1)
+#pragma unroll
+          for (int w = 0; w < h; ++w) v8[w] += v8[w + h];
+        cpart[j] = v8[0];
+      }
+      const long long c2t = p.trace ? clock64() : 0;
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      const long long c4t = p.trace ? clock64() : 0;
+      double dev = 0.0;
+      for (int base = 0; base < ((c1 - c0) << 3); base += NET) {
+        const int idx = base + et;
+        const int jc = idx >> 3, src = idx & 7;
+        const int j = c0 + jc;
+        const bool ok = jc < (c1 - c0) && src < ncl;
+        double v = ok ? cluster.map_shared_rank(cpart, src)[j] : 0.0;
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        if (ok) {
+          const double bj = bcol[2 * j];
+          if (src == 0) {
+            dev += fabs(v - bj);
+            if (!(v >= 1e-28)) s_flags = 1;
+          }
+          const double zn = zs[j] + (bcol[2 * j + 1] - log(v));
+          int kz;
+          const double fzn = split_pow2_fp64(zn * COT_LOG2E, kz);
+          cluster.map_shared_rank(zs, src)[j] = zn;
+          cluster.map_shared_rank(zf, src)[j] = fzn;
+          cluster.map_shared_rank(zk, src)[j] = kz;
+        }
+      }
+      if (need) {
+        dev = warp_sum(dev);
+        if (lane == 0) wdev[warp] = dev;
+        asm volatile("bar.sync 2, %0;" ::"r"(NET) : "memory");
+        if (et == 0) {
+          double d = 0.0;
+          for (int w = 0; w < NE; ++w) d += wdev[w];
+          cluster.map_shared_rank(mon, 0)[crank] = d;
+        }
+      }
+      const long long c5t = p.trace ? clock64() : 0;
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      monitor(need);
+      if (p.trace) {
+        const long long c7t = clock64();
+        tr[0] += c1t - c0t;
+        tr[1] += c2t - c1t;
+        tr[3] += c4t - c2t;
+        tr[4] += c7t - c5t + (c5t - c4t);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nrows; i += blockDim.x)
+    if (t > 0) p.w_hat[b * m + r0 + i] = rstat[4 * i + 3] - rstat[4 * i + 0] - log(rstat[4 * i + 1]);
+  if (crank == 0)
+    for (int j = threadIdx.x; j < m; j += blockDim.x) p.z_hat[b * m + j] = zs[j];
+  __syncthreads();
+  if (s_flags) atomicOr(&p.state[b].flags, (int)STATE_UNDERFLOW);
+  if (crank == 0 && threadIdx.x == 0) {
+    SolverState out = p.state[b];
+    out.iters = st.iters;
+    out.residual = st.residual;
+    out.active = st.active;
+    out.converged = st.converged;
+    p.state[b] = out;
+  }
+  if (p.trace && b < 256) {
+    unsigned long long* tp = p.trace + (size_t)blockIdx.x * 8;
+    if (threadIdx.x == 0) {
+      tp[0] = tr[0];
+      tp[1] = tr[1];
+      tp[3] = tr[3];
+      tp[4] = tr[4];
+    }
+    if (threadIdx.x == NET) {
+      tp[2] = tr[2];
+      tp[5] = tr[5];
+    }
+  }
+  cluster.sync();
+}
+
 static size_t batch_smem_bytes(int n, int m, int RB, int nwarps) {
   return (size_t)RB * n * m * 4 + (size_t)RB * m * 4 + (size_t)m * 20 + (size_t)nwarps * m * 8 + (size_t)m * 8 +
          kMaxNCL * 8 + (size_t)RB * 32 + (size_t)m * 16 + 16;
@@ -405,6 +737,7 @@ constexpr int kLatencyShape = 0, kThroughputShape = 1;
 struct BatchCfg {
   ClusterShape sh;
   int RB;
+  bool ws;   // warp-specialised kernel (512 threads: 8 epilogue + 8 k-sum warps)
   size_t smem;
   void* fn;
 };
@@ -421,6 +754,15 @@ static bool shape_config(int k, int64_t n, int64_t m, BatchCfg* out) {
   out->sh = sh;
   out->RB = RB;
   out->smem = smem;
+  // the 8-CTA shape with <= 16 rows per CTA (m <= 128) runs warp-specialised (COT_BATCH_WS=0: interleaved)
+  const char* wsv = getenv("COT_BATCH_WS");
+  out->ws = sh.ncl == 8 && sh.ctas_per_sm == 1 && m <= 128 && !(wsv && atoi(wsv) == 0);
+  if (out->ws) {
+    out->smem = batch_smem_bytes((int)n, (int)m, RB, kWsE) + (size_t)2 * RB * m * 4;
+    if (out->smem > budget) return false;
+    out->fn = (void*)k_batch_cluster_ws;
+    return true;
+  }
   const bool v1 = m <= 128;
   if (sh.ctas_per_sm == 1)
     out->fn = v1 ? (void*)k_batch_cluster<1, 512, 1> : (void*)k_batch_cluster<2, 512, 1>;
@@ -433,13 +775,13 @@ static bool shape_config(int k, int64_t n, int64_t m, BatchCfg* out) {
 static int active_clusters(const BatchCfg& c) {
   static int64_t cached_key = -1;
   static int cached = 0;
-  const int64_t key = (int64_t)c.smem * 64 + c.sh.ncl;
+  const int64_t key = ((int64_t)c.smem * 64 + c.sh.ncl) * 2 + (c.ws ? 1 : 0);
   if (key == cached_key) return cached;
   cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (c.sh.ncl > 8) cudaFuncSetAttribute(c.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(c.sh.ncl * 64));
-  cfg.blockDim = dim3((unsigned)(std::min(c.RB, c.sh.threads / 32) * 32));
+  cfg.blockDim = dim3((unsigned)(c.ws ? 512 : std::min(c.RB, c.sh.threads / 32) * 32));
   cfg.dynamicSmemBytes = c.smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -519,7 +861,7 @@ cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int ite
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.B * p.ncl));
-  cfg.blockDim = dim3((unsigned)(nwarps * 32));
+  cfg.blockDim = dim3((unsigned)(bc.ws ? 512 : nwarps * 32));
   cfg.dynamicSmemBytes = bc.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -712,9 +712,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
           if (b >= nb) break;
           const int r = r0 + b;
           const double rsum = sm[b];
-          double rinv = (double)__frcp_rn((float)rsum);   // alpha_i / r_i: fast reciprocal + 2 Newton steps
-          rinv = rinv * fma(-rsum, rinv, 2.0);
-          rinv = rinv * fma(-rsum, rinv, 2.0);
+          const double rinv = rcp_nomufu(rsum);   // alpha_i / r_i
           const double rho = rowstat[r * RS + 4] * rinv;
           if (et == 0) {   // the shift used for r_i, r_i, and the next iteration's shift: kM + floor(log2 r_i)
             const int kM = __double2int_rn(Mref[b] * COT_LOG2E);
