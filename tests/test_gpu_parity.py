@@ -378,3 +378,25 @@ def test_tma_kernel_shapes(n, m, R_seed):
     _compare(p, rep.cpu().numpy()[0], T.cpu().numpy(), w, z)
     it, _, _ = prob.state()
     assert it[0] == 25
+
+
+@pytest.mark.parametrize("n,m,B", [(1, 8, 1), (3, 12, 1), (5, 36, 2), (17, 128, 1), (16, 128, 20), (4, 132, 1),
+                                   (7, 132, 20), (2, 256, 3)])
+def test_cluster_kernel_shapes(n, m, B):
+    """The cluster-resident kernel on ragged shapes, in each of its schedules: B within one wave of 8-CTA clusters
+    (warp-specialised for m <= 128, interleaved beyond), B = 20 (the 6-CTA throughput shape where it fits);
+    n = 1 and n not a multiple of 4, rows per CTA not a multiple of the warp count. 30 iterations in two
+    launches, every problem against the oracle."""
+    p = synthetic.random_cyclic(seed=7 * n + m, n=n, m=m, dtype=np.float32, eps=0.05, B=B)
+    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps)).init()
+    assert cot.lib().cot_iter_path(B, n, m, 0, 0) == 2   # the cluster-resident kernel
+    prob.iterate(18)
+    prob.iterate(12)
+    T, rep = prob.plan(T_blocks=True)
+    T, rep = T.cpu().numpy(), rep.cpu().numpy()
+    it, _, _ = prob.state()
+    assert (np.asarray(it) == 30).all()
+    for b in range(B):
+        pb = synthetic.Problem("b", p.C[b], p.alpha[b], p.beta[b], p.eps[b:b + 1], iters=0, tol=0.0, meta={})
+        w, z, _, _ = oracle.cyclic_sinkhorn(pb.alpha, pb.beta, pb.C, 0.05, 30, form="kernel")
+        _compare(pb, rep[b], T[b], w, z)
