@@ -389,15 +389,16 @@ __global__ void __launch_bounds__(NT, MINB) k_batch_cluster(BatchParams p) {
   cluster.sync();   // no CTA leaves while others may still read its shared memory
 }
 
-// Warp-specialised variant (8-CTA clusters, m <= 128: at most 16 rows per CTA, 8 + 8 warps). The k-sums are
-// iterate-independent, so 8 K warps compute iteration t+1's s'_ij (rows w and w + 8) while the 8 E warps run
-// iteration t's chain (epilogues, CTA partial, cluster barrier, column pass, cluster barrier): the MUFU work
-// overlaps the latency-bound chain instead of following it. Hand-off through a double-buffered shared-memory
-// row buffer and named barrier 1 (K arrive, E sync); the E warps' block-level steps use named barrier 2. The
-// arithmetic (and every sum order) is that of k_batch_cluster; only the schedule differs.
-constexpr int kWsE = 8;   // epilogue warps (= k-sum warps)
-
-__global__ void __launch_bounds__(512, 1) k_batch_cluster_ws(BatchParams p) {
+// Warp-specialised variant (m <= 128: one float4 of columns per lane; up to 2 rows per warp). The k-sums are
+// iterate-independent, so NE "K" warps compute iteration t+1's s'_ij (rows w and w + NE) while NE "E" warps
+// run iteration t's chain (epilogues, CTA partial, cluster barrier, column pass, cluster barrier): the MUFU work
+// overlaps the latency-bound chain instead of following it. Hand-off through a shared-memory row buffer,
+// written by the K warps only after the first cluster barrier of iteration t (every E warp has finished its
+// epilogue of iteration t by then, so one buffer suffices), and named barrier 1 (K arrive, E sync); the E
+// warps' block-level steps use named barrier 2. NE = ceil(rows / 2) (8 for the 8-CTA shape, 11 for the
+// 6-CTA shape of C5). The arithmetic and every sum order are those of k_batch_cluster.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_batch_cluster_ws(BatchParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank();
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster_ws(BatchParams p) {
   const int n = p.n, m = p.m, RB = p.RB, mv = m >> 2;
   const int r0 = crank * RB;
   const int nrows = max(0, min(RB, m - r0));
-  constexpr int NE = kWsE, NET = NE * 32;
+  const int NE = (int)(blockDim.x >> 6), NET = NE * 32;   // E warps = K warps
   float* Cs = reinterpret_cast<float*>(smem);
   float* Gs = Cs + (size_t)RB * n * m;
   int* As = reinterpret_cast<int*>(Gs);
@@ -419,10 +420,10 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster_ws(BatchParams p) {
   double* mon = cpart + m;
   double* rstat = mon + kMaxNCL;
   double* bcol = rstat + (size_t)RB * 4;
-  float* sbuf = reinterpret_cast<float*>(bcol + (size_t)m * 2);      // [2][RB][m] s'_ij of iterations t, t+1
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)2 * RB * m);
+  float* sbuf = reinterpret_cast<float*>(bcol + (size_t)m * 2);      // [RB][m] s'_ij of the next epilogue
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)RB * m);
   __shared__ int s_flags;
-  __shared__ double wdev[NE];
+  __shared__ double wdev[16];
 
   SolverState st = p.state[b];
   if (!st.active) return;
@@ -545,19 +546,19 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster_ws(BatchParams p) {
         }
       }
     };
-    auto publish = [&](int buf) {   // s' rows into sbuf[buf], then named barrier 1 (arrive: no wait)
+    auto publish = [&]() {   // s' rows into sbuf, then named barrier 1 (arrive: no wait)
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
         const int i = w + rr * NE;
         if (i < nrows && lane < mv)
-          reinterpret_cast<float4*>(sbuf + ((size_t)buf * RB + i) * m)[lane] = make_float4(s[rr][0], s[rr][1], s[rr][2], s[rr][3]);
+          reinterpret_cast<float4*>(sbuf + (size_t)i * m)[lane] = make_float4(s[rr][0], s[rr][1], s[rr][2], s[rr][3]);
       }
       __threadfence_block();
-      asm volatile("bar.arrive 1, %0;" ::"r"(512) : "memory");
+      asm volatile("bar.arrive 1, %0;" ::"r"(blockDim.x) : "memory");
     };
     zero();
     ksum(0, n);
-    publish(0);
+    publish();
     for (; t < p.iters && !stop; ++t) {
       const bool more = t + 1 < p.iters;
       const bool need = (p.tol > 0.0 && (st.iters + 1) % p.check_every == 0) || t == p.iters - 1;
@@ -573,7 +574,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster_ws(BatchParams p) {
       const long long k3 = p.trace ? clock64() : 0;
       asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
       monitor(need);
-      if (more && !stop) publish((t + 1) & 1);
+      if (more && !stop) publish();   // after B1 of iteration t: the E warps are done with sbuf
       if (p.trace) {
         tr[2] += k1 - k0;
         tr[5] += k3 - k2;
@@ -584,56 +585,74 @@ __global__ void __launch_bounds__(512, 1) k_batch_cluster_ws(BatchParams p) {
     const int et = threadIdx.x;
     for (; t < p.iters && !stop; ++t) {
       const bool need = (p.tol > 0.0 && (st.iters + 1) % p.check_every == 0) || t == p.iters - 1;
-      asm volatile("bar.sync 1, %0;" ::"r"(512) : "memory");   // s'(t) is in sbuf[t & 1]
+      asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");   // s'(t) is in sbuf
       const long long c0t = p.trace ? clock64() : 0;
-      const float* sb = sbuf + (size_t)(t & 1) * RB * m;
+      const float* sb = sbuf;
+      // the warp's two rows side by side (independent shuffle / reduction chains overlap)
       double P[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const int i = warp + rr * NE;
-        if (i >= nrows) break;
+      {
         const int jc = lane < mv ? lane : 0;
-        const int4 a4 = reinterpret_cast<const int4*>(As + (size_t)i * m)[jc];
         const int4 k4 = reinterpret_cast<const int4*>(zk)[jc];
-        const int ex[4] = {k4.x - a4.x, k4.y - a4.y, k4.z - a4.z, k4.w - a4.w};
-        const int emax = lane < mv ? max(max(ex[0], ex[1]), max(ex[2], ex[3])) : -0x7fffffff;
-        const int kM = __reduce_max_sync(0xffffffffu, emax);
-        const float4 s4 = reinterpret_cast<const float4*>(sb + (size_t)i * m)[jc];
-        const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
         const double2* f2 = reinterpret_cast<const double2*>(zf) + 2 * jc;
         const double2 fa = f2[0], fb = f2[1];
         const double fz[4] = {fa.x, fa.y, fb.x, fb.y};
-        double tt[4], lsum = 0.0;
+        bool valid[2];
+        int ex[2][4], kM[2];
+        double tt[2][4], lsum[2];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          tt[v] = lane < mv ? ldexp_pos(sv[v], ex[v] - kM) * fz[v] : 0.0;
-          lsum += tt[v];
-        }
-        const double r = warp_sum(lsum);
-        const double a = rstat[4 * i + 2];
-        if (lane == 0) {
-          rstat[4 * i + 0] = (double)kM * COT_LN2;
-          rstat[4 * i + 1] = r;
-        }
-        const double rinv = rcp_nomufu(r);
-        const double rho = a * rinv;
+        for (int rr = 0; rr < 2; ++rr) {
+          const int i = warp + rr * NE;
+          valid[rr] = i < nrows;
+          const int ic = valid[rr] ? i : 0;
+          const int4 a4 = reinterpret_cast<const int4*>(As + (size_t)ic * m)[jc];
+          ex[rr][0] = k4.x - a4.x;
+          ex[rr][1] = k4.y - a4.y;
+          ex[rr][2] = k4.z - a4.z;
+          ex[rr][3] = k4.w - a4.w;
+          const int emax = lane < mv ? max(max(ex[rr][0], ex[rr][1]), max(ex[rr][2], ex[rr][3])) : -0x7fffffff;
+          kM[rr] = __reduce_max_sync(0xffffffffu, emax);
+          const float4 s4 = reinterpret_cast<const float4*>(sb + (size_t)ic * m)[jc];
+          const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+          lsum[rr] = 0.0;
 #pragma unroll
-        for (int v = 0; v < 4; ++v) P[v] = fma(rho, tt[v], P[v]);
+          for (int v = 0; v < 4; ++v) {
+            tt[rr][v] = lane < mv && valid[rr] ? ldexp_pos(sv[v], ex[rr][v] - kM[rr]) * fz[v] : 0.0;
+            lsum[rr] += tt[rr][v];
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lsum[0] += __shfl_xor_sync(0xffffffffu, lsum[0], o);
+          lsum[1] += __shfl_xor_sync(0xffffffffu, lsum[1], o);
+        }
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          if (!valid[rr]) continue;
+          const int i = warp + rr * NE;
+          const double r = lsum[rr];
+          if (lane == 0) {
+            rstat[4 * i + 0] = (double)kM[rr] * COT_LN2;
+            rstat[4 * i + 1] = r;
+          }
+          const double rho = rstat[4 * i + 2] * rcp_nomufu(r);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) P[v] = fma(rho, tt[rr][v], P[v]);
+        }
       }
       if (lane < mv)
 #pragma unroll
         for (int v = 0; v < 4; ++v) wpart[(size_t)warp * m + 4 * lane + v] = P[v];
       const long long c1t = p.trace ? clock64() : 0;
       asm volatile("bar.sync 2, %0;" ::"r"(NET) : "memory");
-      for (int j = et; j < m; j += NET) {   // CTA partial: the 8 warps in a fixed pairwise tree
-        double v8[8];
+      for (int j = et; j < m; j += NET) {   // CTA partial: the E warps in a fixed pairwise tree
+        double v16[16];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) v8[w] = wpart[(size_t)w * m + j];
+        for (int w = 0; w < 16; ++w) v16[w] = w < NE ? wpart[(size_t)w * m + j] : 0.0;
 #pragma unroll
-        for (int h = 4; h >= 1; h >>= 1)
+        for (int h = 8; h >= 1; h >>= 1)
 #pragma unroll
-          for (int w = 0; w < h; ++w) v8[w] += v8[w + h];
-        cpart[j] = v8[0];
+          for (int w = 0; w < h; ++w) v16[w] += v16[w + h];
+        cpart[j] = v16[0];
       }
       const long long c2t = p.trace ? clock64() : 0;
       asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
@@ -736,8 +755,8 @@ constexpr int kLatencyShape = 0, kThroughputShape = 1;
 
 struct BatchCfg {
   ClusterShape sh;
-  int RB;
-  bool ws;   // warp-specialised kernel (512 threads: 8 epilogue + 8 k-sum warps)
+  int RB, threads;
+  bool ws;   // warp-specialised kernel (threads = 2 x 32 x ceil(rows / 2))
   size_t smem;
   void* fn;
 };
@@ -754,15 +773,19 @@ static bool shape_config(int k, int64_t n, int64_t m, BatchCfg* out) {
   out->sh = sh;
   out->RB = RB;
   out->smem = smem;
-  // the 8-CTA shape with <= 16 rows per CTA (m <= 128) runs warp-specialised (COT_BATCH_WS=0: interleaved)
+  // 1 CTA per SM and m <= 128 (<= 22 rows per CTA): warp-specialised, NE = ceil(rows / 2) epilogue warps and as
+  // many k-sum warps (COT_BATCH_WS=0: the interleaved kernel)
   const char* wsv = getenv("COT_BATCH_WS");
-  out->ws = sh.ncl == 8 && sh.ctas_per_sm == 1 && m <= 128 && !(wsv && atoi(wsv) == 0);
+  out->ws = sh.ctas_per_sm == 1 && m <= 128 && RB <= 22 && !(wsv && atoi(wsv) == 0);
   if (out->ws) {
-    out->smem = batch_smem_bytes((int)n, (int)m, RB, kWsE) + (size_t)2 * RB * m * 4;
+    const int ne = (RB + 1) / 2;
+    out->threads = 64 * ne;
+    out->smem = batch_smem_bytes((int)n, (int)m, RB, ne) + (size_t)RB * m * 4;
     if (out->smem > budget) return false;
-    out->fn = (void*)k_batch_cluster_ws;
+    out->fn = ne <= 8 ? (void*)k_batch_cluster_ws<512> : (void*)k_batch_cluster_ws<704>;
     return true;
   }
+  out->threads = std::min(RB, nwarps) * 32;
   const bool v1 = m <= 128;
   if (sh.ctas_per_sm == 1)
     out->fn = v1 ? (void*)k_batch_cluster<1, 512, 1> : (void*)k_batch_cluster<2, 512, 1>;
@@ -781,7 +804,7 @@ static int active_clusters(const BatchCfg& c) {
   if (c.sh.ncl > 8) cudaFuncSetAttribute(c.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(c.sh.ncl * 64));
-  cfg.blockDim = dim3((unsigned)(c.ws ? 512 : std::min(c.RB, c.sh.threads / 32) * 32));
+  cfg.blockDim = dim3((unsigned)c.threads);
   cfg.dynamicSmemBytes = c.smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -851,7 +874,6 @@ cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int ite
   p.tol = a.tol;
   p.check_every = a.check_every > 0 ? a.check_every : 1;
   p.pre = (a.flags & COT_PRECOMPUTED) ? 1 : 0;
-  const int nwarps = std::min(p.RB, bc.sh.threads / 32);   // one warp per row (two rows per warp beyond)
   void* fn = bc.fn;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bc.smem);
   if (e != cudaSuccess) return e;
@@ -861,7 +883,7 @@ cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int ite
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.B * p.ncl));
-  cfg.blockDim = dim3((unsigned)(bc.ws ? 512 : nwarps * 32));
+  cfg.blockDim = dim3((unsigned)bc.threads);
   cfg.dynamicSmemBytes = bc.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
