@@ -49,6 +49,7 @@ struct BatchParams {
   long long check_every;
   int pre;               // precomputed mode (NEXT-1): C is S [B][1][m][m], s_ij = S_ij
   int ncl;               // CTAs per cluster (one problem per cluster)
+  int ne;                // warp-specialised kernel: epilogue warps (the rest of the block: k-sum warps)
   int gs_log;            // log2 of the column-pass group (a power of two >= ncl: 8 or 16 lanes)
   unsigned long long* trace;   // diagnostics (COT_TRACE=1): [grid][8] cycle counters, or nullptr
 };
@@ -408,7 +409,8 @@ __global__ void __launch_bounds__(NT, 1) k_batch_cluster_ws(BatchParams p) {
   const int n = p.n, m = p.m, RB = p.RB, mv = m >> 2;
   const int r0 = crank * RB;
   const int nrows = max(0, min(RB, m - r0));
-  const int NE = (int)(blockDim.x >> 6), NET = NE * 32;   // E warps = K warps
+  const int NE = p.ne, NET = NE * 32;                       // E warps; the other warps of the block: K warps
+  const int NK = (int)(blockDim.x >> 5) - NE;
   float* Cs = reinterpret_cast<float*>(smem);
   float* Gs = Cs + (size_t)RB * n * m;
   int* As = reinterpret_cast<int*>(Gs);
@@ -489,11 +491,11 @@ __global__ void __launch_bounds__(NT, 1) k_batch_cluster_ws(BatchParams p) {
   };
   if (warp >= NE) {
     // ============================================================== K warps: s'_ij of the next iteration
-    const int w = warp - NE;
-    float gcr[2][4], s[2][4];
+    const int w = warp - NE;   // rows w, w + NK, w + 2 NK, w + 3 NK
+    float gcr[4][4], s[4][4];
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      const int i = w + rr * NE;
+    for (int rr = 0; rr < 4; ++rr) {
+      const int i = w + rr * NK;
       const int4 av = (i < nrows && lane < mv) ? reinterpret_cast<const int4*>(As + (size_t)i * m)[lane]
                                                : make_int4(0, 0, 0, 0);
       gcr[rr][0] = (float)av.x;
@@ -503,14 +505,14 @@ __global__ void __launch_bounds__(NT, 1) k_batch_cluster_ws(BatchParams p) {
     }
     auto zero = [&]() {
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
+      for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
         for (int v = 0; v < 4; ++v) s[rr][v] = 0.f;
     };
     auto ksum = [&](int k_lo, int k_hi) {
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const int i = w + rr * NE;
+      for (int rr = 0; rr < 4; ++rr) {
+        const int i = w + rr * NK;
         if (i >= nrows || lane >= mv) continue;
         const float4* crow = reinterpret_cast<const float4*>(Cs + (size_t)i * n * m);
         if (p.pre) {
@@ -548,8 +550,8 @@ __global__ void __launch_bounds__(NT, 1) k_batch_cluster_ws(BatchParams p) {
     };
     auto publish = [&]() {   // s' rows into sbuf, then named barrier 1 (arrive: no wait)
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const int i = w + rr * NE;
+      for (int rr = 0; rr < 4; ++rr) {
+        const int i = w + rr * NK;
         if (i < nrows && lane < mv)
           reinterpret_cast<float4*>(sbuf + (size_t)i * m)[lane] = make_float4(s[rr][0], s[rr][1], s[rr][2], s[rr][3]);
       }
@@ -755,7 +757,7 @@ constexpr int kLatencyShape = 0, kThroughputShape = 1;
 
 struct BatchCfg {
   ClusterShape sh;
-  int RB, threads;
+  int RB, threads, ne;
   bool ws;   // warp-specialised kernel (threads = 2 x 32 x ceil(rows / 2))
   size_t smem;
   void* fn;
@@ -779,10 +781,15 @@ static bool shape_config(int k, int64_t n, int64_t m, BatchCfg* out) {
   out->ws = sh.ctas_per_sm == 1 && m <= 128 && RB <= 22 && !(wsv && atoi(wsv) == 0);
   if (out->ws) {
     const int ne = (RB + 1) / 2;
-    out->threads = 64 * ne;
+    int kr = 2;   // rows per k-sum warp (COT_BATCH_KR: 1..4; 2 measured best on C5 and C2)
+    if (const char* ev = getenv("COT_BATCH_KR")) kr = std::max(1, std::min(4, atoi(ev)));
+    const int nk = (RB + kr - 1) / kr;
+    out->ne = ne;
+    out->threads = 32 * (ne + nk);
     out->smem = batch_smem_bytes((int)n, (int)m, RB, ne) + (size_t)RB * m * 4;
     if (out->smem > budget) return false;
-    out->fn = ne <= 8 ? (void*)k_batch_cluster_ws<512> : (void*)k_batch_cluster_ws<704>;
+    out->fn = out->threads <= 512 ? (void*)k_batch_cluster_ws<512>
+                                  : out->threads <= 576 ? (void*)k_batch_cluster_ws<576> : (void*)k_batch_cluster_ws<704>;
     return true;
   }
   out->threads = std::min(RB, nwarps) * 32;
@@ -870,6 +877,7 @@ cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int ite
   p.RB = bc.RB;
   p.ncl = bc.sh.ncl;
   p.gs_log = bc.sh.ncl <= 8 ? 3 : 4;
+  p.ne = bc.ws ? bc.ne : 0;
   p.iters = iters;
   p.tol = a.tol;
   p.check_every = a.check_every > 0 ? a.check_every : 1;
