@@ -45,6 +45,25 @@ __device__ __forceinline__ double rcp_nomufu(double r) {
   return y;
 }
 
+// log(x) for a positive normal fp64 x without the MUFU pipe (CUDA's log issues one MUFU.RCP64H, which queues
+// behind the k-sum warps' MUFU.EX2 on the per-iteration critical path): x = m 2^e with m in [1/sqrt2, sqrt2),
+// log m = 2 atanh(s), s = (m - 1)/(m + 1), |s| <= 0.1716, odd series to s^25 (truncation < 1e-20); error
+// <= 5e-16 (relative, or absolute near x = 1) on 4e4 samples over [1e-30, 1e3].
+__device__ __forceinline__ double log_nomufu(double x) {
+  const int hi = __double2hiint(x);
+  int e = (hi >> 20) - 1023;
+  double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, __double2loint(x));
+  if (m > 1.4142135623730951) {
+    m *= 0.5;
+    e += 1;
+  }
+  const double s = (m - 1.0) * rcp_nomufu(m + 1.0), s2 = s * s;
+  double p = 1.0 / 25;
+#pragma unroll
+  for (int k = 23; k >= 1; k -= 2) p = fma(p, s2, 1.0 / k);
+  return fma((double)e, COT_LN2, 2.0 * s * p);
+}
+
 __device__ __forceinline__ bool finite_f(float x) { return fabsf(x) <= 3.402823466e38f; }
 __device__ __forceinline__ bool finite_f(double x) { return fabs(x) <= 1.7976931348623157e308; }
 

@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(NT, MINB) k_batch_cluster(BatchParams p) {
           dev += fabs(v - bj);
           if (!(v >= 1e-28)) s_flags = 1;
         }
-        zn = zs[j] + (bcol[2 * j + 1] - log(v));
+        zn = zs[j] + (bcol[2 * j + 1] - log_nomufu(v));
         int kz;
         const double fz = split_pow2_fp64(zn * COT_LOG2E, kz);
         cluster.map_shared_rank(zs, src)[j] = zn;   // lane `src` of the group writes replica `src`
@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_cluster_ws(BatchParams p) {
             dev += fabs(v - bj);
             if (!(v >= 1e-28)) s_flags = 1;
           }
-          const double zn = zs[j] + (bcol[2 * j + 1] - log(v));
+          const double zn = zs[j] + (bcol[2 * j + 1] - log_nomufu(v));
           int kz;
           const double fzn = split_pow2_fp64(zn * COT_LOG2E, kz);
           cluster.map_shared_rank(zs, src)[j] = zn;

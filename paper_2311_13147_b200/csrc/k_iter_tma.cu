@@ -856,7 +856,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
           dev += fabs(cj - bj);
           if (!(cj >= 1e-28)) atomicOr(&p.state[0].flags, (int)STATE_UNDERFLOW);
           const double zold = cb == col0 ? zown0 : __ldcg(p.z_hat + j);
-          const double zj = zold + ((cb == col0 ? lbeta0 : log(bj)) - log(cj));
+          const double zj = zold + ((cb == col0 ? lbeta0 : log(bj)) - log_nomufu(cj));
           if (cb == col0) zown0 = zj;
           p.z_hat[j] = zj;
           st_line(p.zlines + j, ll_pack(zj, g1));
