@@ -205,6 +205,10 @@ class Runner:
                               q["ws"], wsn, s), "cerot_plan")
         self._ck(L.clot_expand(q["Tb"], None, B, n, m, dt, q["Tf"], s), "clot_expand")
 
+    def input_bytes(self):
+        """Device bytes the step reads as input (the cost blocks dominate)."""
+        return self.C.numel() * self.C.element_size() + 2 * self.alpha.numel() * 8
+
     def iter_kernel_ms(self):
         """Device time of the iteration launch(es) of each timed step (CUDA events on our stream)."""
         ts = [a.elapsed_time(b) for a, b in self.ev]
@@ -345,6 +349,10 @@ class ShardedRunner:
                  "cerot_plan_sharded")
         self._ck(L.clot_expand_shard(q["Tl"], None, n, R, m, dt, q["Tr"], s), "clot_expand_shard")
 
+    def input_bytes(self):
+        """Device bytes this rank's step reads as input (its rows of the cost blocks dominate)."""
+        return self.sh.C.numel() * self.sh.C.element_size() + 2 * self.sh.alpha.numel() * 8
+
     def iter_kernel_ms(self):
         ts = [a.elapsed_time(b) for a, b in self.ev]
         return statistics.mean(ts), statistics.median(ts), len(ts)
@@ -355,6 +363,9 @@ class ShardedRunner:
     def e2e_inputs(self):
         return self.Cl_host, self.sh.C, [(self.p.alpha, self.sh.alpha), (self.p.beta, self.sh.beta),
                                          (self.p.eps, self.sh.eps)], [self.rep, self.sh.w_hat, self.sh.z_hat]
+
+
+L2_BYTES = 126e6   # B200 L2 (cudaDevAttrL2CacheSize reports 126.5 MB)
 
 
 def run_ours(args, rank, world, local_rank):
@@ -397,18 +408,28 @@ def run_ours(args, rank, world, local_rank):
             R.step()
         stream.synchronize()
         rep0 = R.report_row()
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
+        # L2 rule: a rank whose inputs fit in twice the 126 MB L2 (C2, C3, C4 shards at N >= 2) overwrites a
+        # 256 MB scratch buffer between timed steps; each step is timed by its own event pair (the flush is
+        # outside them) and the step times are summed
+        in_bytes = float(R.input_bytes())
+        flush = in_bytes < 2 * L2_BYTES
+        scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         with ClockSampler(local_rank) as clk:
             barrier()
             torch.cuda.synchronize()
-            start.record(stream)
-            for _ in range(args.steps):
+            for e0, e1 in evs:
+                if flush:
+                    scratch.fill_(1)
+                e0.record(stream)
                 R.step(record=True)
-            end.record(stream)
+                e1.record(stream)
             torch.cuda.synchronize()
             barrier()
-        ms_total = max_over_ranks(start.elapsed_time(end))
+        ms_total = max_over_ranks(sum(e0.elapsed_time(e1) for e0, e1 in evs))
+        l2_note = (f"per-rank inputs {in_bytes / 1e6:.1f} MB < 2 x L2 (126 MB): a 256 MB buffer is overwritten "
+                   f"between timed steps (outside the per-step events)" if flush else
+                   f"per-rank inputs {in_bytes / 1e6:.0f} MB > 2 x L2 (126 MB): no flush")
         ms_step = ms_total / args.steps
         it_mean, it_med, nsamp = R.iter_kernel_ms()
         it_mean = max_over_ranks(it_mean)
@@ -457,8 +478,7 @@ def run_ours(args, rank, world, local_rank):
                    "n": p.n, "m": p.m, "d": p.d, "iters": iters,
                    "eps": float(p.eps[0]) if p.B == 1 else "per-problem 1e-2*mean(C_b)",
                    "step": "clot_aggregate + cerot_init + iters x (row pass + column pass) + cerot_plan + clot_expand",
-                   "l2": f"inputs ({p.C.nbytes * (world if mode == 'row_sharded' else 1) / 1e6:.0f} MB of cost) "
-                         f"larger than L2 (126 MB) at N=1: no flush",
+                   "l2": l2_note,
                    "parallelism": {"single": "rows over the SMs of one GPU",
                                    "row_sharded": (f"rows over {world} GPUs, in-kernel exchange of the m column sums "
                                                    f"per iteration over NVLink peer memory" if getattr(R, "fused", False)
