@@ -378,6 +378,8 @@ def run_ours(args, rank, world, local_rank):
         _b.build()
     if world > 1:
         tdist.barrier()
+    import paper_2311_13147_b200 as _cot
+    _cot.use_current_device()   # the library's static CUDA runtime on this rank's GPU
     p, iters = make_problem(args.workload, args.iters)
     mode = "single"
     if world > 1 or os.environ.get("COT_BENCH_SHARDED") == "1":

@@ -86,6 +86,10 @@ typedef struct {
 
 int cot_abi_version(void);
 const char* cot_last_error(void);
+/* Select the CUDA device every later call of this thread runs on (cudaSetDevice in the library's own, statically
+ * linked runtime). Optional: by default the library uses the device whose context is current on the thread
+ * (e.g. the one torch.cuda.set_device selected). Returns COT_E_CUDA for an invalid ordinal. */
+int cot_set_device(int device);
 
 /* Bytes of scratch needed by cerot_* for this shape on the current device (includes G and argmin for
  * cerot_solve, the fp64 column partials, the per-problem solver state and the plan reductions). */

@@ -49,6 +49,7 @@ _SIGS = {
     "clot_expand": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp]),
     "cerot_init": (ctypes.c_int, [_vp, _vp, _i64, _i64, _u32, _vp, _vp, _sz, _vp]),
     "cot_iter_path": (ctypes.c_int, [_i64, _i64, _i64, ctypes.c_int, _u32]),
+    "cot_set_device": (ctypes.c_int, [ctypes.c_int]),
     "cerot_iter": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl, _i64, _u32,
                                   _vp, _vp, _vp, _sz, _vp]),
     "cerot_rows": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _u32, _vp, _vp, _vp, _sz,
@@ -118,6 +119,13 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+def use_current_device():
+    """Point the library's (static) CUDA runtime at torch's current device (one call per process/thread that
+    drives a GPU other than device 0; bench.py and dist.py call it after torch.cuda.set_device)."""
+    import torch
+    _check(lib().cot_set_device(torch.cuda.current_device()), "cot_set_device")
 
 
 def _check(code: int, fn: str, ok=(0,)):

@@ -220,6 +220,11 @@ int cot_abi_version(void) { return COT_ABI_VERSION; }
 
 const char* cot_last_error(void) { return g_last_error.c_str(); }
 
+int cot_set_device(int device) {
+  COT_CHECK_CUDA(cudaSetDevice(device));
+  return COT_OK;
+}
+
 size_t cot_workspace_bytes(int64_t B, int64_t n, int64_t m, int dtype) {
   if (B < 1 || n < 1 || m < 1) return 0;
   return carve_workspace(nullptr, B, n, m, m, dtype, device_sm_count(), nullptr);
