@@ -60,6 +60,7 @@ struct TmaParams {
   int evict_last_rows;   // rows [0, evict_last_rows) of every block are streamed with an L2 evict_last hint
   int diag;              // COT_DIAG_* bits (diagnostics only)
   int pre;               // precomputed mode (NEXT-1): C is S [R][m] (n = 1) and s_ij = S_ij
+  int rpw;               // row-per-warp epilogue (several rows per CTA, EPT == 1): no block reduction per row
   unsigned long long* trace;   // diagnostics: [grid][8] cycle counters, or nullptr
   // fused multi-GPU mode (nranks > 0): the column sums of each slice are exchanged through LL lines
   int nranks, rank;      // ranks of the row partition, this rank
@@ -253,7 +254,12 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
   int* gsh = reinterpret_cast<int*>(queue + (size_t)QN * m);            // [rpu][m] a_ij = round(G_ij log2e/eps)
   double* rowstat = reinterpret_cast<double*>(gsh + (size_t)rpu * m);    // [rpu][RS] (rpu * m even: m % 4 == 0)
   double* xs = rowstat + (size_t)rpu * RS;                               // [kColScratch] column-pass scratch
-  uint64_t* full = reinterpret_cast<uint64_t*>(xs + kColScratch);
+  // row-per-warp mode: the column splits of z (kz, Fz) for every column and one fp64 column-partial row per
+  // epilogue warp
+  double* zfs = xs + kColScratch;                                          // [m] Fz_j (rpw)
+  int* zks = reinterpret_cast<int*>(zfs + (p.rpw ? m : 0));               // [m] kz_j (rpw)
+  double* wpart = reinterpret_cast<double*>(zks + (p.rpw ? m : 0));       // [rpu][m] row terms (rpw)
+  uint64_t* full = reinterpret_cast<uint64_t*>(wpart + (p.rpw ? (size_t)rpu * m : 0));
   uint64_t* empty = full + p.nslot;
   uint64_t* qfull = empty + p.nslot;
   uint64_t* qempty = qfull + QN;
@@ -271,7 +277,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
     }
     for (int q = 0; q < QN; ++q) {
       mbar_init(&qfull[q], nk);
-      mbar_init(&qempty[q], ne);
+      mbar_init(&qempty[q], p.rpw ? 1 : ne);   // row-per-warp: one warp consumes a row
     }
     for (int c = 0; c < 16; ++c) ctl[c] = 0;
     fence_mbar_init();
@@ -594,138 +600,237 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
           break;
         }
       }
-      // rows in batches of RB: one block reduction (the RB row sums) per batch; the batch's k-sums are read
-      // straight from the queue slots (released after the batch) and -G/eps from shared memory
-      for (int r0 = 0; r0 < nrows; r0 += RB) {
-        const int nb = min(RB, nrows - r0);
-        uint32_t qsb[RB];
-        {
-          uint32_t q2 = qs, ph2 = qph;
-          const long long tq0 = p.trace ? clock64() : 0;
-#pragma unroll
-          for (int b = 0; b < RB; ++b) {
-            qsb[b] = q2;
-            if (b < nb) {
-              mbar_wait(&qfull[q2], ph2);
-              if (++q2 == (uint32_t)QN) {
-                q2 = 0;
-                ph2 ^= 1u;
-              }
-            }
-          }
-          if (p.trace) c_qw += clock64() - tq0;
-        }
+      if (p.rpw) {
+        // ---- row-per-warp epilogue (rows per CTA <= 8): warp w takes rows w, w + ne, ...; per row the terms
+        // t_ij = s'_ij 2^{kz_j - kM_i - a_ij} Fz_j are summed by warp shuffles and stored (fp64) in the row's
+        // slot of a shared-memory tile; after one epilogue barrier every thread forms its columns' partial
+        // P_j = sum_i (alpha_i / r_i) t_ij over the rows in row order. kM_i: the previous iteration's shift +
+        // floor(log2 r_i); a row whose sum leaves [1e-280, 1e280] (first iteration, or a jump of the
+        // potentials) is redone with the exact kM_i = max_j (kz_j - a_ij) (warp-local, one REDUX).
         const long long te0 = p.trace ? clock64() : 0;
 #pragma unroll
-        for (int b = 1; b < RB; ++b)
-          if (b >= nb) qsb[b] = qsb[0];          // branch-free: unused rows read a valid slot, masked below
-        // ---- the row epilogues: t_ij = s_ij exp(x_ij - Mref_i), x_ij = z_j - G_ij/eps, with Mref_i the row's
-        // log-sum-exp of the previous iteration (so x - Mref <= ~log(n m) unless z jumped); r_i = sum_j t_ij
-        // in one block reduction for the batch. A batch with a row sum outside [1e-280, 1e280] (no reference
-        // yet, or a jump of the potentials) is redone in the exact two-pass form (maximum first).
-        double Mref[RB], sm[RB], tt[RB][EPT][VEC];
-#pragma unroll
-        for (int b = 0; b < RB; ++b) {
-          Mref[b] = rowstat[(r0 + (b < nb ? b : 0)) * RS + 0];
-          sm[b] = 0.0;
-        }
-        const bool stale = Mref[0] == Mref[0];      // the CTA's rows get their references together
-        auto batch_terms = [&](bool use) {
-#pragma unroll
-          for (int b = 0; b < RB; ++b) {
-            if (b >= nb) {   // CTA-uniform: short batches (e.g. one row per CTA) skip the unused rows
-#pragma unroll
-              for (int q = 0; q < EPT; ++q)
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) tt[b][q][v] = 0.0;
-              continue;
-            }
-            const int rb = r0 + (b < nb ? b : 0);
-            const int kM = __double2int_rn(Mref[b] * COT_LOG2E);   // integer row shift (exact: no rounded factor)
-#pragma unroll
-            for (int q = 0; q < EPT; ++q) {
-              const int jv = q * net + et;
-              const bool ok = use && jv < mv && b < nb;
-              const int jc = jv < mv ? jv : 0;
-              const float4 s4 = reinterpret_cast<const VT*>(queue + (size_t)qsb[b] * m)[jc];
-              const int4 a4 = reinterpret_cast<const int4*>(gsh + (size_t)rb * m)[jc];
-              const double t0 = ldexp_pos(s4.x, kz[q][0] - kM - a4.x) * Fz[q][0];
-              const double t1 = ldexp_pos(s4.y, kz[q][1] - kM - a4.y) * Fz[q][1];
-              const double t2 = ldexp_pos(s4.z, kz[q][2] - kM - a4.z) * Fz[q][2];
-              const double t3 = ldexp_pos(s4.w, kz[q][3] - kM - a4.w) * Fz[q][3];
-              tt[b][q][0] = ok ? t0 : 0.0;
-              tt[b][q][1] = ok ? t1 : 0.0;
-              tt[b][q][2] = ok ? t2 : 0.0;
-              tt[b][q][3] = ok ? t3 : 0.0;
-              sm[b] += (tt[b][q][0] + tt[b][q][1]) + (tt[b][q][2] + tt[b][q][3]);
-            }
+        for (int q = 0; q < EPT; ++q) {
+          const int jv = q * net + et;
+          if (jv < mv) {
+            reinterpret_cast<int4*>(zks)[jv] = make_int4(kz[q][0], kz[q][1], kz[q][2], kz[q][3]);
+            reinterpret_cast<double2*>(zfs)[2 * jv] = make_double2(Fz[q][0], Fz[q][1]);
+            reinterpret_cast<double2*>(zfs)[2 * jv + 1] = make_double2(Fz[q][2], Fz[q][3]);
           }
-        };
-        batch_terms(stale);
-        const long long te1 = p.trace ? clock64() : 0;
-        cblk_sumN<RB>(sm, red2, rbuf, net, nk);
-        if (p.trace) {
-          c_cmp += te1 - te0;
-          c_red += clock64() - te1;
         }
-        bool redo = false;
+        cbar(net);
+        const int ew = et >> 5;
+        const int nq = (mv + 31) >> 5;
+        const int4* zk4 = reinterpret_cast<const int4*>(zks);
+        const double2* zf2 = reinterpret_cast<const double2*>(zfs);
+        for (int r = ew; r < nrows; r += ne) {
+          const unsigned g = (unsigned)t * (unsigned)nrows + (unsigned)r;   // FIFO position of the row
+          const uint32_t slot = g % (unsigned)QN, ph = (g / (unsigned)QN) & 1u;
+          mbar_wait(&qfull[slot], ph);
+          const float4* srow = reinterpret_cast<const float4*>(queue + (size_t)slot * m);
+          const int4* arow = reinterpret_cast<const int4*>(gsh + (size_t)r * m);
+          double2* trow = reinterpret_cast<double2*>(wpart + (size_t)r * m);
+          auto row_terms = [&](int kM) {
+            double lsum = 0.0;
 #pragma unroll
-        for (int b = 0; b < RB; ++b) redo |= b < nb && !(sm[b] >= 1e-280 && sm[b] <= 1e280);
-        if (redo) {   // block-uniform (sm is the block total): exact two-pass for the whole batch
-          double mx[RB];
-#pragma unroll
-          for (int b = 0; b < RB; ++b) {
-            mx[b] = -INFINITY;
-            const int rb = r0 + (b < nb ? b : 0);
-#pragma unroll
-            for (int q = 0; q < EPT; ++q)
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) {
-                const int jv = q * net + et;
-                if (jv < mv && b < nb)   // the largest kz_j - a_ij: every term <= 2^{1/2} s'_ij, the largest >= 1/2
-                  mx[b] = fmax(mx[b], (double)(kz[q][v] - gsh[(size_t)rb * m + VEC * jv + v]));
+            for (int q = 0; q < 8; ++q) {   // nq <= 8 (m <= 1024): unrolled, predicated
+              const int jv = q * 32 + lane;
+              if (q < nq && jv < mv) {
+                const float4 s4 = srow[jv];
+                const int4 a4 = arow[jv], k4 = zk4[jv];
+                const double2 fa = zf2[2 * jv], fb = zf2[2 * jv + 1];
+                const double t0 = ldexp_pos(s4.x, k4.x - a4.x - kM) * fa.x;
+                const double t1 = ldexp_pos(s4.y, k4.y - a4.y - kM) * fa.y;
+                const double t2 = ldexp_pos(s4.z, k4.z - a4.z - kM) * fb.x;
+                const double t3 = ldexp_pos(s4.w, k4.w - a4.w - kM) * fb.y;
+                trow[2 * jv] = make_double2(t0, t1);
+                trow[2 * jv + 1] = make_double2(t2, t3);
+                lsum += (t0 + t1) + (t2 + t3);
               }
-          }
-          cblk_maxN<RB>(mx, red2, rbuf, net, nk);
+            }
+            return warp_sum(lsum);
+          };
+          const double ref = rowstat[r * RS + 0];
+          int kM = ref == ref ? __double2int_rn(ref * COT_LOG2E) : 0;
+          double rsum = ref == ref ? row_terms(kM) : 0.0;
+          if (!(rsum >= 1e-280 && rsum <= 1e280)) {   // warp-uniform: exact shift, terms again
+            int emax = -0x7fffffff;
 #pragma unroll
-          for (int b = 0; b < RB; ++b) {
-            Mref[b] = b < nb ? mx[b] * COT_LN2 : 0.0;
-            sm[b] = 0.0;
+            for (int q = 0; q < 8; ++q) {
+              const int jv = q * 32 + lane;
+              if (q < nq && jv < mv) {
+                const int4 a4 = arow[jv], k4 = zk4[jv];
+                emax = max(emax, max(max(k4.x - a4.x, k4.y - a4.y), max(k4.z - a4.z, k4.w - a4.w)));
+              }
+            }
+            kM = __reduce_max_sync(0xffffffffu, emax);
+            rsum = row_terms(kM);
           }
-          batch_terms(true);
-          cblk_sumN<RB>(sm, red2, rbuf, net, nk);
-        }
-        // release the batch's queue slots
-        __syncwarp();
-#pragma unroll
-        for (int b = 0; b < RB; ++b) {
-          if (b >= nb) break;
-          if (lane == 0) mbar_arrive(&qempty[qs]);
-          ++consumed;
-          if (++qs == (uint32_t)QN) {
-            qs = 0;
-            qph ^= 1u;
-          }
-        }
-#pragma unroll
-        for (int b = 0; b < RB; ++b) {
-          if (b >= nb) break;
-          const int r = r0 + b;
-          const double rsum = sm[b];
-          const double rinv = rcp_nomufu(rsum);   // alpha_i / r_i
-          const double rho = rowstat[r * RS + 4] * rinv;
-          if (et == 0) {   // the shift used for r_i, r_i, and the next iteration's shift: kM + floor(log2 r_i)
-            const int kM = __double2int_rn(Mref[b] * COT_LOG2E);
-            rowstat[r * RS + 0] = (double)(kM + ((__double2hiint(rsum) >> 20) - 1023)) * COT_LN2;
-            rowstat[r * RS + 1] = (double)kM * COT_LN2;
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&qempty[slot]);
+            rowstat[r * RS + 0] = (double)(kM + ((__double2hiint(rsum) >> 20) - 1023)) * COT_LN2;   // next shift
+            rowstat[r * RS + 1] = (double)kM * COT_LN2;   // shift used for r_i (natural units)
             rowstat[r * RS + 2] = rsum;
+            rowstat[r * RS + 5] = rowstat[r * RS + 4] * rcp_nomufu(rsum);   // alpha_i / r_i
           }
+        }
+        // the FIFO position after this iteration's rows (the drain after a halt continues from here)
+        consumed += (unsigned)nrows;
+        qs = consumed % (unsigned)QN;
+        qph = (consumed / (unsigned)QN) & 1u;
+        cbar(net);   // every row's terms and statistics are in shared memory
+        double rho8[8];
 #pragma unroll
-          for (int q = 0; q < EPT; ++q)
+        for (int r = 0; r < 8; ++r) rho8[r] = r < nrows ? rowstat[r * RS + 5] : 0.0;
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) P[q][v] = fma(rho, tt[b][q][v], P[q][v]);
+        for (int q = 0; q < EPT; ++q) {
+          const int jv = q * net + et;
+          if (jv < mv) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              double acc = 0.0;   // rows in order
+#pragma unroll
+              for (int r = 0; r < 8; ++r)
+                if (r < nrows) acc = fma(rho8[r], wpart[(size_t)r * m + VEC * jv + v], acc);
+              P[q][v] = acc;
+            }
+          }
         }
         if (p.trace) c_epi += clock64() - te0;
+      } else {
+      // rows in batches of RB: one block reduction (the RB row sums) per batch; the batch's k-sums are read
+        // straight from the queue slots (released after the batch) and -G/eps from shared memory
+        for (int r0 = 0; r0 < nrows; r0 += RB) {
+          const int nb = min(RB, nrows - r0);
+          uint32_t qsb[RB];
+          {
+            uint32_t q2 = qs, ph2 = qph;
+            const long long tq0 = p.trace ? clock64() : 0;
+  #pragma unroll
+            for (int b = 0; b < RB; ++b) {
+              qsb[b] = q2;
+              if (b < nb) {
+                mbar_wait(&qfull[q2], ph2);
+                if (++q2 == (uint32_t)QN) {
+                  q2 = 0;
+                  ph2 ^= 1u;
+                }
+              }
+            }
+            if (p.trace) c_qw += clock64() - tq0;
+          }
+          const long long te0 = p.trace ? clock64() : 0;
+  #pragma unroll
+          for (int b = 1; b < RB; ++b)
+            if (b >= nb) qsb[b] = qsb[0];          // branch-free: unused rows read a valid slot, masked below
+          // ---- the row epilogues: t_ij = s_ij exp(x_ij - Mref_i), x_ij = z_j - G_ij/eps, with Mref_i the row's
+          // log-sum-exp of the previous iteration (so x - Mref <= ~log(n m) unless z jumped); r_i = sum_j t_ij
+          // in one block reduction for the batch. A batch with a row sum outside [1e-280, 1e280] (no reference
+          // yet, or a jump of the potentials) is redone in the exact two-pass form (maximum first).
+          double Mref[RB], sm[RB], tt[RB][EPT][VEC];
+  #pragma unroll
+          for (int b = 0; b < RB; ++b) {
+            Mref[b] = rowstat[(r0 + (b < nb ? b : 0)) * RS + 0];
+            sm[b] = 0.0;
+          }
+          const bool stale = Mref[0] == Mref[0];      // the CTA's rows get their references together
+          auto batch_terms = [&](bool use) {
+  #pragma unroll
+            for (int b = 0; b < RB; ++b) {
+              if (b >= nb) {   // CTA-uniform: short batches (e.g. one row per CTA) skip the unused rows
+  #pragma unroll
+                for (int q = 0; q < EPT; ++q)
+  #pragma unroll
+                  for (int v = 0; v < VEC; ++v) tt[b][q][v] = 0.0;
+                continue;
+              }
+              const int rb = r0 + (b < nb ? b : 0);
+              const int kM = __double2int_rn(Mref[b] * COT_LOG2E);   // integer row shift (exact: no rounded factor)
+  #pragma unroll
+              for (int q = 0; q < EPT; ++q) {
+                const int jv = q * net + et;
+                const bool ok = use && jv < mv && b < nb;
+                const int jc = jv < mv ? jv : 0;
+                const float4 s4 = reinterpret_cast<const VT*>(queue + (size_t)qsb[b] * m)[jc];
+                const int4 a4 = reinterpret_cast<const int4*>(gsh + (size_t)rb * m)[jc];
+                const double t0 = ldexp_pos(s4.x, kz[q][0] - kM - a4.x) * Fz[q][0];
+                const double t1 = ldexp_pos(s4.y, kz[q][1] - kM - a4.y) * Fz[q][1];
+                const double t2 = ldexp_pos(s4.z, kz[q][2] - kM - a4.z) * Fz[q][2];
+                const double t3 = ldexp_pos(s4.w, kz[q][3] - kM - a4.w) * Fz[q][3];
+                tt[b][q][0] = ok ? t0 : 0.0;
+                tt[b][q][1] = ok ? t1 : 0.0;
+                tt[b][q][2] = ok ? t2 : 0.0;
+                tt[b][q][3] = ok ? t3 : 0.0;
+                sm[b] += (tt[b][q][0] + tt[b][q][1]) + (tt[b][q][2] + tt[b][q][3]);
+              }
+            }
+          };
+          batch_terms(stale);
+          const long long te1 = p.trace ? clock64() : 0;
+          cblk_sumN<RB>(sm, red2, rbuf, net, nk);
+          if (p.trace) {
+            c_cmp += te1 - te0;
+            c_red += clock64() - te1;
+          }
+          bool redo = false;
+  #pragma unroll
+          for (int b = 0; b < RB; ++b) redo |= b < nb && !(sm[b] >= 1e-280 && sm[b] <= 1e280);
+          if (redo) {   // block-uniform (sm is the block total): exact two-pass for the whole batch
+            double mx[RB];
+  #pragma unroll
+            for (int b = 0; b < RB; ++b) {
+              mx[b] = -INFINITY;
+              const int rb = r0 + (b < nb ? b : 0);
+  #pragma unroll
+              for (int q = 0; q < EPT; ++q)
+  #pragma unroll
+                for (int v = 0; v < VEC; ++v) {
+                  const int jv = q * net + et;
+                  if (jv < mv && b < nb)   // the largest kz_j - a_ij: every term <= 2^{1/2} s'_ij, the largest >= 1/2
+                    mx[b] = fmax(mx[b], (double)(kz[q][v] - gsh[(size_t)rb * m + VEC * jv + v]));
+                }
+            }
+            cblk_maxN<RB>(mx, red2, rbuf, net, nk);
+  #pragma unroll
+            for (int b = 0; b < RB; ++b) {
+              Mref[b] = b < nb ? mx[b] * COT_LN2 : 0.0;
+              sm[b] = 0.0;
+            }
+            batch_terms(true);
+            cblk_sumN<RB>(sm, red2, rbuf, net, nk);
+          }
+          // release the batch's queue slots
+          __syncwarp();
+  #pragma unroll
+          for (int b = 0; b < RB; ++b) {
+            if (b >= nb) break;
+            if (lane == 0) mbar_arrive(&qempty[qs]);
+            ++consumed;
+            if (++qs == (uint32_t)QN) {
+              qs = 0;
+              qph ^= 1u;
+            }
+          }
+  #pragma unroll
+          for (int b = 0; b < RB; ++b) {
+            if (b >= nb) break;
+            const int r = r0 + b;
+            const double rsum = sm[b];
+            const double rinv = rcp_nomufu(rsum);   // alpha_i / r_i
+            const double rho = rowstat[r * RS + 4] * rinv;
+            if (et == 0) {   // the shift used for r_i, r_i, and the next iteration's shift: kM + floor(log2 r_i)
+              const int kM = __double2int_rn(Mref[b] * COT_LOG2E);
+              rowstat[r * RS + 0] = (double)(kM + ((__double2hiint(rsum) >> 20) - 1023)) * COT_LN2;
+              rowstat[r * RS + 1] = (double)kM * COT_LN2;
+              rowstat[r * RS + 2] = rsum;
+            }
+  #pragma unroll
+            for (int q = 0; q < EPT; ++q)
+  #pragma unroll
+              for (int v = 0; v < VEC; ++v) P[q][v] = fma(rho, tt[b][q][v], P[q][v]);
+          }
+          if (p.trace) c_epi += clock64() - te0;
+        }
       }
       // ---- w_hat of this CTA's rows, LSE_i = shift_i + log r_i, by the warp of the thread that wrote the row
       // statistics (no block barrier); off the critical path in the iterated launch (after the partial lines are out)
@@ -906,8 +1011,9 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       p.trace[bid * 16 + 10] = c_cp1;
       p.trace[bid * 16 + 11] = c_pub;
     }
-    // ---- drain the queue after a halt: consume every row the k-sum warps still produce
-    while (true) {
+    // ---- drain the queue after a halt: consume every row the k-sum warps still produce (row-per-warp mode:
+    // one warp, the slots count one arrival)
+    while (!p.rpw || et < 32) {
       const unsigned kdone = lds_volatile(&ctl[7]);
       __threadfence_block();
       const unsigned prod = lds_volatile(&ctl[6]);
@@ -1014,8 +1120,12 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
   const size_t gsh_bytes = (size_t)p.rpu * m * 4;   // the integer shifts a_ij
   p.gsh = 1;
   if (gsh_bytes > 64 * 1024) return cudaErrorInvalidConfiguration;   // see tma_eligible
+  // row-per-warp epilogue for CTAs with 4-8 rows (C3: 7 rows of m = 1024 per CTA); COT_RPW=0 disables
+  const char* rpwv = getenv("COT_RPW");
+  p.rpw = (ept == 1 && p.rpu >= 4 && p.rpu <= 8 && !(rpwv && atoi(rpwv) == 0)) ? 1 : 0;
+  const size_t rpw_bytes = p.rpw ? (size_t)m * 12 + (size_t)p.rpu * m * 8 : 0;
   const size_t queue_bytes = (size_t)p.qn * row_bytes + (p.gsh ? gsh_bytes : 0) + (size_t)p.rpu * 6 * 8 +
-                             (size_t)kColScratch * 8;
+                             (size_t)kColScratch * 8 + rpw_bytes;
   const size_t budget = 220 * 1024;
   if (queue_bytes + 2 * slot_bytes + 4096 > budget) return cudaErrorInvalidConfiguration;
   p.nslot = (int)std::max<size_t>(2, std::min<size_t>(64, (budget - queue_bytes - 4096) / slot_bytes));
