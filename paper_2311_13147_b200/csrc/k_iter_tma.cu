@@ -1120,9 +1120,10 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
   const size_t gsh_bytes = (size_t)p.rpu * m * 4;   // the integer shifts a_ij
   p.gsh = 1;
   if (gsh_bytes > 64 * 1024) return cudaErrorInvalidConfiguration;   // see tma_eligible
-  // row-per-warp epilogue for CTAs with 4-8 rows (C3: 7 rows of m = 1024 per CTA); COT_RPW=0 disables
+  // row-per-warp epilogue for CTAs with <= 8 rows and one float4 of columns per epilogue thread (C3: 7 rows,
+  // 10.5 -> 9.0 us/iteration; the 8-way C4 shard: 1 row, 8.3 -> 8.0 us); COT_RPW=0 disables (comparison)
   const char* rpwv = getenv("COT_RPW");
-  p.rpw = (ept == 1 && p.rpu >= 4 && p.rpu <= 8 && !(rpwv && atoi(rpwv) == 0)) ? 1 : 0;
+  p.rpw = (ept == 1 && p.rpu <= 8 && !(rpwv && atoi(rpwv) == 0)) ? 1 : 0;
   const size_t rpw_bytes = p.rpw ? (size_t)m * 12 + (size_t)p.rpu * m * 8 : 0;
   const size_t queue_bytes = (size_t)p.qn * row_bytes + (p.gsh ? gsh_bytes : 0) + (size_t)p.rpu * 6 * 8 +
                              (size_t)kColScratch * 8 + rpw_bytes;
