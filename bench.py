@@ -122,7 +122,9 @@ def make_problem(workload: str, iters_override: int | None):
     import synthetic
     if workload == "C4":
         p = synthetic.c4_large()
-    elif workload == "C2":
+    elif workload == "C2":   # configs[1]: the three eps values of the sweep, one batch of independent problems
+        p = synthetic.c2_sweep()
+    elif workload == "C2e2":   # a single C2 problem (eps = 1e-2 * mean C): the latency-bound case
         p = synthetic.c2_ring(eps_factor=1e-2)
     elif workload == "C3":
         p = synthetic.c3_image()
@@ -639,8 +641,9 @@ def run_reference(args):
     return {"impl": "reference", "metric": _metric(), "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE.json recipe)",
-            "config": {"workload": q.name, "n": q.n, "m": q.m, "d": q.d, "iters_per_step": 1,
-                       "full_solve_iters": iters},
+            "config": {"workload": p.name, "B": p.B, "n": q.n, "m": q.m, "d": q.d, "iters_per_step": 1,
+                       "full_solve_iters": iters,
+                       "sample": "one iteration of problem 0 per step (the metric is per evaluation)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{args.steps} steps x 1 iteration of {q.name} (oracle streaming form, fp64)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -354,6 +354,15 @@ def random_cyclic(seed: int, n: int, m: int, dtype=np.float64, integer: bool = F
                    meta={"seed": seed})
 
 
+def c2_sweep(seed: int = 2) -> Problem:
+    """C2 as configs[1] states it: the ring problem at eps in {1e-1, 1e-2, 1e-3} * mean(C), 500 iterations
+    each -- three independent problems (same C, alpha, beta), one batch of B = 3."""
+    ps = [c2_ring(seed=seed, eps_factor=f) for f in (1e-1, 1e-2, 1e-3)]
+    return Problem("C2_ring_eps_sweep", np.stack([q.C for q in ps]), np.stack([q.alpha for q in ps]),
+                   np.stack([q.beta for q in ps]), np.concatenate([q.eps for q in ps]), iters=ps[0].iters, tol=0.0,
+                   meta={"eps_factors": [1e-1, 1e-2, 1e-3]})
+
+
 CONFIGS = {
     "C1": c1_tiny,
     "C2": c2_ring,
