@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libcyclicot.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "cyclicot.h")
 
 COT_F32, COT_F64 = 0, 1
-COT_COLD_START, COT_FORCE_LDG, COT_PRECOMPUTED, COT_FORCE_TMA = 0x1, 0x2, 0x4, 0x8
+COT_COLD_START, COT_FORCE_LDG, COT_PRECOMPUTED, COT_FORCE_TMA, COT_DETERMINISTIC = 0x1, 0x2, 0x4, 0x8, 0x10
 STATUS = {0: "COT_OK", 1: "COT_NOT_CONVERGED", -1: "COT_E_ARG", -2: "COT_E_NONFINITE", -3: "COT_E_MARGINAL",
           -4: "COT_E_CUDA", -5: "COT_E_NCCL", -6: "COT_E_WORKSPACE", -7: "COT_E_UNDERFLOW", -8: "COT_E_PEER"}
 REPORT_FIELDS = ("objective", "reg_primal", "dual", "row_l1", "col_l1", "col_l2", "mass", "residual")

@@ -69,7 +69,7 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, i
     w.lepoch = reinterpret_cast<unsigned long long*>(take(256));
     w.zlines = reinterpret_cast<uint4*>(take((size_t)m * 16));
     w.rlines = reinterpret_cast<uint4*>(take((size_t)2 * sm_count * 16));
-    w.plines = reinterpret_cast<uint4*>(take((size_t)2 * sm_count * m * 16));
+    w.plines = reinterpret_cast<uint4*>(take((size_t)2 * sm_count * (2 * m) * 16));   // 2 lines / value (deterministic)
     w.lcap = sm_count;
     w.ll_base = base ? static_cast<char*>(base) + o0 : nullptr;
     w.ll_bytes = off - o0;
@@ -818,7 +818,7 @@ int cerot_iter_sharded(const double* alpha, const double* beta, const void* C_lo
 // ------------------------------------------------------------------------------ fused row sharding
 size_t cot_xchg_bytes(int64_t m, int nranks) {
   if (m < 1 || nranks < 1 || nranks > kMaxRanks) return 0;
-  return kXchgHeader + (size_t)2 * nranks * m * sizeof(uint4);
+  return kXchgHeader + (size_t)2 * nranks * (2 * m) * sizeof(uint4);   // 2 lines per value in the deterministic mode
 }
 
 int cot_xchg_alloc(int64_t m, int nranks, void** xbuf, void* ipc_handle) {

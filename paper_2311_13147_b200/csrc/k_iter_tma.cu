@@ -61,6 +61,7 @@ struct TmaParams {
   int diag;              // COT_DIAG_* bits (diagnostics only)
   int pre;               // precomputed mode (NEXT-1): C is S [R][m] (n = 1) and s_ij = S_ij
   int rpw;               // row-per-warp epilogue (several rows per CTA, EPT == 1): no block reduction per row
+  int det;               // deterministic mode: 128-bit fixed-point column partials (implies rpw); 2 lines per value
   unsigned long long* trace;   // diagnostics: [grid][8] cycle counters, or nullptr
   // fused multi-GPU mode (nranks > 0): the column sums of each slice are exchanged through LL lines
   int nranks, rank;      // ranks of the row partition, this rank
@@ -105,7 +106,7 @@ constexpr unsigned long long kPeerTimeoutNs = 20000000000ull;   // 20 s without 
 #define COT_POLL_BACKOFF_NS 0
 #endif
 constexpr unsigned kPollBackoffNs = COT_POLL_BACKOFF_NS;
-constexpr int kColScratch = 256 + kMaxRanks * 8;   // doubles: column-pass groups, then the rank exchange
+constexpr int kColScratch = 256 + 2 * kMaxRanks * 8;   // doubles: column-pass groups, then the rank exchange
 constexpr int kRankScratch = 256;
 
 __device__ __forceinline__ uint4 ll_pack(double v, unsigned g) {
@@ -183,6 +184,35 @@ __device__ __forceinline__ double cblk_sum1(double v, double* red2, int& buf, in
 // product by Fz_j. The only per-element rounding is the fp32 k-sum's (random across i, averaged in the
 // column sums); no factor common to a row or a column is rounded below fp64.
 // (split_pow2_fp64 and ldexp_pos: common.cuh)
+
+// Deterministic mode (COT_DETERMINISTIC): column partials in 128-bit unsigned fixed point with 120 fraction
+// bits. Every term (alpha_i / r_i) t_ij >= 0 is truncated to a multiple of 2^-120 on its own, so the integer
+// sums are exact and do not depend on how rows are grouped into CTAs or ranks.
+__device__ __forceinline__ void fx_add(unsigned long long& lo, unsigned long long& hi, unsigned long long lo2,
+                                       unsigned long long hi2) {
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(lo2), "l"(hi2));
+}
+__device__ __forceinline__ void fx_acc(double x, unsigned long long& lo, unsigned long long& hi) {   // += x 2^120
+  if (!(x > 0.0)) return;
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  const int e = (int)(b >> 52) - 1075 + 120;   // x 2^120 = mant 2^e (x < 2^8 here: e <= 75)
+  const unsigned long long mant = (b & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+  unsigned long long l = 0, h = 0;
+  if (e >= 64) {
+    h = mant << (e - 64);
+  } else if (e > 0) {
+    l = mant << e;
+    h = mant >> (64 - e);
+  } else if (e > -64) {
+    l = mant >> (-e);
+  }
+  fx_add(lo, hi, l, h);
+}
+__device__ __forceinline__ double fx_to_double(unsigned long long lo, unsigned long long hi) {
+  return (double)hi * 0x1p-56 + (double)lo * 0x1p-120;
+}
+__device__ __forceinline__ unsigned long long dbits(double x) { return (unsigned long long)__double_as_longlong(x); }
+__device__ __forceinline__ double bitsd(unsigned long long x) { return __longlong_as_double((long long)x); }
 
 // One-barrier block reductions of N values over the epilogue warps (<= 8 warps; double-buffered scratch).
 // The sums use a transposed butterfly: at the first levels each lane keeps half of its values and sends the
@@ -649,7 +679,9 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
             }
             return warp_sum(lsum);
           };
-          const double ref = rowstat[r * RS + 0];
+          // deterministic mode: always the exact shift (a function of z and the row only, so iterates do not
+          // depend on launch boundaries either)
+          const double ref = p.det ? __longlong_as_double(0x7ff8000000000000LL) : rowstat[r * RS + 0];
           int kM = ref == ref ? __double2int_rn(ref * COT_LOG2E) : 0;
           double rsum = ref == ref ? row_terms(kM) : 0.0;
           if (!(rsum >= 1e-280 && rsum <= 1e280)) {   // warp-uniform: exact shift, terms again
@@ -679,13 +711,13 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         qs = consumed % (unsigned)QN;
         qph = (consumed / (unsigned)QN) & 1u;
         cbar(net);   // every row's terms and statistics are in shared memory
-        double rho8[8];
+        double rho8[8];   // (deterministic mode: the fixed-point partial is formed when the lines are written)
 #pragma unroll
         for (int r = 0; r < 8; ++r) rho8[r] = r < nrows ? rowstat[r * RS + 5] : 0.0;
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
           const int jv = q * net + et;
-          if (jv < mv) {
+          if (jv < mv && !p.det) {
 #pragma unroll
             for (int v = 0; v < VEC; ++v) {
               double acc = 0.0;   // rows in order
@@ -865,7 +897,23 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       const long long tp0 = p.trace ? clock64() : 0;
       // ---- publish the column partial of iteration t as LL lines of generation g1
       const unsigned g1 = (unsigned)(lep0 + t + 1);
-      {
+      if (p.det) {   // 128-bit fixed point: lines 2j (low word) and 2j + 1 (high word) of a 2m-line unit row
+        uint4* pl = p.plines + ((size_t)(g1 & 1u) * p.lcap + u) * (2 * m);
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+          const int jv = q * net + et;
+          if (jv < mv) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              const int j = VEC * jv + v;
+              unsigned long long lo = 0, hi = 0;
+              for (int r = 0; r < nrows; ++r) fx_acc(rowstat[r * RS + 5] * wpart[(size_t)r * m + j], lo, hi);
+              st_line(pl + 2 * j, ll_pack(bitsd(lo), g1));
+              st_line(pl + 2 * j + 1, ll_pack(bitsd(hi), g1));
+            }
+          }
+        }
+      } else {
         uint4* pl = p.plines + ((size_t)(g1 & 1u) * p.lcap + u) * m;
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
@@ -884,6 +932,100 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       if (p.trace) c_pub += tc0 - tp0;
       double dev = 0.0;
       const uint4* plr = p.plines + (size_t)(g1 & 1u) * p.lcap * m;
+      if (p.det) {
+        // ---- deterministic column pass: the units' 128-bit partials summed exactly (any order), the rank sums
+        // likewise; one conversion to fp64 per column, identical for every row partition
+        const uint4* pld = p.plines + (size_t)(g1 & 1u) * p.lcap * (2 * m);
+        for (int cb = col0; cb < col1; cb += 8) {
+          const int c = et & 7, grp = et >> 3;
+          const bool colok = cb + c < col1;
+          unsigned long long alo = 0, ahi = 0;
+          for (int ub = grp; ub < nblk; ub += 4 * ngrp) {   // 4 units (8 lines) in flight per thread
+            uint4 l[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int u2 = ub + (k >> 1) * ngrp;
+              l[k] = (colok && u2 < nblk) ? ld_line(pld + (size_t)u2 * (2 * m) + 2 * (cb + c) + (k & 1))
+                                          : make_uint4(0u, g1, 0u, g1);
+            }
+            unsigned todo = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (colok && ub + (k >> 1) * ngrp < nblk && !ll_ready(l[k], g1)) todo |= 1u << k;
+            const unsigned long long tp0 = todo ? gtimer() : 0ull;
+            while (todo) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (todo & (1u << k)) {
+                  l[k] = ld_line(pld + (size_t)(ub + (k >> 1) * ngrp) * (2 * m) + 2 * (cb + c) + (k & 1));
+                  if (ll_ready(l[k], g1)) todo &= ~(1u << k);
+                }
+              if (todo && gtimer() - tp0 > kPeerTimeoutNs) {
+                timeout = true;
+                break;
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; k += 2) fx_add(alo, ahi, dbits(ll_value(l[k])), dbits(ll_value(l[k + 1])));
+          }
+          if (p.trace) c_cp1 += clock64() - tc0;
+#pragma unroll
+          for (int o = 8; o <= 16; o <<= 1) {
+            const unsigned long long olo = __shfl_xor_sync(0xffffffffu, alo, o);
+            const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, ahi, o);
+            fx_add(alo, ahi, olo, ohi);
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+          if (lane < 8) {
+            xs[(grp >> 2) * 8 + c] = bitsd(alo);
+            xs[64 + (grp >> 2) * 8 + c] = bitsd(ahi);
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+          double cj = 0.0;
+          unsigned long long slo = 0, shi = 0;
+          if (et < 8)
+            for (int w2 = 0; w2 < (ngrp >> 2); ++w2) fx_add(slo, shi, dbits(xs[w2 * 8 + et]), dbits(xs[64 + w2 * 8 + et]));
+          if (fused) {   // the slice's 128-bit sums to every rank (2 lines each), then all ranks' sums, exactly
+            const int nr = p.nranks;
+            const unsigned xg = (unsigned)(xep0 + t + 1);
+            const int par = (int)(xg & 1u);
+            if (et < 8 && cb + et < col1) {
+              const uint4 llo = ll_pack(bitsd(slo), xg), lhi = ll_pack(bitsd(shi), xg);
+              for (int q = 0; q < nr; ++q) {
+                uint4* dst = p.xpeer[q] + ((size_t)(par * nr + p.rank)) * (2 * m) + 2 * (cb + et);
+                st_line(dst, llo);
+                st_line(dst + 1, lhi);
+              }
+            }
+            for (int q = et >> 3; q < nr && colok; q += ngrp) {
+              double vlo, vhi;
+              const uint4* src = p.xpeer[p.rank] + ((size_t)(par * nr + q)) * (2 * m) + 2 * (cb + c);
+              timeout |= !poll_line(src, xg, vlo);
+              timeout |= !poll_line(src + 1, xg, vhi);
+              xs[kRankScratch + q * 8 + c] = vlo;
+              xs[kRankScratch + kMaxRanks * 8 + q * 8 + c] = vhi;
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(net) : "memory");
+            if (et < 8) {
+              slo = shi = 0;
+              for (int q2 = 0; q2 < nr; ++q2)
+                fx_add(slo, shi, dbits(xs[kRankScratch + q2 * 8 + et]), dbits(xs[kRankScratch + kMaxRanks * 8 + q2 * 8 + et]));
+            }
+          }
+          if (et < 8 && cb + et < col1) {
+            cj = fx_to_double(slo, shi);
+            const int j = cb + et;
+            const double bj = cb == col0 ? beta0 : p.beta[j];
+            dev += fabs(cj - bj);
+            if (!(cj >= 1e-28)) atomicOr(&p.state[0].flags, (int)STATE_UNDERFLOW);
+            const double zold = cb == col0 ? zown0 : __ldcg(p.z_hat + j);
+            const double zj = zold + ((cb == col0 ? lbeta0 : log(bj)) - log_nomufu(cj));
+            if (cb == col0) zown0 = zj;
+            p.z_hat[j] = zj;
+            st_line(p.zlines + j, ll_pack(zj, g1));
+          }
+        }
+      } else
       for (int cb = col0; cb < col1; cb += 8) {
         const int c = et & 7, grp = et >> 3;
         const bool colok = cb + c < col1;
@@ -1123,7 +1265,9 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
   // row-per-warp epilogue for CTAs with <= 8 rows and one float4 of columns per epilogue thread (C3: 7 rows,
   // 10.5 -> 9.0 us/iteration; the 8-way C4 shard: 1 row, 8.3 -> 8.0 us); COT_RPW=0 disables (comparison)
   const char* rpwv = getenv("COT_RPW");
-  p.rpw = (ept == 1 && p.rpu <= 8 && !(rpwv && atoi(rpwv) == 0)) ? 1 : 0;
+  p.det = (a.flags & COT_DETERMINISTIC) ? 1 : 0;
+  if (p.det && (p.rpu > 8 || rows_only)) return cudaErrorInvalidValue;   // the deterministic mode needs rpw
+  p.rpw = ((ept == 1 && p.rpu <= 8 && !(rpwv && atoi(rpwv) == 0)) || p.det) ? 1 : 0;
   const size_t rpw_bytes = p.rpw ? (size_t)m * 12 + (size_t)p.rpu * m * 8 : 0;
   const size_t queue_bytes = (size_t)p.qn * row_bytes + (p.gsh ? gsh_bytes : 0) + (size_t)p.rpu * 6 * 8 +
                              (size_t)kColScratch * 8 + rpw_bytes;
