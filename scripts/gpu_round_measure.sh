@@ -2,7 +2,7 @@
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 timeout 600 python bench.py > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err; echo c4=$?
-for w in C2 C3; do timeout 600 python bench.py --workload $w --no-cpu > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; echo $w=$?; done
+for w in C2 C2e2 C3; do timeout 600 python bench.py --workload $w --no-cpu > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; echo $w=$?; done
 timeout 900 python bench.py --workload C5 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err; echo C5=$?
 COT_BENCH_MODE=precomputed timeout 600 python bench.py --no-cpu > gpurun_out/bench_C4_precomputed.json 2> gpurun_out/bench_pre.err; echo pre=$?
 COT_BENCH_SHARDED=1 timeout 600 python bench.py --no-cpu > gpurun_out/bench_C4_fused1.json 2> gpurun_out/bench_f1.err; echo f1=$?
