@@ -167,7 +167,7 @@ class Runner:
         P = lambda t: t.data_ptr()
         self.ptr = dict(C=P(self.C), a=P(self.alpha), b=P(self.beta), e=P(self.eps), G=P(self.G), A=P(self.A),
                         w=P(self.w), z=P(self.z), ws=P(self.ws), Tb=P(self.Tb), Tf=P(self.Tfull), rep=P(self.rep))
-        self.flags = int(os.environ.get("COT_BENCH_FLAGS", "0"))
+        self.flags = int(os.environ.get("COT_BENCH_FLAGS", "0"), 0)
         self.pre = os.environ.get("COT_BENCH_MODE") == "precomputed"   # NEXT-1 line (separate metric)
         self.S = torch.empty((self.B, 1, self.m, self.m), dtype=self.C.dtype, device=dev) if self.pre else None
         # which iteration kernel the library runs: 1 = persistent TMA stream (all iterations in one launch),
@@ -257,6 +257,7 @@ class ShardedRunner:
         # fused (default): the exchange inside the persistent kernel over peer-mapped buffers (cerot_iter_fused);
         # COT_SHARD_IMPL=nccl: the baseline, one ncclAllReduce + 3 launches per iteration (cerot_iter_sharded)
         self.fused = os.environ.get("COT_SHARD_IMPL", "fused") == "fused"
+        self.flags = int(os.environ.get("COT_BENCH_FLAGS", "0"), 0)   # e.g. 0x10: COT_DETERMINISTIC
         self.fused_note = None
         with stdout_to_stderr():
             self.comm = cdist.NcclComm()
@@ -337,7 +338,7 @@ class ShardedRunner:
             e0.record(self.stream)
         if self.fused:
             self._ck(L.cerot_iter_fused(q["a"], q["b"], q["C"], q["G"], n, m, self.row_begin, R, dt, q["e"],
-                                        self.iters, 0.0, 1, 0, q["w"], q["z"], q["ws"], wsn, self.xchg.world,
+                                        self.iters, 0.0, 1, self.flags, q["w"], q["z"], q["ws"], wsn, self.xchg.world,
                                         self.xchg.rank, self.xchg.xbufs, s), "cerot_iter_fused")
         else:
             self._ck(L.cerot_iter_sharded(q["a"], q["b"], q["C"], q["G"], n, m, self.row_begin, R, dt, q["e"],
@@ -482,6 +483,7 @@ def run_ours(args, rank, world, local_rank):
                    "n": p.n, "m": p.m, "d": p.d, "iters": iters,
                    "eps": float(p.eps[0]) if p.B == 1 else "per-problem 1e-2*mean(C_b)",
                    "step": "clot_aggregate + cerot_init + iters x (row pass + column pass) + cerot_plan + clot_expand",
+                   "flags": hex(getattr(R, "flags", 0)) + (" (COT_DETERMINISTIC)" if getattr(R, "flags", 0) & 0x10 else ""),
                    "l2": l2_note,
                    "parallelism": {"single": "rows over the SMs of one GPU",
                                    "row_sharded": (f"rows over {world} GPUs, in-kernel exchange of the m column sums "
