@@ -154,3 +154,16 @@ def test_lift_golden_and_mass():
     assert np.array_equal(T.sum(0), S)                                     # sum_k T_k = S exactly
     assert (T[:, 1, 2] == 0).all()
     assert np.array_equal(oracle.lift(S, np.zeros((4, 4), int), 1)[0], S)  # S:217 (n = 1)
+
+
+def test_c2_sweep_is_configs1():
+    """bench.py's C2 workload = BASELINE configs[1] as stated: the ring problem at eps in {1e-1, 1e-2, 1e-3} x
+    mean(C), as one batch of three independent problems sharing C, alpha and beta (each problem equal to the
+    single-eps generator's)."""
+    p = synthetic.c2_sweep()
+    assert p.batched and p.B == 3 and p.n == 8 and p.m == 128 and p.iters == 500 and p.C.dtype == np.float32
+    for b, f in enumerate((1e-1, 1e-2, 1e-3)):
+        q = synthetic.c2_ring(eps_factor=f)
+        assert np.array_equal(p.C[b], q.C) and np.array_equal(p.alpha[b], q.alpha) and np.array_equal(p.beta[b], q.beta)
+        assert p.eps[b] == q.eps[0]
+        assert np.isclose(p.eps[b], f * p.C[b].astype(np.float64).mean(), rtol=1e-12)
