@@ -3,6 +3,8 @@
 // once and written to the n output positions (r*m + i, ((r + k) mod n)*m + j), r = 0..n-1, with 128-bit
 // streaming (evict-first) stores. In C-LOT mode the source value is S_ij where argmin_ij == k, else 0
 // (the lift of eq. optimal_solution_problem_CLOT). Pure placement => bit-exact.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -115,6 +117,54 @@ __global__ void __launch_bounds__(128) k_expand_bulk(const T* __restrict__ S, co
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Small blocks (C5: n = 16, m = 128, a 512-byte segment per block row): one unit = row i of all n blocks of a
+// problem. The n segments are assembled in shared memory twice over (T_0 .. T_{n-1}, T_0 .. T_{n-2}), so every
+// row r*R + i of the dense plan -- T_{(s - r) mod n}[i] for s = 0 .. n-1 -- is one contiguous window, written by
+// ONE bulk store of d values (n stores of n*m values instead of n^2 stores of m).
+template <typename T>
+__global__ void __launch_bounds__(256) k_expand_rows(const T* __restrict__ S, const int32_t* __restrict__ A,
+                                                     int64_t B, int n, int64_t m, int64_t R, T* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* bufs = reinterpret_cast<T*>(smem_raw);
+  const int64_t d = (int64_t)n * m;
+  const int64_t win = (int64_t)(2 * n - 1) * m;   // elements per slot
+  const int64_t units = B * R;
+  const uint32_t row_bytes = (uint32_t)(d * sizeof(T));
+  int slot = 0;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x, slot ^= 1) {
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();
+    const int64_t b = u / R, i = u - b * R;
+    T* buf = bufs + slot * win;
+    for (int64_t idx = threadIdx.x; idx < d; idx += blockDim.x) {
+      const int k = (int)(idx / m);
+      const int64_t j = idx - (int64_t)k * m;
+      T v;
+      if (A == nullptr) {
+        v = __ldg(S + ((b * n + k) * R + i) * m + j);
+      } else {
+        const int64_t o = (b * R + i) * m + j;
+        v = (__ldg(A + o) == k) ? __ldg(S + o) : T(0);
+      }
+      buf[idx] = v;
+      if (k < n - 1) buf[idx + d] = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int r = 0; r < n; ++r) {
+        const int start = (n - r) % n;
+        T* dst = out + (b * (int64_t)n * R + (int64_t)r * R + i) * d;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                     "r"(smem_u32(buf + (int64_t)start * m)), "r"(row_bytes)
+                     : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 cudaError_t launch_expand(const void* S, const int32_t* A, int64_t B, int64_t n, int64_t m, int dtype, void* out,
                           cudaStream_t s, int64_t R) {
   if (R < 0) R = m;
@@ -122,6 +172,16 @@ cudaError_t launch_expand(const void* S, const int32_t* A, int64_t B, int64_t n,
   const int64_t units = B * n * R;
   const int grid = (int)(units < (int64_t)sms * 16 ? units : (int64_t)sms * 16);
   const size_t esz = dtype == COT_F32 ? 4 : 8;
+  const size_t rows_smem = 2 * (size_t)(2 * n - 1) * m * esz;
+  if ((m * esz) % 16 == 0 && rows_smem <= 48 * 1024 && !getenv("COT_EXPAND_SEGMENTS")) {
+    const int64_t runits = B * R;
+    const int rgrid = (int)(runits < (int64_t)sms * 8 ? runits : (int64_t)sms * 8);
+    if (dtype == COT_F32)
+      k_expand_rows<float><<<rgrid, 256, rows_smem, s>>>((const float*)S, A, B, (int)n, m, R, (float*)out);
+    else
+      k_expand_rows<double><<<rgrid, 256, rows_smem, s>>>((const double*)S, A, B, (int)n, m, R, (double*)out);
+    return cudaGetLastError();
+  }
   if ((m * esz) % 16 == 0 && m * esz <= 32768) {
     const int64_t mpad = (m + 31) & ~int64_t(31);
     const size_t smem = 2 * mpad * esz;

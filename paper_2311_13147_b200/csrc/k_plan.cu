@@ -4,6 +4,8 @@
 // Numerics: y_ij = w_hat_i + z_hat_j - G_ij/eps and E_ij = exp(y_ij) in fp64 once per (i,j);
 // a_ijk = (G_ij - C_ijk)/eps <= 0 in fp64, exp(a) in fp32 (accurate exp2f, not ex2.approx),
 // T = E * exp(a) and log T = y + a in fp64. All sums fp64 in a fixed order (deterministic).
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -222,11 +224,17 @@ cudaError_t launch_plan(const IterArgs& a, const Workspace& ws, const UnitPlan& 
   pp.partials = ws.partials[0];
   pp.scal = ws.plan_scal;
   pp.state = ws.state;
+  // a unit's CTA has one thread per vector of columns (32 for m = 128): with small m, keep up to 32 such CTAs
+  // resident per SM (C5: 4096 single-warp units; 4 per SM left the T-block stream at 1.5 TB/s)
+  const int64_t vw = a.dtype == COT_F32 ? (a.m % 4 == 0 ? 4 : 1) : (a.m % 2 == 0 ? 2 : 1);
+  const int64_t nt = std::min<int64_t>(256, (a.m / vw + 31) / 32 * 32);
+  const int per_sm = (int)std::max<int64_t>(4, std::min<int64_t>(32, 1024 / nt));
+  const int grid = (int)std::min<int64_t>(up.U, (int64_t)device_sm_count() * per_sm);
   cudaError_t e;
   if (a.dtype == COT_F32)
-    e = (a.m % 4 == 0) ? plan_dispatch<float, 4>(pp, up.grid, a.m, s) : plan_dispatch<float, 1>(pp, up.grid, a.m, s);
+    e = (a.m % 4 == 0) ? plan_dispatch<float, 4>(pp, grid, a.m, s) : plan_dispatch<float, 1>(pp, grid, a.m, s);
   else
-    e = (a.m % 2 == 0) ? plan_dispatch<double, 2>(pp, up.grid, a.m, s) : plan_dispatch<double, 1>(pp, up.grid, a.m, s);
+    e = (a.m % 2 == 0) ? plan_dispatch<double, 2>(pp, grid, a.m, s) : plan_dispatch<double, 1>(pp, grid, a.m, s);
   return e;
 }
 
