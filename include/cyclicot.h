@@ -127,6 +127,11 @@ int cot_check_nonfinite(const int32_t* d_nonfinite, void* stream);
 /*   Pure placement: bit-exact copies. T_full must hold B*d*d elements.                               */
 int clot_expand(const void* S, const int32_t* argmin, int64_t B, int64_t n, int64_t m, int dtype,
                 void* T_full, void* stream);
+/* Which expansion kernel clot_expand / clot_expand_shard select for (n, m, dtype) (introspection for tests   */
+/* and profiling; no device work): 2 = whole dense rows assembled in shared memory (small n*m), 1 = one       */
+/* m-segment per unit written by n TMA bulk stores (m*esize % 16 == 0, m*esize <= 32 KiB), 0 = vector stores  */
+/* (ragged m). -1 on bad arguments.                                                                           */
+int cot_expand_path(int64_t n, int64_t m, int dtype);
 
 /* ---------------------------------------------------------------------------------------------- */
 /* A3+A4  Cyclic Sinkhorn iterations (Alg. 2 lines 3-6) in the log domain of             */

@@ -4,7 +4,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["expand_vector", "expand_cost", "expand_plan", "block_shift_permutation", "symmetrize",
+__all__ = ["expand_vector", "expand_cost", "expand_plan", "expand_plan_rows", "block_shift_permutation", "symmetrize",
            "aggregate", "lift", "fold_average", "is_block_circulant"]
 
 
@@ -39,6 +39,21 @@ def expand_plan(T_blocks: np.ndarray) -> np.ndarray:
     for r in range(n):
         for s in range(n):
             out[r * m:(r + 1) * m, s * m:(s + 1) * m] = T_blocks[(s - r) % n]
+    return out
+
+
+def expand_plan_rows(T_blocks: np.ndarray, rows) -> np.ndarray:
+    """Selected rows I of the d x d plan of Lemma 1 without building the whole plan: row
+    I = r*m + i is (T_{(0 - r) mod n}[i], T_{(1 - r) mod n}[i], ..., T_{(n-1 - r) mod n}[i]), the same
+    placement block (r, s) = T_{(s - r) mod n} as expand_plan, written out per row. For sampling plans
+    too large for the host (C4: d = 65536)."""
+    T_blocks = np.asarray(T_blocks)
+    n, m, _ = T_blocks.shape
+    out = np.empty((len(rows), n * m), dtype=T_blocks.dtype)
+    for q, I in enumerate(rows):
+        r, i = divmod(int(I), m)
+        for s in range(n):
+            out[q, s * m:(s + 1) * m] = T_blocks[(s - r) % n][i]
     return out
 
 

@@ -323,6 +323,11 @@ int cerot_iter(const double* alpha, const double* beta, const void* C, const voi
   return COT_OK;
 }
 
+int cot_expand_path(int64_t n, int64_t m, int dtype) {
+  if (n < 1 || m < 1 || (dtype != COT_F32 && dtype != COT_F64)) return -1;
+  return expand_path(n, m, dtype);
+}
+
 int cot_iter_path(int64_t B, int64_t n, int64_t m, int dtype, uint32_t flags) {
   if (B < 1 || n < 1 || m < 1) return -1;
   const IterArgs a = make_args(nullptr, nullptr, nullptr, nullptr, B, n, m, dtype, nullptr, 0.0, 1, flags, nullptr,

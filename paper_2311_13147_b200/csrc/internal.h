@@ -75,6 +75,7 @@ cudaError_t launch_aggregate(const void* C, int64_t B, int64_t n, int64_t m, int
                              int32_t* nonfinite, cudaStream_t s, int64_t R = -1);
 cudaError_t launch_precompute(const void* C, const void* G, int64_t B, int64_t n, int64_t m, int dtype,
                               const double* eps, void* S, cudaStream_t s);
+int expand_path(int64_t n, int64_t m, int dtype);
 cudaError_t launch_expand(const void* S, const int32_t* A, int64_t B, int64_t n, int64_t m, int dtype, void* out,
                           cudaStream_t s, int64_t R = -1);
 

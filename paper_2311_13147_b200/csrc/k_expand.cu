@@ -165,6 +165,16 @@ __global__ void __launch_bounds__(256) k_expand_rows(const T* __restrict__ S, co
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Which kernel launch_expand selects: 2 = k_expand_rows (whole dense rows from shared memory), 1 = k_expand_bulk
+// (one segment, n bulk stores), 0 = k_expand (vector stores; ragged m).
+int expand_path(int64_t n, int64_t m, int dtype) {
+  const size_t esz = dtype == COT_F32 ? 4 : 8;
+  const size_t rows_smem = 2 * (size_t)(2 * n - 1) * m * esz;
+  if ((m * esz) % 16 == 0 && rows_smem <= 48 * 1024 && !getenv("COT_EXPAND_SEGMENTS")) return 2;
+  if ((m * esz) % 16 == 0 && m * esz <= 32768) return 1;
+  return 0;
+}
+
 cudaError_t launch_expand(const void* S, const int32_t* A, int64_t B, int64_t n, int64_t m, int dtype, void* out,
                           cudaStream_t s, int64_t R) {
   if (R < 0) R = m;
@@ -173,7 +183,8 @@ cudaError_t launch_expand(const void* S, const int32_t* A, int64_t B, int64_t n,
   const int grid = (int)(units < (int64_t)sms * 16 ? units : (int64_t)sms * 16);
   const size_t esz = dtype == COT_F32 ? 4 : 8;
   const size_t rows_smem = 2 * (size_t)(2 * n - 1) * m * esz;
-  if ((m * esz) % 16 == 0 && rows_smem <= 48 * 1024 && !getenv("COT_EXPAND_SEGMENTS")) {
+  const int path = expand_path(n, m, dtype);
+  if (path == 2) {
     const int64_t runits = B * R;
     const int rgrid = (int)(runits < (int64_t)sms * 8 ? runits : (int64_t)sms * 8);
     if (dtype == COT_F32)
@@ -182,7 +193,7 @@ cudaError_t launch_expand(const void* S, const int32_t* A, int64_t B, int64_t n,
       k_expand_rows<double><<<rgrid, 256, rows_smem, s>>>((const double*)S, A, B, (int)n, m, R, (double*)out);
     return cudaGetLastError();
   }
-  if ((m * esz) % 16 == 0 && m * esz <= 32768) {
+  if (path == 1) {
     const int64_t mpad = (m + 31) & ~int64_t(31);
     const size_t smem = 2 * mpad * esz;
     cudaError_t e;

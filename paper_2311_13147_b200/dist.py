@@ -227,12 +227,13 @@ class ShardedCerot:
                                         self._comm, _stream(self.stream)), "cerot_plan_sharded")
         return T, rep
 
-    def expand(self, T_local, out=None):
-        """The held rows of the dense d x d plan: [n][R][d] (row (r, i) = full row r*m + row_begin + i)."""
+    def expand(self, T_local, out=None, argmin=None):
+        """The held rows of the dense d x d plan: [n][R][d] (row (r, i) = full row r*m + row_begin + i).
+        T_local: C-EROT blocks [n][R][m], or with argmin [R][m] (C-LOT lift) the small-LP solution rows S [R][m]."""
         import torch
         d = self.n * self.m
         out = torch.empty((self.n, self.R, d), dtype=T_local.dtype, device=T_local.device) if out is None else out
-        _check(lib().clot_expand_shard(_ptr(T_local), None, self.n, self.R, self.m, self.dt, _ptr(out),
+        _check(lib().clot_expand_shard(_ptr(T_local), _ptr(argmin), self.n, self.R, self.m, self.dt, _ptr(out),
                                        _stream(self.stream)), "clot_expand_shard")
         return out
 

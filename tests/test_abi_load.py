@@ -70,3 +70,13 @@ def test_sass_is_sm100a_and_uses_bulk_copies(L):
                           text=True).stdout
     assert "MUFU.EX2" in sass           # the Gibbs-kernel exponentials on the SFU
     assert "UBLKCP" in sass             # TMA bulk copies (expand stores)
+
+
+def test_expand_path_query(L):
+    """cot_expand_path reports the kernel clot_expand selects (no device work): the C3/C4 shapes take the TMA
+    bulk-store kernel, C5 the whole-row kernel, ragged m the vector-store kernel."""
+    assert L.cot_expand_path(4, 1024, cot.COT_F32) == 1
+    assert L.cot_expand_path(64, 1024, cot.COT_F32) == 1
+    assert L.cot_expand_path(16, 128, cot.COT_F32) == 2
+    assert L.cot_expand_path(4, 130, cot.COT_F32) == 0
+    assert L.cot_expand_path(0, 4, cot.COT_F32) == -1

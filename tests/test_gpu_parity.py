@@ -171,14 +171,21 @@ def test_c1_solve_api():
     _compare(p, np.array([reps[0][f] for f in cot.REPORT_FIELDS]), T.cpu().numpy(), w, z, 1e-10, 1e-10)
 
 
+_PATH_FLAGS = {"cluster": 0, "tma": 0x8, "ldg": 0x2}   # default (cluster-resident), COT_FORCE_TMA, COT_FORCE_LDG
+_PATH_CODE = {"cluster": 2, "tma": 1, "ldg": 0}
+
+
 @pytest.mark.parametrize("eps_factor", [1e-1, 1e-2, 1e-3])
-@pytest.mark.parametrize("path", ["tma", "ldg"])
+@pytest.mark.parametrize("path", ["cluster", "tma", "ldg"])
 def test_c2_500_iterations(eps_factor, path):
     """C2 (configs[1]): ring, fp32, 500 iterations at each eps; iterate parity (not converged at 1e-3).
-    Both row paths: the persistent TMA kernel and the generic LDG kernels (COT_FORCE_LDG)."""
+    Every row path: the cluster-resident kernel C2 takes by default, the persistent TMA kernel (COT_FORCE_TMA)
+    and the generic LDG kernels (COT_FORCE_LDG); the path taken is asserted."""
     p = synthetic.c2_ring(eps_factor=eps_factor)
+    flags = _PATH_FLAGS[path]
+    assert cot.lib().cot_iter_path(1, p.n, p.m, 0, flags) == _PATH_CODE[path]
     w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 500, form="kernel")
-    _, T, rep, it, _ = _gpu_run(p, 500, flags=cot.COT_FORCE_LDG if path == "ldg" else 0)
+    _, T, rep, it, _ = _gpu_run(p, 500, flags=flags)
     assert it[0] == 500
     _compare(p, rep[0], T, w, z)
 
@@ -289,6 +296,33 @@ def test_split_rows_cols_api_matches_iter():
     assert it[0] == 25
 
 
+def check_stop_iteration(q, it_g, tol, check_every, iters_max, run_fixed, rep_g=None, T_g=None, rel_band=1e-3):
+    """Freeze-rule parity for fp32 problems, with no silent skip:
+      * the GPU's stopping iteration equals the oracle's, or it is one check away AND the oracle's fp64 monitor at
+        the two checks involved lies within `rel_band` of tol (the only case where fp32 rounding of the monitor
+        may legitimately decide the other way);
+      * the GPU's tol-run state (rep_g, T_g) is compared with the oracle run for exactly it_g iterations;
+      * the plan and report at the ORACLE's stopping iteration are always compared too: run_fixed(t) runs the GPU
+        for exactly t iterations (no tol) and returns (rep, T)."""
+    eps = float(q.eps[0])
+    w, z, t, hist = oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, eps, iters_max, tol=tol, check_every=check_every,
+                                           form="kernel", record=True)
+    assert t < iters_max, "oracle did not converge"
+    it_g = int(it_g)
+    if it_g != t:
+        assert abs(it_g - t) == check_every, (it_g, t)
+        res = {k + 1: h[2] for k, h in enumerate(hist)}
+        edge = min(it_g, t)                 # the check at which the two decisions differ
+        assert abs(res[edge] / tol - 1) < rel_band, ("stop iteration differs without a borderline monitor",
+                                                     it_g, t, res[edge], tol)
+    if rep_g is not None:
+        wg, zg, _, _ = oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, eps, it_g, form="kernel")
+        _compare(q, rep_g, T_g, wg, zg)
+    rep_t, T_t = run_fixed(t)
+    _compare(q, rep_t, T_t, w, z)
+    return t
+
+
 def test_cluster_path_batch_freeze_fp32():
     """The cluster-resident path (fp32, m <= 256): per-problem freeze rule in a batch with mixed eps."""
     p = synthetic.random_cyclic(seed=6, n=6, m=32, B=4, eps=0.1, dtype=np.float32)
@@ -297,13 +331,16 @@ def test_cluster_path_batch_freeze_fp32():
     prob.init().iterate(4000, tol=1e-7, check_every=5)
     T, rep = prob.plan(T_blocks=True)
     it, conv, _ = prob.state()
+    T, rep = T.cpu().numpy(), rep.cpu().numpy()
     for b in range(p.B):
         q = p.single(b)
-        w, z, t, _ = oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, float(q.eps[0]), 4000, tol=1e-7, check_every=5,
-                                            form="kernel")
-        assert conv[b] == 1 and abs(int(it[b]) - t) <= 5
-        if it[b] == t:
-            _compare(q, rep.cpu().numpy()[b], T.cpu().numpy()[b], w, z)
+        assert conv[b] == 1
+
+        def run_fixed(t, q=q):
+            _, Tq, rq, itq, _ = _gpu_run(q, t)
+            assert itq[0] == t
+            return rq[0], Tq
+        check_stop_iteration(q, it[b], 1e-7, 5, 4000, run_fixed, rep[b], T[b])
 
 
 @pytest.mark.parametrize("maker,path", [(lambda: synthetic.c2_ring(eps_factor=1e-2), "cluster"),

@@ -20,6 +20,28 @@ def test_expand_golden():
         assert np.array_equal(oracle.expand_plan(blocks), np.array(case["dense"])), case["cite"]
 
 
+def test_expand_plan_rows_golden_and_against_whole_plan():
+    """expand_plan_rows (row sampling of Lemma 1's plan, for plans too large to build) on the SPEC worked
+    examples (golden dense matrices) and, on random blocks, row for row against
+    expand_plan -- including a broken placement that must be caught."""
+    g = golden("expand_examples.json")
+    for case in g["cases"]:
+        blocks = np.array(case["blocks"], dtype=np.float64)
+        dense = np.array(case["dense"])
+        rows = list(range(dense.shape[0]))
+        assert np.array_equal(oracle.expand_plan_rows(blocks, rows), dense), case["cite"]
+    rng = np.random.default_rng(3)
+    for n, m in [(1, 5), (3, 4), (7, 2)]:
+        blocks = rng.random((n, m, m)).astype(np.float32)
+        rows = rng.permutation(n * m)[: max(1, n * m // 2)]
+        got = oracle.expand_plan_rows(blocks, rows)
+        assert got.dtype == np.float32
+        assert np.array_equal(got, oracle.expand_plan(blocks)[rows])
+        if n > 1:   # a transposed shift (s + r instead of s - r) differs on some sampled row
+            wrong = np.stack([np.concatenate([blocks[(s + I // m) % n][I % m] for s in range(n)]) for I in rows])
+            assert not np.array_equal(got, wrong) or n == 2
+
+
 def test_expand_vector_and_fold_golden():
     g = golden("expand_examples.json")
     for case in g["fold_average"]:
