@@ -104,7 +104,7 @@ def test_bulk_fp64_full_bitexact():
 
 def test_bulk_batched_bitexact():
     """B > 1 through k_expand_bulk (the (b, k, i) unit decomposition and the b * d * d output offset)."""
-    B, n, m = 3, 5, 512
+    B, n, m = 3, 7, 512
     assert cot.lib().cot_expand_path(n, m, F32) == 1
     T = np.stack([_blocks(40 + b, n, m, np.float32) for b in range(B)])
     got = cot.clot_expand(_dev(T), n).cpu().numpy()
