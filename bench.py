@@ -306,6 +306,14 @@ class ShardedRunner:
                 self.fused = False
                 self.fused_note = f"fused exchange probe failed ({err or 'on another rank'}): NCCL baseline"
                 print(f"[bench] {self.fused_note}", file=sys.stderr)
+        # flags actually run: the NCCL baseline has no fixed-point partials (COT_DETERMINISTIC is the fused path's)
+        self.flags_requested = self.flags
+        if not self.fused and self.flags & 0x10:
+            self.flags &= ~0x10
+            self.fused_note = (self.fused_note or "NCCL baseline") + "; COT_DETERMINISTIC dropped (fused path only)"
+        self.exchange = {"path": "fused" if self.fused else "nccl",
+                         "probe": ("ok (3 fused iterations on every rank)" if self.fused else
+                                   (self.fused_note or "not attempted (COT_SHARD_IMPL=nccl)"))}
         d = p.n * p.m
         self.Tl = torch.empty_like(self.sh.C)
         self.Trows = torch.empty((p.n, self.R, d), dtype=self.sh.C.dtype, device=dev)
@@ -342,7 +350,8 @@ class ShardedRunner:
                                         self.xchg.rank, self.xchg.xbufs, s), "cerot_iter_fused")
         else:
             self._ck(L.cerot_iter_sharded(q["a"], q["b"], q["C"], q["G"], n, m, self.row_begin, R, dt, q["e"],
-                                          self.iters, 0.0, 1, 0, q["w"], q["z"], q["ws"], wsn, self.comm.handle, s),
+                                          self.iters, 0.0, 1, self.flags, q["w"], q["z"], q["ws"], wsn,
+                                          self.comm.handle, s),
                      "cerot_iter_sharded")
         if record:
             e1.record(self.stream)
@@ -509,10 +518,13 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": R.launches_per_step * args.steps,
         "result": {"objective": float(rep0[0]), "dual": float(rep0[2]), "row_l1": float(rep0[3])},
     }
+    out["exchange"] = (R.exchange if mode == "row_sharded" else
+                       {"path": "none", "probe": "not needed (" + ("single GPU" if mode == "single" else
+                                                                    "independent problems per rank") + ")"})
     if e2e:
         out["e2e"] = e2e
     if not args.no_cpu and rank == 0:
-        out["cpu_baseline"] = cpu_baseline(p, args)
+        out["cpu_baseline"] = cpu_baseline(p, args, args.workload)
     out["clocks"] = clocks
     if mode == "row_sharded":
         if R.xchg is not None:
@@ -595,59 +607,155 @@ def run_e2e(R, p, steps, stream):
 
 
 # ------------------------------------------------------------------------------------------ oracle arm
-def _oracle_iters(p, iters):
-    import oracle
-    q = p.single(0) if p.batched else p
-    t = time.perf_counter()
-    oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, float(q.eps[0]), iters, form="stream")
-    return time.perf_counter() - t, q
+# The oracle as it stands (fp64 NumPy, never tuned for this), on the box's host cores: one BLAS
+# thread per worker process, one worker per core of sched_getaffinity, each worker running the oracle on its own
+# problem of the workload (C5: problem `worker` of the batch; C2: the eps sweep's problems round-robin; C3/C4: the
+# single problem, i.e. independent replicas). Workers are spawned (no fork of a CUDA process) and build their
+# problem from the seeded generators before the timed region.
+_W = {}
 
 
-def cpu_baseline(p, args):
-    """The oracle as it stands (fp64 NumPy, streaming form = the same n*m^2 work per iteration), timed on
-    the host on a bounded sample: a few iterations of one problem of the same workload."""
+def _worker_problem(workload: str, w: int):
+    import synthetic
+    if workload == "C4":
+        return synthetic.c4_large()
+    if workload == "C3":
+        return synthetic.c3_image()
+    if workload == "C2":
+        return synthetic.c2_sweep().single(w % 3)
+    if workload == "C2e2":
+        return synthetic.c2_ring(eps_factor=1e-2)
+    if workload == "C5":
+        return synthetic.c5_batched(B=1, first=w % 4096).single(0)
+    raise SystemExit(f"unknown workload {workload}")
+
+
+def _worker_init(workload: str, counter, lock):
     try:
         from threadpoolctl import threadpool_limits
-        lim = threadpool_limits(1)
+        _W["lim"] = threadpool_limits(1)
     except Exception:
-        lim = None
+        pass
+    with lock:
+        w = counter.value
+        counter.value += 1
+    _W["q"] = _worker_problem(workload, w)
+    _W["w"] = w
+
+
+def _worker_run(args):
+    """k iterations of the oracle's cyclic Sinkhorn in `form` on this worker's problem, after a barrier (so the
+    all-core runs overlap). Returns (evaluations-equivalent n*m^2*k, seconds)."""
+    import oracle
+    k, form, barrier = args
+    q = _W["q"]
+    if barrier is not None:
+        barrier.wait()
+    t = time.perf_counter()
+    oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, float(q.eps[0]), k, form=form)
+    return float(q.n * q.m * q.m * k), time.perf_counter() - t
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+class OraclePool:
+    """All host cores running the oracle (one single-threaded worker per core)."""
+
+    def __init__(self, workload: str, cores: int | None = None):
+        import multiprocessing as mp
+        self.ctx = mp.get_context("spawn")
+        self.cores = cores or len(os.sched_getaffinity(0))
+        self.mgr = self.ctx.Manager()
+        counter, lock = self.mgr.Value("i", 0), self.mgr.Lock()
+        self.pool = self.ctx.Pool(self.cores, initializer=_worker_init, initargs=(workload, counter, lock))
+        self.pool.map(_worker_run, [(0, "stream", None)] * self.cores, chunksize=1)   # all workers built
+
+    def run(self, k: int, form: str, workers: int | None = None):
+        """k iterations on `workers` workers at once; returns (total evals, wall seconds, per-worker seconds)."""
+        P = workers or self.cores
+        bar = self.mgr.Barrier(P) if P > 1 else None
+        t = time.perf_counter()
+        res = self.pool.map(_worker_run, [(k, form, bar)] * P, chunksize=1)
+        wall = time.perf_counter() - t
+        ev = sum(r[0] for r in res)
+        return ev, max(r[1] for r in res), wall
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+        self.mgr.shutdown()
+
+
+def _iters_for(p, seconds: float, rate: float = 4.0e7) -> int:
     q = p.single(0) if p.batched else p
-    per_iter = q.n * q.m * q.m
-    k = max(1, min(50, int(12.0 / max(per_iter / 4.0e7, 1e-6))))     # ~10-20 s at ~40M evals/s
-    dt, _ = _oracle_iters(p, k)
-    if lim is not None:
-        lim.unregister() if hasattr(lim, "unregister") else None
-    return {"value": per_iter * k / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{q.name}: {k} cyclic Sinkhorn iterations (oracle streaming form, fp64 NumPy, 1 thread), "
-                      f"{dt:.1f} s", "host_cores_available": len(os.sched_getaffinity(0))}
+    return max(1, min(500, int(seconds * rate / (q.n * q.m * q.m))))
+
+
+def cpu_baseline(p, args, workload: str):
+    """The oracle as it stands timed on this box's host cores on a bounded sample of the same workload: the
+    streaming form (the same n*m^2 work per iteration as the kernel) on one core and on all cores, and Alg. 2 with
+    K precomputed (the paper's own CPU algorithm; its rate counted in n*m^2-equivalent evaluations, the one-off
+    log K build inside the timed region) on all cores. ~25 s in total."""
+    sec = float(os.environ.get("COT_CPU_BASELINE_SECONDS", "6"))   # per leg (tests use less)
+    pool = OraclePool(workload)
+    try:
+        k = _iters_for(p, sec)
+        ev1, t1, _ = pool.run(k, "stream", workers=1)
+        evP, tP, _ = pool.run(k, "stream")
+        kk = max(k, _iters_for(p, sec, rate=4.0e7 * p.n))
+        evK, tK, _ = pool.run(kk, "kernel")
+    finally:
+        pool.close()
+    q = p.single(0) if p.batched else p
+    return {"value": evP / tP, "unit": UNIT, "cores": pool.cores, "kind": "oracle",
+            "per_core": ev1 / t1, "all_core": evP / tP,
+            "kernel_form": {"value": evK / tK, "unit": "n*m^2-equivalent evals/s (Alg. 2, K precomputed once)",
+                            "iters": kk, "cores": pool.cores, "seconds": tK},
+            "cpu_model": _cpu_model(),
+            "sample": (f"{workload}: {k} cyclic Sinkhorn iterations per worker (oracle streaming form, fp64 NumPy, "
+                       f"1 BLAS thread), 1 worker ({t1:.1f} s) and {pool.cores} workers at once ({tP:.1f} s); "
+                       f"kernel form {kk} iterations x {pool.cores} workers ({tK:.1f} s); "
+                       f"each worker its own problem ({q.name} recipe)")}
 
 
 def run_reference(args):
-    """--impl reference: the oracle timed on the host; one step = one cyclic Sinkhorn
-    iteration (streaming form) of the same workload, a bounded sample of the full solve."""
+    """--impl reference: the oracle timed on the host's cores. One step = one cyclic Sinkhorn
+    iteration (streaming form: the same n*m^2 work as the kernel) on every core at once, each worker on its own
+    problem of the workload -- a bounded sample of the full solve; value = evaluations / step time."""
     p, iters = make_problem(args.workload, args.iters)
+    pool = OraclePool(args.workload)
     try:
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(1)
-    except Exception:
-        pass
-    for _ in range(args.warmup):
-        _oracle_iters(p, 1)
-    t = time.perf_counter()
-    for _ in range(args.steps):
-        dt, q = _oracle_iters(p, 1)
-    total = time.perf_counter() - t
-    ms = total / args.steps * 1e3
+        for _ in range(args.warmup):
+            pool.run(1, "stream")
+        tot_ev, tot_t = 0.0, 0.0
+        for _ in range(args.steps):
+            ev, t, wall = pool.run(1, "stream")
+            tot_ev += ev
+            tot_t += wall
+    finally:
+        pool.close()
+    ms = tot_t / args.steps * 1e3
+    value = tot_ev / tot_t
     q = p.single(0) if p.batched else p
-    value = q.n * q.m * q.m / (ms / 1e3)
+    sample = (f"{args.steps} steps x 1 iteration (oracle streaming form, fp64 NumPy, 1 BLAS thread per worker) on "
+              f"{pool.cores} worker processes at once, each on its own problem of the {args.workload} recipe")
     return {"impl": "reference", "metric": _metric(), "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE.json recipe)",
             "config": {"workload": p.name, "B": p.B, "n": q.n, "m": q.m, "d": q.d, "iters_per_step": 1,
-                       "full_solve_iters": iters,
-                       "sample": "one iteration of problem 0 per step (the metric is per evaluation)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} steps x 1 iteration of {q.name} (oracle streaming form, fp64)"},
+                       "full_solve_iters": iters, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": pool.cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -665,6 +773,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        # one process per GPU: N > 1 must be launched by torchrun (WORLD_SIZE = N); never report n_gpus silently
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch N > 1 with "
+              f"`python -m torch.distributed.run --nproc-per-node {args.gpus} ... bench.py --gpus {args.gpus}`",
+              file=sys.stderr)
+        return 2
     if args.impl == "reference":
         if rank != 0:
             return 0

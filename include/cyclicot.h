@@ -61,12 +61,15 @@ typedef enum {
                               /* or cluster-resident (small problems) kernels apply                    */
 #define COT_FORCE_TMA  0x8u   /* B == 1 fp32 problems that would run cluster-resident use the persistent  */
                               /* TMA-streaming kernel instead (tests of that kernel on small shapes)     */
-#define COT_PRECOMPUTED 0x4u
+#define COT_PRECOMPUTED 0x4u  /* NEXT-1: `C` is S from cerot_precompute ([B][1][m][m], pass n = 1); the   */
+                              /* row pass uses s_ij = S_ij instead of re-streaming the n blocks          */
 #define COT_DETERMINISTIC 0x10u  /* persistent / fused path (B == 1, fp32): column sums accumulated exactly in    */
                                  /* 128-bit fixed point (2^-120) and row sums in a fixed warp order, so every   */
-                                 /* iterate is bitwise identical for any row partition (SM count, 1-8 ranks);   */
-                                 /* needs <= 8 rows per CTA (COT_E_CUDA otherwise)                              */  /* NEXT-1: `C` is S from cerot_precompute ([B][1][m][m], pass n = 1); the  */
-                              /* row pass uses s_ij = S_ij instead of re-streaming the n blocks          */
+                                 /* iterate is bitwise identical for any row partition (SM count, 1-8 ranks).   */
+                                 /* Needs <= 8 rows per CTA (COT_E_CUDA otherwise) and sum(alpha) < 2^7 (the    */
+                                 /* fixed point has 8 integer bits; cerot_state returns COT_E_ARG otherwise).   */
+                                 /* Rejected (COT_E_ARG) by the split / NCCL entry points (cerot_rows,          */
+                                 /* cerot_rows_shard, cerot_iter_sharded, cerot_solve_sharded).                 */
 /* Diagnostic flags (results are NOT valid with them; used by scripts/ubench_iter.py only):          */
 #define COT_DIAG_NO_COMPUTE 0x100u  /* TMA kernel: consumers only acknowledge slots (pure HBM stream)    */
 #define COT_DIAG_NO_SYNC    0x200u  /* TMA kernel: skip the column pass and device-wide barriers        */

@@ -342,6 +342,9 @@ int cerot_rows(const double* alpha, const void* C, const void* G, int64_t B, int
                size_t ws_bytes, int parity, void* stream) {
   int st = check_shape(B, n, m, dtype);
   if (st) return st;
+  if (flags & COT_DETERMINISTIC)
+    return arg_error("cerot_rows: COT_DETERMINISTIC is implemented by the persistent kernel only (cerot_iter, "
+                     "cerot_iter_fused); the split row pass has no fixed-point partials");
   if (!alpha || !C || !G || !eps || !w_hat || !z_hat) return arg_error("cerot_rows: NULL argument");
   Workspace ws;
   st = check_ws(workspace, ws_bytes, B, n, m, m, dtype, &ws);
@@ -390,6 +393,11 @@ int cerot_state(const void* workspace, int64_t B, int64_t m, int64_t n, int dtyp
   if (flags & STATE_UNDERFLOW) {
     set_error("a column sum fell below 1e-28 (fp32 underflow; eps too small for this cost scale)");
     return COT_E_UNDERFLOW;
+  }
+  if (flags & STATE_DET_REFUSED) {
+    set_error("COT_DETERMINISTIC needs sum(alpha) < 2^7 (128-bit fixed point with 120 fraction bits); "
+              "rescale alpha and beta");
+    return COT_E_ARG;
   }
   if (flags & STATE_PEER_TIMEOUT) {
     set_error("fused multi-GPU path: a peer rank's exchange line did not arrive within 20 s");
@@ -757,6 +765,9 @@ int cerot_rows_shard(const double* alpha, const void* C_local, const void* G_loc
                      double* w_hat, double* c_local, void* workspace, size_t ws_bytes, void* stream) {
   int st = check_shape(1, n, m, dtype);
   if (st) return st;
+  if (flags & COT_DETERMINISTIC)
+    return arg_error("cerot_rows_shard: COT_DETERMINISTIC is implemented by the persistent kernel only (cerot_iter, "
+                     "cerot_iter_fused); the split row pass has no fixed-point partials");
   if (R < 1 || row_begin < 0 || row_begin + R > m) return arg_error("cerot_rows_shard: bad row range");
   if (!alpha || !C_local || !G_local || !eps || !z_hat || !w_hat || !c_local)
     return arg_error("cerot_rows_shard: NULL argument");
@@ -792,6 +803,9 @@ int cerot_iter_sharded(const double* alpha, const double* beta, const void* C_lo
                        size_t ws_bytes, void* comm, void* stream) {
   int st = check_shape(1, n, m, dtype);
   if (st) return st;
+  if (flags & COT_DETERMINISTIC)
+    return arg_error("cerot_iter_sharded: COT_DETERMINISTIC is implemented by the persistent kernel only (cerot_iter, "
+                     "cerot_iter_fused); the split row pass has no fixed-point partials");
   if (R < 1 || row_begin < 0 || row_begin + R > m) return arg_error("cerot_iter_sharded: bad row range");
   if (!alpha || !beta || !C_local || !G_local || !eps || !w_hat || !z_hat)
     return arg_error("cerot_iter_sharded: NULL argument");
@@ -962,6 +976,9 @@ int cerot_solve_sharded(const double* alpha, const double* beta, const void* C_l
                         void* workspace, size_t ws_bytes, void* comm, cot_report* report, void* stream) {
   int st = check_shape(1, n, m, dtype);
   if (st) return st;
+  if (flags & COT_DETERMINISTIC)
+    return arg_error("cerot_solve_sharded: COT_DETERMINISTIC is implemented by the persistent kernel only (cerot_iter, "
+                     "cerot_iter_fused); the split row pass has no fixed-point partials");
   if (R < 1 || row_begin < 0 || row_begin + R > m) return arg_error("cerot_solve_sharded: bad row range");
   if (!alpha || !beta || !C_local || !eps || !w_hat || !z_hat || !report)
     return arg_error("cerot_solve_sharded: NULL argument");

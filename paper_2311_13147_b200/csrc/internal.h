@@ -18,7 +18,11 @@ struct SolverState {
   int flags;         // bit 0: marginal validation failed; bit 1: column underflow
   int pad;
 };
-enum { STATE_BAD_MARGINAL = 1, STATE_UNDERFLOW = 2, STATE_PEER_TIMEOUT = 4 };
+// STATE_DET_RANGE: set by cerot_init when sum(alpha) >= 2^7 (not an error by itself); a COT_DETERMINISTIC launch
+// on such a problem refuses to iterate and sets STATE_DET_REFUSED (cerot_state: COT_E_ARG).
+enum { STATE_BAD_MARGINAL = 1, STATE_UNDERFLOW = 2, STATE_PEER_TIMEOUT = 4, STATE_DET_RANGE = 8,
+       STATE_DET_REFUSED = 16 };
+constexpr double kDetAlphaMax = 128.0;   // 2^7: every fixed-point column partial stays below 2^8
 
 constexpr int kMaxRanks = 8;   // fused multi-GPU exchange: ranks of one row partition (one 8-GPU node)
 constexpr size_t kXchgHeader = 256;   // exchange buffer: epoch counter, then the LL lines

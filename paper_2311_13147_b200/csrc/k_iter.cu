@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(256) k_init(const double* __restrict__ alpha, 
     st.residual = INFINITY;
     st.flags = (bad > 0.0 || mism) ? STATE_BAD_MARGINAL : 0;
     st.active = st.flags ? 0 : 1;
+    if (!(sa < kDetAlphaMax)) st.flags |= STATE_DET_RANGE;
     st.pad = 0;
     state[b] = st;
     counters[b] = 0u;

@@ -73,6 +73,16 @@ struct TmaParams {
 __device__ __forceinline__ void cbar(int nthreads) {   // consumer-only named barrier
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
+// OR of a predicate over the `nthreads` threads of named barrier 1 (a barrier itself: every epilogue thread calls it)
+__device__ __forceinline__ bool bar_red_or(bool v, int nthreads) {
+  unsigned r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.or.pred q, 1, %2, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((unsigned)v), "r"(nthreads)
+      : "memory");
+  return r != 0;
+}
 __device__ __forceinline__ unsigned lds_volatile(const unsigned* p) { return *(volatile const unsigned*)p; }
 __device__ __forceinline__ unsigned lds_acquire(const unsigned* p) {
   unsigned v;
@@ -195,10 +205,12 @@ __device__ __forceinline__ void fx_add(unsigned long long& lo, unsigned long lon
 __device__ __forceinline__ void fx_acc(double x, unsigned long long& lo, unsigned long long& hi) {   // += x 2^120
   if (!(x > 0.0)) return;
   const unsigned long long b = (unsigned long long)__double_as_longlong(x);
-  const int e = (int)(b >> 52) - 1075 + 120;   // x 2^120 = mant 2^e (x < 2^8 here: e <= 75)
+  const int e = (int)(b >> 52) - 1075 + 120;   // x 2^120 = mant 2^e (x < 2^8 is guaranteed: e <= 75)
   const unsigned long long mant = (b & 0xFFFFFFFFFFFFFull) | (1ull << 52);
   unsigned long long l = 0, h = 0;
-  if (e >= 64) {
+  if (e > 75) {   // unreachable (sum(alpha) < 2^7 is checked before the launch iterates): saturate, no UB
+    l = h = ~0ull;
+  } else if (e >= 64) {
     h = mant << (e - 64);
   } else if (e > 0) {
     l = mant << e;
@@ -324,7 +336,11 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
   }
   __syncthreads();
 
-  const bool active0 = p.state[0].active != 0;
+  // deterministic mode: the 128-bit fixed point (8 integer bits) holds every column partial only if
+  // sum(alpha) < 2^7 (cerot_init flags larger masses); such a launch refuses to iterate (COT_E_ARG)
+  const bool det_refused = p.det && (p.state[0].flags & STATE_DET_RANGE);
+  const bool active0 = p.state[0].active != 0 && !det_refused;
+  if (det_refused && bid == 0 && threadIdx.x == 0) atomicOr(&p.state[0].flags, (int)STATE_DET_REFUSED);
 
   if (warp == wprod) {
     // ===================================================================== producer (one lane)
@@ -617,7 +633,10 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         if (need_resid(t - 1)) st.residual = read_resid(g) * (double)n;
         if (p.trace) c_wait += clock64() - tw0;
         // a CTA that gave up waiting halts (its peers then time out on its lines and halt too); no global read
-        // of the state flags on the per-iteration critical path
+        // of the state flags on the per-iteration critical path. `timeout` is per thread (only the threads whose
+        // lines went missing see it): OR it over the epilogue warps first, so the whole CTA takes the same exit
+        // (the named barriers and the queue's mbarrier phases stay matched).
+        timeout = bar_red_or(timeout, net);
         if (timeout) halted = true;
         if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
           st.active = 0;

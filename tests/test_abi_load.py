@@ -80,3 +80,13 @@ def test_expand_path_query(L):
     assert L.cot_expand_path(16, 128, cot.COT_F32) == 2
     assert L.cot_expand_path(4, 130, cot.COT_F32) == 0
     assert L.cot_expand_path(0, 4, cot.COT_F32) == -1
+
+
+def test_deterministic_flag_rejected_by_split_entry_points(L):
+    """COT_DETERMINISTIC on the rows-only / NCCL entry points is an argument error before any device work."""
+    det = cot.COT_DETERMINISTIC
+    assert L.cerot_rows(None, None, None, 1, 4, 16, 0, None, det, None, None, None, 0, 0, None) == -1
+    assert b"COT_DETERMINISTIC" in L.cot_last_error()
+    assert L.cerot_iter_sharded(None, None, None, None, 4, 16, 0, 8, 0, None, 1, 0.0, 1, det, None, None, None, 0,
+                                None, None) == -1
+    assert b"COT_DETERMINISTIC" in L.cot_last_error()

@@ -38,3 +38,36 @@ def test_reference_arm_under_torchrun_two_ranks():
     lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
     assert len(lines) == 1
     assert json.loads(lines[0])["impl"] == "reference"
+
+
+def test_reference_arm_uses_all_host_cores():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1", "--workload", "C2"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.strip()][0])
+    assert d["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
+    assert d["cpu_baseline"]["cpu_model"]
+
+
+def test_gpus_flag_must_match_world_size():
+    """`--gpus N` without torchrun (WORLD_SIZE unset) must fail loudly instead of reporting n_gpus = 1."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                         capture_output=True, text=True, timeout=300, env={**os.environ, "WORLD_SIZE": "1"})
+    assert out.returncode == 2
+    assert "WORLD_SIZE" in out.stderr and not out.stdout.strip()
+
+
+def test_cpu_baseline_per_core_all_core_and_kernel_form():
+    """The cpu_baseline leg of our arm: all cores, per-core and all-core rates of the streaming
+    oracle, Alg. 2's precomputed-K form beside it, the CPU model (short sample for the test)."""
+    sys.path.insert(0, ROOT)
+    os.environ["COT_CPU_BASELINE_SECONDS"] = "0.5"
+    try:
+        import bench
+        import synthetic
+        cb = bench.cpu_baseline(synthetic.c2_sweep(), None, "C2")
+    finally:
+        del os.environ["COT_CPU_BASELINE_SECONDS"]
+    assert cb["kind"] == "oracle" and cb["cores"] == len(os.sched_getaffinity(0))
+    assert cb["per_core"] > 0 and cb["all_core"] > 0 and cb["value"] == cb["all_core"]
+    assert cb["kernel_form"]["value"] > 0 and cb["cpu_model"]

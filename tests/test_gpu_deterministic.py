@@ -96,3 +96,37 @@ def test_bitwise_identical_across_partitions(maker):
     assert abs(rg["objective"] - ro["objective"]) <= 1e-6 * abs(ro["objective"])
     assert abs(rg["dual"] - ro["dual"]) <= 1e-6 * abs(ro["dual"])
     assert abs(rg["row_l1"] - ro["row_l1"]) <= 1e-5
+
+
+def test_fixed_point_range_is_enforced():
+    """The 128-bit fixed point has 8 integer bits: a problem with sum(alpha) >= 2^7 (un-normalised masses) is
+    refused by the deterministic launch (COT_E_ARG at the state check), not silently wrapped; the same problem
+    runs in the default mode and matches the oracle (the solver itself is scale-agnostic)."""
+    p = synthetic.c4_large(m=256, n=8)
+    scale = 200.0 * p.n            # sum(alpha) = 200
+    a, b = p.alpha * scale, p.beta * scale
+    prob = cot.CerotProblem(_dev(p.C), _dev(a), _dev(b), _dev(p.eps)).init()
+    prob.iterate(5, flags=DET)
+    with pytest.raises(cot.CotError) as e:
+        prob.state()
+    assert e.value.code == -1 and "2^7" in str(e.value)
+    prob2 = cot.CerotProblem(_dev(p.C), _dev(a), _dev(b), _dev(p.eps)).init()
+    prob2.iterate(5)
+    it, _, _ = prob2.state()
+    assert it[0] == 5
+    eps = float(p.eps[0])
+    wo, zo, _, _ = oracle.cyclic_sinkhorn(a, b, p.C, eps, 5, form="kernel")
+    w, z = prob2.w_hat.cpu().numpy(), prob2.z_hat.cpu().numpy()
+    rg = oracle.report(w * eps, z * eps, a, b, p.C, eps)
+    ro = oracle.report(wo, zo, a, b, p.C, eps)
+    assert abs(rg["objective"] - ro["objective"]) <= 1e-6 * abs(ro["objective"])
+
+
+def test_split_entry_points_reject_deterministic():
+    """cerot_rows / the NCCL sharded path have no fixed-point partials: COT_DETERMINISTIC is an argument error
+    with an explicit message (not an opaque CUDA 'invalid argument')."""
+    p = synthetic.c4_large(m=256, n=8)
+    sh = cdist.ShardedCerot(_dev(p.C), _dev(p.alpha), _dev(p.beta), float(p.eps[0]), 0, p.m).init()
+    with pytest.raises(cot.CotError) as e:
+        sh.iterate(2, flags=DET)
+    assert e.value.code == -1 and "COT_DETERMINISTIC" in str(e.value)
