@@ -173,7 +173,7 @@ class Runner:
         # which iteration kernel the library runs: 1 = persistent TMA stream (all iterations in one launch),
         # 2 = cluster-resident (all iterations in one launch, whole problems on chip), 0 = launch pair / iteration
         self.path = int(self.L.cot_iter_path(self.B, 1 if self.pre else self.n, self.m, self.dt, self.flags))
-        self.persistent = self.path in (1, 2)
+        self.persistent = self.path in (1, 2, 3)
         self.launches_per_step = 1 + 1 + (1 if self.persistent else 2 * iters) + 3 + 1 + (1 if self.pre else 0)
         self.bytes_iter = float(p.B) * ((2 if self.pre else p.n + 1) * p.m * p.m) * p.C.itemsize
 
@@ -464,7 +464,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
     dom_share = it_mean / ms_step
     clocks = clk.summary()
-    cluster = getattr(R, "path", None) == 2
+    cluster = getattr(R, "path", None) in (2, 3)
     if cluster:   # whole problems on chip: the bound is the SFU (one MUFU.EX2 per Gibbs evaluation), DESIGN.md §6
         ex2_launch = float(B_local_evals(p, iters))
         achieved_sfu = ex2_launch / (per_launch_ms / 1e3)
@@ -477,7 +477,8 @@ def run_ours(args, rank, world, local_rank):
                   (f" [{R.fused_note}]" if R.fused_note else ""))
     else:
         kernel = {1: "k_iter_tma (persistent: all iterations in one launch)",
-                  2: "k_batch_cluster (one thread-block cluster per problem: 8 CTAs while the batch fits one wave, else 6; all iterations in one launch, on chip)"}.get(
+                  2: "k_batch_cluster (one thread-block cluster per problem: 8 CTAs while the batch fits one wave, else 6; all iterations in one launch, on chip)",
+                  3: "k_batch_chain (one thread-block cluster per problem, 8 CTAs while the batch fits one wave, else 6: one CTA runs the iteration chain, the others evaluate the n*m^2 Gibbs terms every iteration into its shared memory; all iterations in one launch, on chip)"}.get(
                       getattr(R, "path", 0), "k_rows_ldg + k_cols (one launch pair per iteration)")
     trf = _ncu_traffic_per_iter(args.workload) if world == 1 else None
     metric = _metric()

@@ -162,7 +162,10 @@ int cerot_iter(const double* alpha, const double* beta, const void* C, const voi
 /* Which kernel cerot_iter / cerot_solve run for this shape (no device work): 0 = generic row/column      */
 /* kernels (k_rows_ldg + k_cols, one launch pair per iteration), 1 = the persistent TMA-streaming kernel  */
 /* (k_iter_tma: B == 1, fp32, m % 4 == 0, m <= 1024; HBM-bound), 2 = the cluster-resident kernel          */
-/* (k_batch_cluster: fp32, m % 4 == 0, 8 <= m <= 256; whole problem on chip, SFU-bound); -1: bad shape.   */
+/* (k_batch_cluster: fp32, m % 4 == 0, 8 <= m <= 256; whole problem on chip, SFU-bound), 3 = the          */
+/* cluster-resident chain kernel (k_batch_chain: fp32, m % 4 == 0, m <= 128; one CTA per cluster runs the  */
+/* iteration chain, the others stream the Gibbs terms; COT_BATCH_CHAIN=0 in the environment disables it);  */
+/* -1: bad shape.                                                                                          */
 int cot_iter_path(int64_t B, int64_t n, int64_t m, int dtype, uint32_t flags);
 /* The two halves of one cerot_iter iteration, for callers that interleave work between them (the
  * row-sharded multi-GPU path reduces the column sums across ranks in between; bench.py times the row

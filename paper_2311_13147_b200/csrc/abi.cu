@@ -81,6 +81,7 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, i
   w.c_global = reinterpret_cast<double*>(take((size_t)(B * m) * 8));
   w.plan_buf = reinterpret_cast<double*>(take((size_t)(B * (kPlanBufHead + m)) * 8));
   w.rowscal = reinterpret_cast<double*>(take((size_t)(B * m * 4) * 8));
+  w.zcache = reinterpret_cast<double*>(take((size_t)(B * m * 3) * 8));
   w.A = reinterpret_cast<int32_t*>(take((size_t)(B * R * m) * 4));
   w.G = take((size_t)(B * R * m) * esz);
   if (ws) *ws = w;
@@ -332,6 +333,7 @@ int cot_iter_path(int64_t B, int64_t n, int64_t m, int dtype, uint32_t flags) {
   if (B < 1 || n < 1 || m < 1) return -1;
   const IterArgs a = make_args(nullptr, nullptr, nullptr, nullptr, B, n, m, dtype, nullptr, 0.0, 1, flags, nullptr,
                                nullptr);
+  if (batch_chain_eligible(a)) return 3;
   if (batch_cluster_eligible(a)) return 2;
   if (tma_eligible(a)) return 1;
   return 0;

@@ -55,6 +55,7 @@ struct Workspace {
   double* c_global;        // [B][m] column sums after the cross-GPU reduction
   double* plan_buf;        // [B][kPlanBufHead + m] local plan reductions (allreduced in place)
   double* rowscal;         // [B][m][4] per-row plan scalars of the C-SROT report
+  double* zcache;          // [B][m][3] k_batch_chain: z_hat as written, and its split (Fz, kz) kept across launches
   // LL-line region of the persistent kernel (B == 1 only; zeroed by cerot_init; offsets depend on B, m and
   // the SM count only, so cerot_init finds it without n, R or the dtype)
   void* ll_base;
@@ -108,6 +109,10 @@ cudaError_t launch_cols(const IterArgs& a, const Workspace& ws, const UnitPlan& 
 bool tma_eligible(const IterArgs& a, int sms = 0);   // sms: SMs the launch may use (0: all)
 // Cluster-resident small problems (fp32, m <= 256, m % 4 == 0): `iters` full iterations of every problem.
 bool batch_cluster_eligible(const IterArgs& a);
+// m <= 128: one CTA of each cluster runs the whole iteration chain, the others stream the Gibbs terms
+// (k_batch_chain.cu); launch_batch_cluster dispatches to it when eligible.
+bool batch_chain_eligible(const IterArgs& a);
+cudaError_t launch_batch_chain(const IterArgs& a, const Workspace& ws, int iters, cudaStream_t s);
 cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int iters, cudaStream_t s);
 // Persistent TMA kernel: `iters` full iterations (cooperative launch), or the row pass of one iteration
 // into ws.partials[parity] when rows_only.

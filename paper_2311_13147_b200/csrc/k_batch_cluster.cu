@@ -854,6 +854,7 @@ static bool batch_config(int64_t n, int64_t m, int64_t B, BatchCfg* out) {
 }
 
 bool batch_cluster_eligible(const IterArgs& a) {
+  if (batch_chain_eligible(a)) return true;
   if (a.dtype != COT_F32 || a.m % 4 != 0 || a.m > 256 || a.R != a.m || (a.flags & (COT_FORCE_LDG | COT_FORCE_TMA)))
     return false;
   BatchCfg c;
@@ -861,6 +862,7 @@ bool batch_cluster_eligible(const IterArgs& a) {
 }
 
 cudaError_t launch_batch_cluster(const IterArgs& a, const Workspace& ws, int iters, cudaStream_t s) {
+  if (batch_chain_eligible(a)) return launch_batch_chain(a, ws, iters, s);
   BatchCfg bc;
   if (!batch_config(a.n, a.m, a.B, &bc)) return cudaErrorInvalidConfiguration;
   BatchParams p;

@@ -172,7 +172,7 @@ def test_c1_solve_api():
 
 
 _PATH_FLAGS = {"cluster": 0, "tma": 0x8, "ldg": 0x2}   # default (cluster-resident), COT_FORCE_TMA, COT_FORCE_LDG
-_PATH_CODE = {"cluster": 2, "tma": 1, "ldg": 0}
+_PATH_CODE = {"cluster": 3, "tma": 1, "ldg": 0}        # 3: k_batch_chain (m <= 128)
 
 
 @pytest.mark.parametrize("eps_factor", [1e-1, 1e-2, 1e-3])
@@ -417,19 +417,44 @@ def test_tma_kernel_shapes(n, m, R_seed):
     assert it[0] == 25
 
 
+class _env:
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        import os
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update({k: str(v) for k, v in self.kv.items()})
+
+    def __exit__(self, *a):
+        import os
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("kernel", ["chain", "cluster"])
 @pytest.mark.parametrize("n,m,B", [(1, 8, 1), (3, 12, 1), (5, 36, 2), (17, 128, 1), (16, 128, 20), (4, 132, 1),
-                                   (7, 132, 20), (2, 256, 3)])
-def test_cluster_kernel_shapes(n, m, B):
-    """The cluster-resident kernel on ragged shapes, in each of its schedules: B within one wave of 8-CTA clusters
-    (warp-specialised for m <= 128, interleaved beyond), B = 20 (the 6-CTA throughput shape where it fits);
-    n = 1 and n not a multiple of 4, rows per CTA not a multiple of the warp count. 30 iterations in two
-    launches, every problem against the oracle."""
+                                   (7, 132, 20), (2, 256, 3), (16, 128, 40), (8, 124, 3)])
+def test_cluster_kernel_shapes(kernel, n, m, B):
+    """The cluster-resident kernels on ragged shapes, in each of their schedules. kernel = "chain": k_batch_chain
+    (m <= 128; one CTA runs the iteration chain, the others stream the Gibbs terms), 8-CTA clusters while B fits
+    one wave, 6-CTA clusters beyond (B = 20, 40: several waves); kernel = "cluster": k_batch_cluster
+    (COT_BATCH_CHAIN=0, and m > 128), warp-specialised for m <= 128, interleaved beyond. n = 1 and n not a
+    multiple of 4, rows not a multiple of the warp count. 30 iterations in two launches, every problem against
+    the oracle."""
+    if kernel == "chain" and m > 128:
+        pytest.skip("k_batch_chain holds the m x m problem in one CTA: m <= 128")
+    env = {"COT_BATCH_CHAIN": "0"} if kernel == "cluster" else {}
     p = synthetic.random_cyclic(seed=7 * n + m, n=n, m=m, dtype=np.float32, eps=0.05, B=B)
-    prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps)).init()
-    assert cot.lib().cot_iter_path(B, n, m, 0, 0) == 2   # the cluster-resident kernel
-    prob.iterate(18)
-    prob.iterate(12)
-    T, rep = prob.plan(T_blocks=True)
+    with _env(**env):
+        prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps)).init()
+        assert cot.lib().cot_iter_path(B, n, m, 0, 0) == (3 if kernel == "chain" else 2)
+        prob.iterate(18)
+        prob.iterate(12)
+        T, rep = prob.plan(T_blocks=True)
     T, rep = T.cpu().numpy(), rep.cpu().numpy()
     it, _, _ = prob.state()
     assert (np.asarray(it) == 30).all()
@@ -437,3 +462,19 @@ def test_cluster_kernel_shapes(n, m, B):
         pb = synthetic.Problem("b", p.C[b], p.alpha[b], p.beta[b], p.eps[b:b + 1], iters=0, tol=0.0, meta={})
         w, z, _, _ = oracle.cyclic_sinkhorn(pb.alpha, pb.beta, pb.C, 0.05, 30, form="kernel")
         _compare(pb, rep[b], T[b], w, z)
+
+
+def test_chain_kernel_launch_boundaries_bitwise():
+    """k_batch_chain carries nothing across launches but z_hat (the row shift is the exact maximum every
+    iteration): 30 iterations in one launch and in launches of 7 + 11 + 12 give bitwise identical potentials."""
+    p = synthetic.c5_batched(B=30, first=200)
+    out = []
+    for split in ([30], [7, 11, 12]):
+        prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps)).init()
+        for k in split:
+            prob.iterate(k)
+        torch.cuda.synchronize()
+        out.append((prob.w_hat.cpu().numpy(), prob.z_hat.cpu().numpy()))
+    assert cot.lib().cot_iter_path(30, p.n, p.m, 0, 0) == 3
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
