@@ -70,8 +70,11 @@ __device__ __forceinline__ void st_async_f4(uint32_t addr, float4 v, uint32_t re
 __device__ __forceinline__ void st_cluster_release_u32(uint32_t addr, unsigned v) {
   asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t remote_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+// Remote arrival without a release fence (a release at cluster scope compiles to MEMBAR.ALL.GPU): used only to
+// hand a buffer back to its writers after every read of it has completed (the values were consumed before a
+// CTA barrier), so nothing needs ordering.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
 }
 __device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -84,13 +87,14 @@ __device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, uint32_t parity
   return ok != 0;
 }
 
-// f * 2^e for f = s'_ij in [2^-1/2, 1.42 n] (fp32) and e <= 0 (the exact row shift makes every exponent <= 0),
-// exactly, with e clamped below at -1000 (terms < 2^-999 come out ~1e-301: negligible); integer operations only
-// (ldexp_pos without the upper clamp).
-__device__ __forceinline__ double ldexp_nonpos(float f, int e) {
+// f * 2^(eb - 896) for f = s'_ij in [2^-1/2, 1.42 n] (fp32) and a biased exponent eb = e + 896 with e <= 0 (the
+// exact row shift makes every exponent <= 0), exactly, with e clamped below at -1000 (terms < 2^-999 come out
+// ~1e-301: negligible); integer operations only. The bias (fp64 1023 - fp32 127) is carried in the column
+// exponents kz_j + 896, so no per-element add is needed for it.
+__device__ __forceinline__ double ldexp_biased(float f, int eb) {
   const unsigned bits = __float_as_uint(f);
-  e = max(e, -1000);
-  return __hiloint2double((int)((bits >> 3) + 0x38000000u + ((unsigned)e << 20)), (int)(bits << 29));
+  eb = max(eb, 896 - 1000);
+  return __hiloint2double((int)((bits >> 3) + ((unsigned)eb << 20)), (int)(bits << 29));
 }
 
 // The chain CTA: every iteration of the problem on s' from the producers (FULL: m == 128, no masking).
@@ -106,7 +110,7 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
   double* bcol = zf + m;                                               // [m] beta_j
   double* rstat = bcol + m;                                            // [m][2] kM_i ln2, r_i
   double* red = rstat + 2 * m;                                         // [32]
-  int* zk = reinterpret_cast<int*>(red + 32);                          // [m] kz_j
+  int* zk = reinterpret_cast<int*>(red + 32);                          // [m] kz_j + 896 (biased: see ldexp_biased)
   for (int idx = threadIdx.x; idx < m * m; idx += kChainThreads)
     As[idx] = __float2int_rn(__ldg(p.G + (size_t)b * m * m + idx) * c2);
   // z_hat_j log2e = kz_j + log2 Fz_j: the split this kernel left in the workspace when z_hat still holds exactly
@@ -120,11 +124,11 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     if (__double_as_longlong(z) == __double_as_longlong(zc[3 * j]) && cf >= 0.7071067811865475 &&
         cf <= 1.4142135623730951 && fabs(ck - rint(z * COT_LOG2E)) <= 1.0) {
       zf[j] = cf;
-      zk[j] = (int)ck;
+      zk[j] = (int)ck + 896;
     } else {
       int kz;
       zf[j] = split_pow2_fp64(z * COT_LOG2E, kz);
-      zk[j] = kz;
+      zk[j] = kz + 896;
     }
     bcol[j] = p.beta[b * m + j];
   }
@@ -166,14 +170,15 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
       const int ic = FULL || i < m ? i : 0;
       const float4 s4 = reinterpret_cast<const float4*>(sq + (size_t)ic * m)[jc];
       const int4 a4 = reinterpret_cast<const int4*>(As + (size_t)ic * m)[jc];
-      const int ex[4] = {k4.x - a4.x, k4.y - a4.y, k4.z - a4.z, k4.w - a4.w};
+      const int ex[4] = {k4.x - a4.x, k4.y - a4.y, k4.z - a4.z, k4.w - a4.w};   // kz_j + 896 - a_ij
       const int em = max(max(ex[0], ex[1]), max(ex[2], ex[3]));
-      kM[k] = __reduce_max_sync(0xffffffffu, ok ? em : -0x7fffffff);   // exact row shift: largest term >= 1/2
+      // exact row shift kM_i = max_j (kz_j - a_ij): the largest term is >= 1/2
+      kM[k] = __reduce_max_sync(0xffffffffu, ok ? em : -0x7fffffff) - 896;
       const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
       ls[k] = 0.0;
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        uu[k][v] = ldexp_nonpos(sv[v], ex[v] - kM[k]);
+        uu[k][v] = ldexp_biased(sv[v], ex[v] - kM[k]);
         if (!FULL && !ok) uu[k][v] = 0.0;
         ls[k] = fma(uu[k][v], fz[v], ls[k]);
       }
@@ -214,7 +219,7 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     __syncthreads();
     const long long c2t = p.trace ? clock64() : 0;
     // s' buffer q has been read: the producers may fill it with iteration t + 2
-    if (threadIdx.x < NP) mbar_arrive_cluster(mapa_u32(smem_u32(&bars[2 + q]), (uint32_t)threadIdx.x + 1));
+    if (threadIdx.x < NP) mbar_arrive_cluster_relaxed(mapa_u32(smem_u32(&bars[2 + q]), (uint32_t)threadIdx.x + 1));
     // ---- column pass: 4 threads per column (4 warps' partials each, then a fixed xor tree) and the q-update
     //      z_hat_j += log beta_j - log c_j carried on the split: Fz_j beta_j / c_j = M 2^E, M in [2^-1/2, 2^1/2)
     //      -> kz_j += E, Fz_j = M (no log, no exp on the critical path)
@@ -279,11 +284,12 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
   for (int i = threadIdx.x; i < m; i += kChainThreads)
     if (t > 0) p.w_hat[b * m + i] = log(p.alpha[b * m + i]) - rstat[2 * i] - log(rstat[2 * i + 1]);
   for (int j = threadIdx.x; j < m; j += kChainThreads) {   // z_hat_j = (kz_j + log2 Fz_j) ln 2, and its split
-    const double z = (double)zk[j] * COT_LN2 + log(zf[j]);
+    const int kz = zk[j] - 896;
+    const double z = (double)kz * COT_LN2 + log(zf[j]);
     p.z_hat[b * m + j] = z;
     zc[3 * j] = z;
     zc[3 * j + 1] = zf[j];
-    zc[3 * j + 2] = (double)zk[j];
+    zc[3 * j + 2] = (double)kz;
   }
   if (underflow) atomicOr(&p.state[b].flags, (int)STATE_UNDERFLOW);
   if (threadIdx.x == 0) {
