@@ -52,6 +52,8 @@ struct ChainParams {
   double tol;
   long long check_every;
   int pre;
+  int diag;              // diagnostics only (COT_CHAIN_DIAG=2): the chain skips its passes and hands every buffer
+                         // straight back (timing of the producers and the DSMEM delivery alone; results invalid)
   unsigned long long* trace;   // diagnostics (COT_TRACE=1): [grid][8] cycle counters, or nullptr
 };
 
@@ -154,6 +156,11 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     // the free signal below)
     if (threadIdx.x == 0 && t + 2 < p.iters) mbar_arrive_expect_tx(&bars[q], (uint32_t)(m * m * 4));
     const long long c1t = p.trace ? clock64() : 0;
+    if (p.diag & 2) {   // diagnostics: producers alone
+      if (threadIdx.x < NP) mbar_arrive_cluster_relaxed(mapa_u32(smem_u32(&bars[2 + q]), (uint32_t)threadIdx.x + 1));
+      st.iters += 1;
+      continue;
+    }
     // ---- r-pass: the warp's 8 rows, one float4 of columns per lane:
     //      u_ij = s'_ij 2^{kz_j - a_ij - kM_i},  r_i = sum_j u_ij Fz_j,  P_j = Fz_j sum_i rho_i u_ij
     const int4 k4 = reinterpret_cast<const int4*>(zk)[jc];
@@ -195,7 +202,7 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     double r = (h2 ? a2s[1] : a2s[0]) + __shfl_xor_sync(0xffffffffu, h2 ? a2s[0] : a2s[1], 4);
     r += __shfl_xor_sync(0xffffffffu, r, 2);
     r += __shfl_xor_sync(0xffffffffu, r, 1);
-    const double rho_my = my_valid ? my_alpha * rcp_nomufu(r) : 0.0;   // alpha_i / r_i (no MUFU)
+    const double rho_my = my_valid ? my_alpha * __drcp_rn(r) : 0.0;   // alpha_i / r_i (this SM's MUFU is idle)
     if (need && (lane & 3) == 0 && my_valid) {   // the row statistics of w_hat (kept for the last iteration)
       int km = 0;
 #pragma unroll
@@ -237,7 +244,7 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
       const double bj = bcol[col];
       dev = fabs(c - bj);
       underflow |= !(c >= 1e-28);
-      const double R = (zf[col] * bj) * rcp_nomufu(c);
+      const double R = (zf[col] * bj) * __drcp_rn(c);
       const int hi = __double2hiint(R);
       int E = (hi >> 20) - 1023;
       double M = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, __double2loint(R));   // [1, 2)
@@ -561,6 +568,7 @@ cudaError_t launch_batch_chain(const IterArgs& a, const Workspace& ws, int iters
   p.tol = a.tol;
   p.check_every = a.check_every > 0 ? a.check_every : 1;
   p.pre = (a.flags & COT_PRECOMPUTED) ? 1 : 0;
+  p.diag = getenv("COT_CHAIN_DIAG") ? (atoi(getenv("COT_CHAIN_DIAG")) & 2) : 0;
   cudaError_t e = cudaFuncSetAttribute((void*)k_batch_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)cc.smem);
   if (e != cudaSuccess) return e;
