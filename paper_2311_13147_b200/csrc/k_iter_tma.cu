@@ -60,6 +60,8 @@ struct TmaParams {
   int evict_last_rows;   // rows [0, evict_last_rows) of every block are streamed with an L2 evict_last hint
   int diag;              // COT_DIAG_* bits (diagnostics only)
   int pre;               // precomputed mode (NEXT-1): C is S [R][m] (n = 1) and s_ij = S_ij
+  int kres;              // k-blocks [0, kres) of the CTA's rows are resident in shared memory (loaded once per
+                         // launch); only [kres, n) is streamed through the ring every iteration
   int rpw;               // row-per-warp epilogue (several rows per CTA, EPT == 1): no block reduction per row
   int det;               // deterministic mode: 128-bit fixed-point column partials (implies rpw); 2 lines per value
   unsigned long long* trace;   // diagnostics: [grid][8] cycle counters, or nullptr
@@ -275,6 +277,45 @@ __device__ __forceinline__ void cblk_maxN(double* v, double* red2, int& buf, int
   buf ^= 1;
 }
 
+// k-sum of four consecutive k-rows at `b` (row stride mv float4s): all loads first, then the 16 x CPT independent
+// FFMA + MUFU.EX2 back to back, then a fixed pairwise sum per element (in-order issue would otherwise stall on
+// each MUFU result before the next k-row's work)
+template <int CPT>
+__device__ __forceinline__ void ksum4(const float4* __restrict__ b, int mv, int nkt, int kt, const float c2,
+                                      const float (&gc)[CPT][4], float (&s)[CPT][4]) {
+  float4 c[4][CPT];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) c[kk][q] = b[(size_t)kk * mv + q * nkt + kt];
+  float e[4][CPT][4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      e[kk][q][0] = ex2(fmaf(-c[kk][q].x, c2, gc[q][0]));
+      e[kk][q][1] = ex2(fmaf(-c[kk][q].y, c2, gc[q][1]));
+      e[kk][q][2] = ex2(fmaf(-c[kk][q].z, c2, gc[q][2]));
+      e[kk][q][3] = ex2(fmaf(-c[kk][q].w, c2, gc[q][3]));
+    }
+#pragma unroll
+  for (int q = 0; q < CPT; ++q)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) s[q][v] += (e[0][q][v] + e[1][q][v]) + (e[2][q][v] + e[3][q][v]);
+}
+template <int CPT>
+__device__ __forceinline__ void ksum1(const float4* __restrict__ b, int nkt, int kt, const float c2,
+                                      const float (&gc)[CPT][4], float (&s)[CPT][4]) {
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    const float4 c = b[q * nkt + kt];
+    s[q][0] += ex2(fmaf(-c.x, c2, gc[q][0]));
+    s[q][1] += ex2(fmaf(-c.y, c2, gc[q][1]));
+    s[q][2] += ex2(fmaf(-c.z, c2, gc[q][2]));
+    s[q][3] += ex2(fmaf(-c.w, c2, gc[q][3]));
+  }
+}
+
 template <int CPT, int EPT, int KS>
 __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid, const int nblk) {
   constexpr int VEC = 4;
@@ -292,7 +333,9 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
   const size_t slot_floats = (size_t)KS * m;
   // ---- shared memory layout
   float* ring = reinterpret_cast<float*>(smem);
-  float* queue = reinterpret_cast<float*>(smem + (size_t)p.nslot * slot_floats * 4 + 1024);   // [QN][m]
+  // resident k-blocks [rpu][kres][m] after the ring and its 1 KiB over-read pad
+  float* resid = reinterpret_cast<float*>(smem + (size_t)p.nslot * slot_floats * 4 + 1024);
+  float* queue = resid + (size_t)rpu * p.kres * m;                                          // [QN][m]
   int* gsh = reinterpret_cast<int*>(queue + (size_t)QN * m);            // [rpu][m] a_ij = round(G_ij log2e/eps)
   double* rowstat = reinterpret_cast<double*>(gsh + (size_t)rpu * m);    // [rpu][RS] (rpu * m even: m % 4 == 0)
   double* xs = rowstat + (size_t)rpu * RS;                               // [kColScratch] column-pass scratch
@@ -305,7 +348,8 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
   uint64_t* empty = full + p.nslot;
   uint64_t* qfull = empty + p.nslot;
   uint64_t* qempty = qfull + QN;
-  unsigned* ctl = reinterpret_cast<unsigned*>(qempty + QN);
+  uint64_t* resbar = qempty + QN;                                        // the resident k-blocks have landed
+  unsigned* ctl = reinterpret_cast<unsigned*>(resbar + 2);
   // ctl: [0] TMA slots issued [1] producer done [2] stop producer [5] halt
   //      [6] rows produced by the k-sum warps [7] k-sum warps done [8] k-sum broadcast
   double* red2 = reinterpret_cast<double*>(ctl + 16);   // [2][64]
@@ -321,6 +365,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       mbar_init(&qfull[q], nk);
       mbar_init(&qempty[q], p.rpw ? 1 : ne);   // row-per-warp: one warp consumes a row
     }
+    mbar_init(resbar, 1);
     for (int c = 0; c < 16; ++c) ctl[c] = 0;
     fence_mbar_init();
   }
@@ -347,6 +392,14 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
     if (lane == 0 && active0) {
       const uint64_t pol_first = policy_evict_first();
       const uint64_t pol_last = policy_evict_last();
+      if (p.kres > 0 && nrows > 0) {   // the resident k-blocks of every row of the unit, once per launch
+        const uint32_t rb = (uint32_t)m * 4u;
+        mbar_arrive_expect_tx(resbar, (uint32_t)nrows * (uint32_t)p.kres * rb);
+        for (int i = i0; i < i1; ++i)
+          for (int k = 0; k < p.kres; ++k)
+            bulk_g2s(resid + ((size_t)(i - i0) * p.kres + k) * m, p.C + ((size_t)k * R + i) * m, rb, resbar,
+                     pol_first);
+      }
       uint32_t slot = 0, phase = 0;
       unsigned issued = 0;
       long long prod_wait = 0;
@@ -355,7 +408,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       for (int t = 0; t < p.iters; ++t) {
         for (int i = i0; i < i1; ++i) {
           const uint64_t pol = i < p.evict_last_rows ? pol_last : pol_first;
-          for (int k0 = 0; k0 < n; k0 += KS) {
+          for (int k0 = p.kres; k0 < n; k0 += KS) {
             if (lds_volatile(&ctl[2])) goto producer_done;
             const int kk = min(KS, n - k0);
             const long long tw0 = p.trace ? clock64() : 0;
@@ -442,7 +495,16 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       }
       load_g(r + 1 < nrows ? i0 + r + 1 : i0);
       const long long tk0 = p.trace ? clock64() : 0;
-      int k0 = 0;
+      int k0 = p.kres;
+      if (p.kres > 0) {   // the resident k-blocks of the row, straight from shared memory (k ascending, as streamed)
+        if (rr == 0) mbar_wait(resbar, 0);
+        const VT* rb = reinterpret_cast<const VT*>(resid + (size_t)r * p.kres * m);
+        if (!(p.diag & COT_DIAG_NO_COMPUTE)) {
+          int k = 0;
+          for (; k + 4 <= p.kres; k += 4) ksum4<CPT>(rb + (size_t)k * mv, mv, nkt, kt, c2, gc, s);
+          for (; k < p.kres; ++k) ksum1<CPT>(rb + (size_t)k * mv, nkt, kt, c2, gc, s);
+        }
+      }
       for (; k0 + KS <= n; k0 += KS) {
         mbar_wait(&full[slot], phase);
         const VT* sb = reinterpret_cast<const VT*>(ring + (size_t)slot * slot_floats);
@@ -456,16 +518,12 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
             s[q][3] = c.w * pf[q][3];
           }
         } else if (!(p.diag & COT_DIAG_NO_COMPUTE)) {
+          if (KS >= 4) {
 #pragma unroll
-          for (int q2 = 0; q2 < KS; ++q2) {
+            for (int q2 = 0; q2 < KS; q2 += 4) ksum4<CPT>(sb + (size_t)q2 * mv, mv, nkt, kt, c2, gc, s);
+          } else {
 #pragma unroll
-            for (int q = 0; q < CPT; ++q) {
-              const float4 c = sb[q2 * mv + q * nkt + kt];
-              s[q][0] += ex2(fmaf(-c.x, c2, gc[q][0]));
-              s[q][1] += ex2(fmaf(-c.y, c2, gc[q][1]));
-              s[q][2] += ex2(fmaf(-c.z, c2, gc[q][2]));
-              s[q][3] += ex2(fmaf(-c.w, c2, gc[q][3]));
-            }
+            for (int q2 = 0; q2 < KS; ++q2) ksum1<CPT>(sb + (size_t)q2 * mv, nkt, kt, c2, gc, s);
           }
         }
         release();
@@ -475,16 +533,9 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         mbar_wait(&full[slot], phase);
         const VT* sb = reinterpret_cast<const VT*>(ring + (size_t)slot * slot_floats);
         if (!(p.diag & COT_DIAG_NO_COMPUTE)) {
-          for (int q2 = 0; q2 < kk; ++q2) {
-#pragma unroll
-            for (int q = 0; q < CPT; ++q) {
-              const float4 c = sb[q2 * mv + q * nkt + kt];
-              s[q][0] += ex2(fmaf(-c.x, c2, gc[q][0]));
-              s[q][1] += ex2(fmaf(-c.y, c2, gc[q][1]));
-              s[q][2] += ex2(fmaf(-c.z, c2, gc[q][2]));
-              s[q][3] += ex2(fmaf(-c.w, c2, gc[q][3]));
-            }
-          }
+          int q2 = 0;
+          for (; q2 + 4 <= kk; q2 += 4) ksum4<CPT>(sb + (size_t)q2 * mv, mv, nkt, kt, c2, gc, s);
+          for (; q2 < kk; ++q2) ksum1<CPT>(sb + (size_t)q2 * mv, nkt, kt, c2, gc, s);
         }
         release();
       }
@@ -602,6 +653,16 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
     double zown0 = own0 ? __ldcg(p.z_hat + col0 + et) : 0.0;   // this thread's z_hat of the slice, kept in a register
     int done = 0;   // iterations completed (q-update applied) in this launch
     bool halted = false;
+    // ---- w_hat of this CTA's rows, LSE_i = shift_i + log r_i, from the row statistics of the last completed
+    // iteration: written once per launch (after the last iteration, or where the launch halts), not per iteration;
+    // log without MUFU (the k-sum warps keep it busy)
+    auto write_w_hat = [&]() {
+      if (et < 32) {   // the writer's warp (__syncwarp orders its shared-memory writes for the lanes)
+        __syncwarp();
+        for (int r = et; r < nrows; r += 32)
+          p.w_hat[p.row_begin + i0 + r] = rowstat[r * RS + 3] - (rowstat[r * RS + 1] + log_nomufu(rowstat[r * RS + 2]));
+      }
+    };
     for (int t = 0; active0 && t < p.iters; ++t) {
       if (t > 0 && sync) {
         // ---- z_hat of generation g (the q-update of iteration t-1) and, if due, its monitor
@@ -646,6 +707,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
         if (halted) {
           st.active = 0;
           if (et == 0) sts_release(&ctl[5], 1u);   // stop the k-sum warps (their rows are drained below)
+          write_w_hat();                            // the row statistics of iteration t - 1 are still in place
           break;
         }
       }
@@ -883,15 +945,6 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
           if (p.trace) c_epi += clock64() - te0;
         }
       }
-      // ---- w_hat of this CTA's rows, LSE_i = shift_i + log r_i, by the warp of the thread that wrote the row
-      // statistics (no block barrier); off the critical path in the iterated launch (after the partial lines are out)
-      auto write_w_hat = [&]() {
-        if (et < 32) {   // the writer's warp (__syncwarp orders its shared-memory writes for the lanes)
-          __syncwarp();
-          for (int r = et; r < nrows; r += 32)
-            p.w_hat[p.row_begin + i0 + r] = rowstat[r * RS + 3] - (rowstat[r * RS + 1] + log(rowstat[r * RS + 2]));
-        }
-      };
       if (p.rows_only) {   // cerot_rows: the plain fp64 partial, no device-wide step
         write_w_hat();
 #pragma unroll
@@ -945,7 +998,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
           for (int v = 0; v < VEC; ++v) P[q][v] = 0.0;
         }
       }
-      write_w_hat();
+      if (t == p.iters - 1) write_w_hat();
       // ---- column pass of this CTA's slice: c_j = sum_u P_uj in unit order; q-update; z lines
       const long long tc0 = p.trace ? clock64() : 0;
       if (p.trace) c_pub += tc0 - tp0;
@@ -1292,10 +1345,28 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
                              (size_t)kColScratch * 8 + rpw_bytes;
   const size_t budget = 220 * 1024;
   if (queue_bytes + 2 * slot_bytes + 4096 > budget) return cudaErrorInvalidConfiguration;
-  p.nslot = (int)std::max<size_t>(2, std::min<size_t>(64, (budget - queue_bytes - 4096) / slot_bytes));
-  // ring + 1 KiB pad (branch-free over-reads past the last column stay in-bounds) + row queue + row
-  // statistics + barriers + control + reduction scratch
-  cfg->smem = (size_t)p.nslot * slot_bytes + 1024 + queue_bytes + ((size_t)p.nslot + p.qn) * 16 + 64 + 128 * 8 + 64;
+  // Resident k-blocks: shared memory the ring does not need (beyond kMinSlots slots in flight) holds the first
+  // kres k-blocks of every row of the unit for the whole launch, so only n - kres blocks per row are re-streamed
+  // each iteration (every Gibbs term is still evaluated every iteration; the bytes come from on-chip memory).
+  // Not for single-iteration launches (nothing to reuse) or the precomputed mode. COT_KRES overrides.
+  int kMinSlots = 4;
+  if (const char* ev = getenv("COT_MIN_SLOTS")) kMinSlots = std::max(2, atoi(ev));   // tuning experiments
+  p.kres = 0;
+  if (!rows_only && iters > 1 && !(a.flags & COT_PRECOMPUTED)) {
+    const size_t fixed = queue_bytes + 4096 + (size_t)kMinSlots * slot_bytes;
+    const size_t per_k = (size_t)p.rpu * row_bytes;
+    if (budget > fixed) p.kres = (int)std::min<size_t>((size_t)a.n, (budget - fixed) / per_k);
+  }
+  if (const char* ev = getenv("COT_KRES")) {
+    const int want = atoi(ev);
+    if (want >= 0) p.kres = std::min(p.kres, want);
+  }
+  const size_t resid_bytes = (size_t)p.rpu * p.kres * row_bytes;
+  p.nslot = (int)std::max<size_t>(2, std::min<size_t>(64, (budget - queue_bytes - 4096 - resid_bytes) / slot_bytes));
+  // ring + 1 KiB pad (branch-free over-reads past the last column stay in-bounds) + resident k-blocks + row
+  // queue + row statistics + barriers + control + reduction scratch
+  cfg->smem = (size_t)p.nslot * slot_bytes + 1024 + resid_bytes + queue_bytes + ((size_t)p.nslot + p.qn) * 16 +
+              16 + 64 + 128 * 8 + 64;
   p.iters = rows_only ? 1 : iters;
   p.rows_only = rows_only ? 1 : 0;
   p.tol = a.tol;
