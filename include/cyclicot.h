@@ -193,8 +193,11 @@ int cerot_plan(const double* alpha, const double* beta, const void* C, const voi
                const double* w_hat, const double* z_hat, void* T_blocks, double* d_report,
                void* workspace, size_t ws_bytes, void* stream);
 
-/* Whole C-EROT solve (A2..A5): clot_aggregate into the workspace, cerot_init, iterations in chunks  */
-/* of check_every until every problem converged (tol > 0) or max_iter, then cerot_plan. Synchronises.*/
+/* Whole C-EROT solve (A2..A5): clot_aggregate into the workspace, cerot_init, then up to max_iter   */
+/* iterations with the freeze rule applied ON THE DEVICE every check_every iterations ("until        */
+/* convergence"): one persistent launch (cluster-resident / TMA kernels), or one CUDA graph    */
+/* with a device-side while loop (generic kernels) -- no host round trip per check -- then cerot_plan.*/
+/* Synchronises once, for the report.                                                                */
 /* report: HOST array of B cot_report. T_blocks may be NULL. Returns COT_OK, COT_NOT_CONVERGED if    */
 /* some problem did not reach tol (tol > 0), or an error.                                             */
 int cerot_solve(const double* alpha, const double* beta, const void* C,

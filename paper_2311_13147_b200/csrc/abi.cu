@@ -60,6 +60,7 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, i
   w.state = reinterpret_cast<SolverState*>(take((size_t)B * sizeof(SolverState)));
   w.counters = reinterpret_cast<unsigned*>(take((size_t)B * 4));
   w.grid_bar = reinterpret_cast<unsigned*>(take(16));
+  w.loopctl = reinterpret_cast<unsigned*>(take(16));
   w.nonfinite = reinterpret_cast<int32_t*>(take(4));
   w.report = reinterpret_cast<double*>(take((size_t)B * kReportDoubles * 8));
   // monitor partials: per 32-column tile (k_cols, k_zupdate) or per 4-column tile (C-SROT z-step)
@@ -444,26 +445,21 @@ int cerot_solve(const double* alpha, const double* beta, const void* C, int64_t 
   std::vector<int64_t> it((size_t)B);
   std::vector<int32_t> conv((size_t)B);
   std::vector<double> res((size_t)B);
-  int64_t done = 0;
-  while (done < max_iter) {
-    const int64_t chunk = std::min<int64_t>(check_every, max_iter - done);
-    if (batch_cluster_eligible(a)) {
-      COT_CHECK_CUDA(launch_batch_cluster(a, ws, (int)chunk, s));
-    } else if (tma_eligible(a)) {
-      COT_CHECK_CUDA(launch_iter_tma(a, ws, (int)chunk, false, 0, s));
-    } else {
-      for (int64_t t = 0; t < chunk; ++t) {
-        COT_CHECK_CUDA(launch_rows(a, ws, up, (int)((done + t) & 1), s));
-        COT_CHECK_CUDA(launch_cols(a, ws, up, (int)((done + t) & 1), s));
+  // "Until convergence" (Alg. 2 line 6) on the device: the persistent kernels run up to max_iter iterations
+  // in one launch and apply the freeze rule themselves; the generic kernels run as one CUDA graph
+  // with a device-side while loop. No host round trip until the report.
+  if (max_iter > 0) {
+    if (batch_cluster_eligible(a) || tma_eligible(a)) {
+      for (int64_t done = 0; done < max_iter;) {   // int-sized launches (one launch unless max_iter >= 2^31)
+        const int chunk = (int)std::min<int64_t>(max_iter - done, 0x7fffffff);
+        if (batch_cluster_eligible(a))
+          COT_CHECK_CUDA(launch_batch_cluster(a, ws, chunk, s));
+        else
+          COT_CHECK_CUDA(launch_iter_tma(a, ws, chunk, false, 0, s));
+        done += chunk;
       }
-    }
-    done += chunk;
-    if (tol > 0.0 || done >= max_iter) {
-      st = cerot_state(workspace, B, m, n, dtype, it.data(), conv.data(), res.data(), stream);
-      if (st) return st;
-      bool all = tol > 0.0;
-      for (int64_t b = 0; b < B && all; ++b) all = conv[(size_t)b] != 0;
-      if (all) break;
+    } else {
+      COT_CHECK_CUDA(launch_ldg_loop(a, ws, up, max_iter, s));
     }
   }
   st = plan_and_report(a, ws, T_blocks, ws.report, nullptr, s);

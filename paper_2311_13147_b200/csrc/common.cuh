@@ -19,12 +19,16 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 // 2^x = 2^k * 2^f with k = round(x) an integer and 2^f (|f| <= 1/2) in fp64 (the 1.5 * 2^52 rounding trick,
-// valid for |x| < 2^31).
+// valid for |x| < 2^31). Explicitly rounded operations: the compiler must not contract them into FMAs
+// differently at different call sites (the split of a z value has to be bitwise the same wherever it is taken,
+// or launches that continue each other would not reproduce a single launch).
 __device__ __forceinline__ double split_pow2_fp64(double x, int& k) {
-  const double big = x + 6755399441055744.0;   // 1.5 * 2^52: round to an integer in the low word
+  const double big = __dadd_rn(x, 6755399441055744.0);   // 1.5 * 2^52: round to an integer in the low word
   k = __double2loint(big);
-  return exp2(x - (big - 6755399441055744.0));
+  return exp2(__dsub_rn(x, __dsub_rn(big, 6755399441055744.0)));
 }
+// The split of a potential z (natural units): z log2e = k + f.
+__device__ __forceinline__ double split_z(double z, int& k) { return split_pow2_fp64(__dmul_rn(z, COT_LOG2E), k); }
 // f * 2^e, exactly, for f in [2^-22, 2^23) (the k-sums s'_ij lie in [0.7, 1.42 n]) and e clamped to
 // [-1000, 1000]: terms below 2^-1000 come out ~1e-301 (negligible); callers whose exponents can exceed 1000
 // check the sums' range. Integer operations only.

@@ -49,6 +49,7 @@ struct Workspace {
   SolverState* state;      // [B]
   unsigned* counters;      // [B] last-block-done tickets (self-resetting)
   unsigned* grid_bar;      // [4] two device-wide barriers of the persistent TMA kernel (count, generation)
+  unsigned* loopctl;       // [4] cerot_solve's device-side loop (CUDA graph while-node): iterations launched
   int32_t* nonfinite;      // [1]
   double* report;          // [B][kReportDoubles]
   double* c_local;         // [B][m] column sums over the held rows (sharded path)
@@ -106,6 +107,11 @@ cudaError_t launch_init(const double* alpha, const double* beta, int64_t B, int6
 cudaError_t launch_rows(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int parity, cudaStream_t s);
 // Column pass (deterministic reduction + q-update + monitor) reading ws.partials[parity].
 cudaError_t launch_cols(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int parity, cudaStream_t s);
+// Up to max_iter iterations of the generic row/column kernels as ONE CUDA graph with a device-side while loop
+// (conditional node): the loop ends when every problem is frozen by the freeze rule or after max_iter
+// iterations; no host synchronisation in between.
+cudaError_t launch_ldg_loop(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int64_t max_iter,
+                            cudaStream_t s);
 bool tma_eligible(const IterArgs& a, int sms = 0);   // sms: SMs the launch may use (0: all)
 // Cluster-resident small problems (fp32, m <= 256, m % 4 == 0): `iters` full iterations of every problem.
 bool batch_cluster_eligible(const IterArgs& a);

@@ -129,7 +129,7 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
       zk[j] = (int)ck + 896;
     } else {
       int kz;
-      zf[j] = split_pow2_fp64(z * COT_LOG2E, kz);
+      zf[j] = split_z(z, kz);
       zk[j] = kz + 896;
     }
     bcol[j] = p.beta[b * m + j];

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(NT, MINB) k_batch_cluster(BatchParams p) {
   }
   for (int j = threadIdx.x; j < m; j += blockDim.x) {
     zs[j] = p.z_hat[b * m + j];
-    zf[j] = split_pow2_fp64(zs[j] * COT_LOG2E, zk[j]);
+    zf[j] = split_z(zs[j], zk[j]);
     const double bj = p.beta[b * m + j];
     bcol[2 * j] = bj;
     bcol[2 * j + 1] = log(bj);
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(NT, MINB) k_batch_cluster(BatchParams p) {
         }
         zn = zs[j] + (bcol[2 * j + 1] - log_nomufu(v));
         int kz;
-        const double fz = split_pow2_fp64(zn * COT_LOG2E, kz);
+        const double fz = split_z(zn, kz);
         cluster.map_shared_rank(zs, src)[j] = zn;   // lane `src` of the group writes replica `src`
         cluster.map_shared_rank(zf, src)[j] = fz;
         cluster.map_shared_rank(zk, src)[j] = kz;
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_cluster_ws(BatchParams p) {
   }
   for (int j = threadIdx.x; j < m; j += blockDim.x) {
     zs[j] = p.z_hat[b * m + j];
-    zf[j] = split_pow2_fp64(zs[j] * COT_LOG2E, zk[j]);
+    zf[j] = split_z(zs[j], zk[j]);
     const double bj = p.beta[b * m + j];
     bcol[2 * j] = bj;
     bcol[2 * j + 1] = log(bj);
@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_cluster_ws(BatchParams p) {
           }
           const double zn = zs[j] + (bcol[2 * j + 1] - log_nomufu(v));
           int kz;
-          const double fzn = split_pow2_fp64(zn * COT_LOG2E, kz);
+          const double fzn = split_z(zn, kz);
           cluster.map_shared_rank(zs, src)[j] = zn;
           cluster.map_shared_rank(zf, src)[j] = fzn;
           cluster.map_shared_rank(zk, src)[j] = kz;

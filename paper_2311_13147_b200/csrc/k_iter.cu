@@ -366,6 +366,63 @@ cudaError_t launch_rows(const IterArgs& a, const Workspace& ws, const UnitPlan& 
   return rows_dispatch<double, 1>(rp, up.grid, a.m, s);
 }
 
+// The condition of cerot_solve's device-side loop: continue while some problem is still active and fewer than
+// max_iter iterations have been launched (one block).
+__global__ void __launch_bounds__(256) k_loop_cond(cudaGraphConditionalHandle h, const SolverState* __restrict__ state,
+                                                   int64_t B, unsigned* __restrict__ ctr, int64_t max_iter) {
+  int any = 0;
+  for (int64_t b = threadIdx.x; b < B; b += blockDim.x) any |= state[b].active;
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) {
+    const unsigned done = ctr[0] + 1u;
+    ctr[0] = done;
+    cudaGraphSetConditional(h, (any && (int64_t)done < max_iter) ? 1u : 0u);
+  }
+}
+
+cudaError_t launch_ldg_loop(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int64_t max_iter,
+                            cudaStream_t s) {
+  if (max_iter < 1) return cudaSuccess;
+  cudaGraph_t g = nullptr, body = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  cudaError_t e = cudaGraphCreate(&g, 0);
+  if (e != cudaSuccess) return e;
+  cudaGraphConditionalHandle h;
+  e = cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault);
+  cudaGraphNode_t node;
+  cudaGraphNodeParams cp = {};
+  if (e == cudaSuccess) {
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+  }
+  cudaStream_t cs = nullptr;
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {   // the loop body: one iteration of every active problem, then the condition
+    body = cp.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) {
+      cudaError_t e1 = launch_rows(a, ws, up, 0, cs);
+      if (e1 == cudaSuccess) e1 = launch_cols(a, ws, up, 0, cs);
+      if (e1 == cudaSuccess) {
+        k_loop_cond<<<1, 256, 0, cs>>>(h, ws.state, a.B, ws.loopctl, max_iter);
+        e1 = cudaGetLastError();
+      }
+      e = cudaStreamEndCapture(cs, &body);
+      if (e1 != cudaSuccess) e = e1;
+    }
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
+  if (e == cudaSuccess) e = cudaMemsetAsync(ws.loopctl, 0, 16, s);
+  if (e == cudaSuccess) e = cudaGraphLaunch(ge, s);
+  if (ge) cudaGraphExecDestroy(ge);   // freed once the in-flight launch completes
+  if (g) cudaGraphDestroy(g);
+  if (cs) cudaStreamDestroy(cs);
+  return e;
+}
+
 cudaError_t launch_cols(const IterArgs& a, const Workspace& ws, const UnitPlan& up, int parity, cudaStream_t s) {
   dim3 grid((unsigned)((a.m + 31) / 32), (unsigned)a.B);
   k_cols<<<grid, 256, 0, s>>>(ws.partials[parity], up.upp, a.m, a.n, a.beta, a.z_hat, ws.resid_part, ws.state,

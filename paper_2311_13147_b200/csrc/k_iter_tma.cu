@@ -628,7 +628,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         const int jv = q * net + et;
-        Fz[q][v] = split_pow2_fp64((jv < mv ? __ldcg(p.z_hat + VEC * jv + v) : 0.0) * COT_LOG2E, kz[q][v]);
+        Fz[q][v] = split_z((jv < mv ? __ldcg(p.z_hat + VEC * jv + v) : 0.0), kz[q][v]);
         P[q][v] = 0.0;
       }
     auto need_resid = [&](int t) {
@@ -688,7 +688,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
               }
             }
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) Fz[q][v] = split_pow2_fp64(ll_value(zl[v]) * COT_LOG2E, kz[q][v]);
+            for (int v = 0; v < VEC; ++v) Fz[q][v] = split_z(ll_value(zl[v]), kz[q][v]);
           }
         }
         if (need_resid(t - 1)) st.residual = read_resid(g) * (double)n;
@@ -1361,6 +1361,10 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
     const int want = atoi(ev);
     if (want >= 0) p.kres = std::min(p.kres, want);
   }
+  // a multiple of 4: the k-sum's blocks of four k-rows then start at the same k whether a block is resident or
+  // streamed, so the sums (and every iterate) do not depend on kres -- a single-iteration launch (kres = 0)
+  // continues a resident launch bit for bit
+  if (p.kres < (int)a.n) p.kres &= ~3;
   const size_t resid_bytes = (size_t)p.rpu * p.kres * row_bytes;
   p.nslot = (int)std::max<size_t>(2, std::min<size_t>(64, (budget - queue_bytes - 4096 - resid_bytes) / slot_bytes));
   // ring + 1 KiB pad (branch-free over-reads past the last column stay in-bounds) + resident k-blocks + row

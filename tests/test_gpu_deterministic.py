@@ -4,8 +4,8 @@ Column partials are accumulated exactly in 128-bit fixed point and every row's s
 order, so the iterates must not depend on the row partition: the unsharded persistent kernel on all SMs, on
 fewer SMs, and 2/4/8 emulated ranks of the fused path (one cooperative launch, each virtual rank on 1/N of the
 SMs: the profiling recipe's way of testing ranks that wait on each other on one GPU) give bitwise identical
-potentials, and stay within the parity bars of the oracle. (Launch boundaries are part of the schedule: a
-solve split over several launches agrees with a single launch to ~1e-14, not bit for bit.)"""
+potentials, and stay within the parity bars of the oracle; a solve split over several launches reproduces one launch
+bit for bit."""
 import os
 
 import numpy as np
@@ -130,3 +130,16 @@ def test_split_entry_points_reject_deterministic():
     with pytest.raises(cot.CotError) as e:
         sh.iterate(2, flags=DET)
     assert e.value.code == -1 and "COT_DETERMINISTIC" in str(e.value)
+
+
+@pytest.mark.parametrize("maker", [lambda: synthetic.c4_large(m=512, n=16), lambda: synthetic.c3_image()],
+                         ids=["C4_m512_n16", "C3"])
+def test_bitwise_identical_across_launch_boundaries(maker):
+    """COT_DETERMINISTIC: the row shift is the exact maximum every iteration and the column sums are exact, so a
+    solve split over several launches (7 + 11 + 7) gives the bits of one 25-iteration launch."""
+    p = maker()
+    w1, z1 = _unsharded(p, [25])
+    for split in ([7, 11, 7], [1, 23, 1], [12, 13]):   # 1-iteration launches keep no k-blocks resident
+        w2, z2 = _unsharded(p, split)
+        assert np.array_equal(z1.view(np.uint64), z2.view(np.uint64)), split
+        assert np.array_equal(w1.view(np.uint64), w2.view(np.uint64)), split

@@ -478,3 +478,31 @@ def test_chain_kernel_launch_boundaries_bitwise():
     assert cot.lib().cot_iter_path(30, p.n, p.m, 0, 0) == 3
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("maker,path", [(lambda: synthetic.c1_tiny(), 0), (lambda: synthetic.c3_image(pair=1), 1),
+                                        (lambda: synthetic.c2_ring(eps_factor=1e-1), 3)],
+                         ids=["C1_ldg_graph_loop", "C3_tma_one_launch", "C2_chain_one_launch"])
+def test_solve_to_tolerance_on_device(maker, path):
+    """cerot_solve: "until convergence" on the device -- one persistent launch, or (fp64 / generic path) one
+    CUDA graph with a device-side while loop -- stops at the oracle's stopping iteration with the freeze rule
+    checked every check_every iterations, and the report matches the oracle there."""
+    p = maker()
+    tol = p.tol if p.tol > 0 else 1e-7
+    ce = 1 if path == 0 else 5
+    assert cot.lib().cot_iter_path(p.B, p.n, p.m, 1 if p.C.dtype == np.float64 else 0, 0) == path
+    w, z, t, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 20000, tol=tol, check_every=ce,
+                                        form="kernel")
+    wg, zg, T, reps = cot.cerot_solve(_dev(p.C), _dev(p.alpha), _dev(p.beta), p.eps, tol=tol, max_iter=20000,
+                                      check_every=ce, T_blocks=True)
+    fp64 = p.C.dtype == np.float64
+    assert reps[0]["converged"]
+    if fp64:
+        assert reps[0]["iters"] == t
+        _compare(p, np.array([reps[0][f] for f in cot.REPORT_FIELDS]), T.cpu().numpy(), w, z, 1e-10, 1e-10)
+    else:
+        def run_fixed(tt):
+            _, Tq, rq, itq, _ = _gpu_run(p, tt)
+            return rq[0], Tq
+        check_stop_iteration(p, reps[0]["iters"], tol, ce, 20000, run_fixed,
+                             np.array([reps[0][f] for f in cot.REPORT_FIELDS]), T.cpu().numpy())
