@@ -32,6 +32,7 @@ import numpy as np  # noqa: E402
 
 DEFAULT_METRIC = "C-EROT Gibbs-kernel evals/s (n·m² per iter) and % of HBM/SFU roofline, 1–8 GPU"
 UNIT = "Gibbs-kernel evals/s"
+_JSON_OUT = sys.stdout   # replaced in main() by the saved stdout
 
 
 def _metric() -> str:
@@ -761,6 +762,13 @@ def run_reference(args):
 
 
 def main():
+    # stdout carries exactly one JSON line: everything else written to fd 1 by native code (e.g. NCCL's version
+    # banner at its first collective) goes to stderr; the JSON line is written to the saved stdout
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    global _JSON_OUT
+    _JSON_OUT = os.fdopen(json_fd, "w")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -783,7 +791,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        print(json.dumps(run_reference(args)), flush=True)
+        print(json.dumps(run_reference(args)), file=_JSON_OUT, flush=True)
         return 0
     force_sharded = os.environ.get("COT_BENCH_SHARDED") == "1"   # exercise the row-sharded path at N = 1
     if world > 1 or force_sharded:
@@ -797,7 +805,7 @@ def main():
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=_JSON_OUT, flush=True)
     if torch_dist_initialized():
         import torch.distributed as tdist
         tdist.destroy_process_group()
