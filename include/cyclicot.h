@@ -331,6 +331,10 @@ int cerot_two_stage(const double* a, const double* b, const void* C, int64_t n, 
 /* the pivot count. Synchronous, single-threaded, no device work; thread-safe on distinct buffers.        */
 int clot_small_lot(const double* alpha, const double* beta, const double* G, int64_t m, double* S,
                    double* value, double* u, double* v, int64_t* pivots);
+/* The C-LOT value of the explicit d x d problem (Theorem 1, at full scale): value_full = n * <G, S*> */
+/* with S* from clot_small_lot (written to S, HOST [m][m]); value_small = <G, S*> (may be NULL). HOST, synchronous. */
+int clot_lot_value(const double* alpha, const double* beta, const double* G, int64_t m, int64_t n, double* S,
+                   double* value_full, double* value_small);
 
 /* ---------------------------------------------------------------------------------------------- */
 /* NEXT-3: C-SROT, strongly convex regularised OT through the 2m-variable Fenchel dual        */

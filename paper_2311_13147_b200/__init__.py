@@ -86,6 +86,7 @@ _SIGS = {
     # NEXT-4: host network simplex for the small LOT (host pointers)
     "clot_small_lot": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, ctypes.POINTER(_dbl), _vp, _vp,
                                       ctypes.POINTER(_i64)]),
+    "clot_lot_value": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
     "cerot_solve_sharded": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _dbl, _i64,
                                            _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp, ctypes.POINTER(cot_report),
                                            _vp]),

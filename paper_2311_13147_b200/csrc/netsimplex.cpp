@@ -274,3 +274,19 @@ extern "C" int clot_small_lot(const double* alpha, const double* beta, const dou
   if (pivots) *pivots = ns.pivots;
   return COT_OK;
 }
+
+// Theorem 1 with the full-scale factor of P:251: the optimal value of the explicit d x d C-LOT problem is
+// n times the small LOT's <G, S*>. The library applies the factor (callers need not know the reduction's scaling).
+extern "C" int clot_lot_value(const double* alpha, const double* beta, const double* G, int64_t m, int64_t n,
+                              double* S, double* value_full, double* value_small) {
+  if (n < 1 || !value_full) {
+    cot::set_error("clot_lot_value: need n >= 1 and value_full");
+    return COT_E_ARG;
+  }
+  double small = 0.0;
+  const int st = clot_small_lot(alpha, beta, G, m, S, &small, nullptr, nullptr, nullptr);
+  if (st != COT_OK) return st;
+  *value_full = (double)n * small;
+  if (value_small) *value_small = small;
+  return COT_OK;
+}

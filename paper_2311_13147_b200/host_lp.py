@@ -39,9 +39,18 @@ def clot_solve(C, alpha: np.ndarray, beta: np.ndarray, expand: bool = True, stre
     C: device tensor [n][m][m]. Returns dict(value = n <G, S*> (full scale), S, G, argmin, T_full)."""
     import torch
     n = C.shape[0]
+    import ctypes
+    from . import _check, lib
     G, A = clot_aggregate(C, stream=stream)
-    Gh = G.double().cpu().numpy()
-    small, S = small_lot(np.asarray(alpha, np.float64), np.asarray(beta, np.float64), Gh)
+    Gh = np.ascontiguousarray(G.double().cpu().numpy())
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    b = np.ascontiguousarray(beta, dtype=np.float64)
+    m = Gh.shape[0]
+    S = np.zeros((m, m))
+    full, small = ctypes.c_double(), ctypes.c_double()
+    Pn = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    _check(lib().clot_lot_value(Pn(a), Pn(b), Pn(Gh), m, n, Pn(S), ctypes.byref(full), ctypes.byref(small)),
+           "clot_lot_value")   # the full-scale factor n (P:251) is applied by the library
     S_dev = torch.as_tensor(S, dtype=C.dtype, device=C.device)   # rounded once to the problem dtype
     T = clot_expand(S_dev, n, argmin=A, stream=stream) if expand else None
-    return {"value": n * small, "small_value": small, "S": S_dev, "G": G, "argmin": A, "T_full": T}
+    return {"value": full.value, "small_value": small.value, "S": S_dev, "G": G, "argmin": A, "T_full": T}

@@ -100,3 +100,26 @@ def test_argument_errors():
         host_lp.small_lot(np.array([1.0, 0.0]), np.array([0.5, 0.5]), np.zeros((2, 2)))   # zero entry
     with pytest.raises(CotError):
         host_lp.small_lot(np.array([1.0]), np.array([1.0]), np.array([[np.nan]]))
+
+
+def test_clot_lot_value_applies_full_scale_factor():
+    """clot_lot_value: the library returns the explicit problem's C-LOT value n * <G, S*> (Theorem 1)
+    -- equal to the oracle's brute-force LP on the expanded d x d problem (C1)."""
+    import ctypes
+    import oracle
+    import synthetic
+    import paper_2311_13147_b200 as cot
+    p = synthetic.c1_tiny()
+    G, _ = oracle.aggregate(p.C)
+    m = p.m
+    S = np.zeros((m, m))
+    full, small = ctypes.c_double(), ctypes.c_double()
+    a, b, Gc = (np.ascontiguousarray(x, dtype=np.float64) for x in (p.alpha, p.beta, G))
+    assert cot.lib().clot_lot_value(a.ctypes.data_as(ctypes.c_void_p), b.ctypes.data_as(ctypes.c_void_p),
+                                    Gc.ctypes.data_as(ctypes.c_void_p), m, p.n, S.ctypes.data_as(ctypes.c_void_p),
+                                    ctypes.byref(full), ctypes.byref(small)) == 0
+    assert abs(full.value - p.n * small.value) <= 1e-15 * abs(full.value)
+    ref, _ = oracle.lot(oracle.expand_vector(p.alpha, p.n), oracle.expand_vector(p.beta, p.n),
+                        oracle.expand_cost(p.C))
+    assert abs(full.value - ref) <= 1e-9 * max(1.0, abs(ref))
+    assert cot.lib().clot_lot_value(None, None, None, m, 0, None, ctypes.byref(full), None) == -1
