@@ -78,10 +78,25 @@ __device__ __forceinline__ void st_cluster_release_u32(uint32_t addr, unsigned v
 __device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t remote_bar) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
 }
-__device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
+// Phase test with CTA-scope acquire: the s' bytes land through st.async, counted by complete_tx on this CTA's own
+// barrier, and the free signal carries no data; a cluster-scope acquire would add an L1 invalidation (CCTL.IVALL)
+// after every successful test.
+__device__ __forceinline__ bool mbar_test_cta(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Non-blocking phase test (same scope): issued early, its result is consumed later.
+__device__ __forceinline__ bool mbar_probe_cta(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
@@ -104,11 +119,12 @@ template <bool FULL>
 __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b, unsigned char* smem,
                                            uint64_t* bars, float* sb, const float c2, const SolverState st0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = p.n, m = p.m, mv = m >> 2, NP = p.ncl - 1;
+  const int n = p.n, m = FULL ? 128 : p.m, mv = m >> 2, NP = p.ncl - 1;   // FULL: compile-time offsets
+  const int wps = m + 2;   // warp-partial row stride: the column pass's four row groups fall in two bank halves
   unsigned* stopf = reinterpret_cast<unsigned*>(smem + 64);
   int* As = reinterpret_cast<int*>(sb + (size_t)2 * m * m);            // [m][m] a_ij
-  double* wpart = reinterpret_cast<double*>(As + (size_t)m * m);       // [16][m] warp column partials
-  double* zf = wpart + (size_t)kChainWarps * m;                        // [m] Fz_j
+  double* wpart = reinterpret_cast<double*>(As + (size_t)m * m);       // [16][m + 2] warp column partials
+  double* zf = wpart + (size_t)kChainWarps * wps;                      // [m] Fz_j
   double* bcol = zf + m;                                               // [m] beta_j
   double* rstat = bcol + m;                                            // [m][2] kM_i ln2, r_i
   double* red = rstat + 2 * m;                                         // [32]
@@ -150,7 +166,7 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     const long long c0t = p.trace ? clock64() : 0;
     const int q = t & 1;
     const bool need = (p.tol > 0.0 && (st.iters + 1) % p.check_every == 0) || t == p.iters - 1;
-    while (!mbar_test_cluster(&bars[q], (uint32_t)((t >> 1) & 1))) {
+    while (!mbar_test_cta(&bars[q], (uint32_t)((t >> 1) & 1))) {
     }
     // arm buffer q for iteration t + 2 (its phase of iteration t has completed; the producers fill it only after
     // the free signal below)
@@ -219,7 +235,7 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
       for (int v = 0; v < 4; ++v) P[v] = fma(rho, uu[k][v], P[v]);
     }
     if (lane_ok) {
-      double2* wp = reinterpret_cast<double2*>(wpart + (size_t)warp * m);
+      double2* wp = reinterpret_cast<double2*>(wpart + (size_t)warp * wps);
       wp[2 * lane] = make_double2(P[0] * fz[0], P[1] * fz[1]);
       wp[2 * lane + 1] = make_double2(P[2] * fz[2], P[3] * fz[3]);
     }
@@ -234,8 +250,8 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     const bool cok = FULL || col < m;
     double c = 0.0;
     if (cok) {
-      const double* wp = wpart + (size_t)(4 * g) * m + col;
-      c = (wp[0] + wp[m]) + (wp[2 * (size_t)m] + wp[3 * (size_t)m]);
+      const double* wp = wpart + (size_t)(4 * g) * wps + col;
+      c = (wp[0] + wp[wps]) + (wp[2 * (size_t)wps] + wp[3 * (size_t)wps]);
     }
     c += __shfl_xor_sync(0xffffffffu, c, 1);   // (a0 + a1) + (a2 + a3) in every lane of the group: the
     c += __shfl_xor_sync(0xffffffffu, c, 2);   // additions commute bitwise
@@ -381,6 +397,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
     long long tk = 0, tw = 0, tsv = 0;
     for (int t = 0; t < p.iters; ++t) {
       const long long c0t = p.trace ? clock64() : 0;
+      // buffer q is free once the chain has finished the r-pass of iteration t - 2 (no wait for the first two);
+      // it almost always is by now: probe before the k-sum, so that the probe's trip through the SM's
+      // shared-memory pipe (queued behind the other warps' MUFU.EX2) overlaps the k-sum
+      const int q = t & 1;
+      const uint32_t par = (uint32_t)(((t >> 1) - 1) & 1);
+      bool freed = t < 2 || mbar_probe_cta(&bars[2 + q], par);
       float s[2][4];
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
@@ -420,22 +442,18 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
           s[rr][3] += ex2(fmaf(-c.w, c2, gcr[rr][3]));
         }
       }
-      const int q = t & 1;
       const long long c1t = p.trace ? clock64() : 0;
-      // buffer q is free once the chain has finished the r-pass of iteration t - 2 (no wait for the first two)
-      int go = 1;
-      if (t >= 2 && lane == 0) {
-        const uint32_t par = (uint32_t)(((t >> 1) - 1) & 1);
-        while (!mbar_test_cluster(&bars[2 + q], par)) {
-          if (*(volatile unsigned*)stopf) {
-            go = 0;
+      // else poll: the whole warp (one instruction, a uniform result, no shuffle)
+      bool go = true;
+      if (!freed) {
+        while (!mbar_test_cta(&bars[2 + q], par)) {
+          if (*(volatile unsigned*)stopf) {   // the chain has stopped (it converged, or its launch ends)
+            go = false;
             break;
           }
         }
       }
-      go = __shfl_sync(0xffffffffu, go, 0);
       if (!go) break;
-      __syncwarp();
       const long long c2t = p.trace ? clock64() : 0;
       // fire and forget: each 16-byte store counts its bytes on the chain's full[q] barrier when it lands
 #pragma unroll
@@ -451,7 +469,6 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
         tw += c2t - c1t;
         tsv += c3t - c2t;
       }
-      if (__shfl_sync(0xffffffffu, *(volatile unsigned*)stopf, 0)) break;   // the chain has stopped
     }
     if (p.trace && threadIdx.x == 0 && b < 64) {
       unsigned long long* tp = p.trace + (size_t)blockIdx.x * 8;
@@ -476,7 +493,7 @@ struct ChainCfg {
 };
 
 size_t chain_smem_chain(int64_t m) {   // s' x 2, a_ij, warp partials, Fz, beta, row stats, scratch, kz
-  return kChainHeader + (size_t)2 * m * m * 4 + (size_t)m * m * 4 + (size_t)kChainWarps * m * 8 + (size_t)m * 8 +
+  return kChainHeader + (size_t)2 * m * m * 4 + (size_t)m * m * 4 + (size_t)kChainWarps * (m + 2) * 8 + (size_t)m * 8 +
          (size_t)m * 8 + (size_t)m * 16 + 32 * 8 + (size_t)m * 4;
 }
 
