@@ -343,6 +343,31 @@ def test_cluster_path_batch_freeze_fp32():
         check_stop_iteration(q, it[b], 1e-7, 5, 4000, run_fixed, rep[b], T[b])
 
 
+def test_chain_batch_freeze_six_cta_clusters():
+    """k_batch_chain in the 6-CTA schedule C5 runs (26-row producers): per-problem freeze rule with mixed eps --
+    the problems stop at iterations 20..70 while their producers run up to two iterations ahead of the chain
+    CTA and must leave through the stop flag, not a buffer hand-back."""
+    p = synthetic.random_cyclic(seed=9, n=4, m=128, B=4, eps=0.1, dtype=np.float32)
+    p.eps = np.array([0.01, 0.004, 0.02, 0.007])
+    with _env(COT_CHAIN_NCL="6"):
+        assert cot.lib().cot_iter_path(p.B, p.n, p.m, 0, 0) == 3
+        prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps))
+        prob.init().iterate(4000, tol=1e-7, check_every=5)
+        T, rep = prob.plan(T_blocks=True)
+        it, conv, _ = prob.state()
+    T, rep = T.cpu().numpy(), rep.cpu().numpy()
+    assert len(set(int(x) for x in it)) > 1
+    for b in range(p.B):
+        q = p.single(b)
+        assert conv[b] == 1
+
+        def run_fixed(t, q=q):
+            _, Tq, rq, itq, _ = _gpu_run(q, t)
+            assert itq[0] == t
+            return rq[0], Tq
+        check_stop_iteration(q, it[b], 1e-7, 5, 4000, run_fixed, rep[b], T[b])
+
+
 @pytest.mark.parametrize("maker,path", [(lambda: synthetic.c2_ring(eps_factor=1e-2), "cluster"),
                                         (lambda: synthetic.c2_ring(eps_factor=1e-2), "ldg"),
                                         (lambda: synthetic.c4_large(m=512, n=32), "tma"),
