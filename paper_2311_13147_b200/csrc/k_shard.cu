@@ -19,8 +19,19 @@ __global__ void __launch_bounds__(256) k_colsum(const double* __restrict__ parti
   const int64_t j = (int64_t)blockIdx.x * 32 + lane;
   __shared__ double sh[8][33];
   double acc = 0.0;
-  if (j < m)
-    for (int64_t u = w; u < upp; u += 8) acc += __ldcg(partials + (b * upp + u) * m + j);
+  if (j < m) {
+    // units w, w + 8, ... in order; eight loads in flight per step (one L2 latency per eight units, not one each)
+    const double* pc = partials + b * upp * m + j;
+    int64_t u = w;
+    for (; u + 56 < upp; u += 64) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldcg(pc + (u + 8 * q) * m);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += v[q];
+    }
+    for (; u < upp; u += 8) acc += __ldcg(pc + u * m);
+  }
   sh[w][lane] = acc;
   __syncthreads();
   if (w == 0 && j < m) {
@@ -61,19 +72,31 @@ __global__ void __launch_bounds__(256) k_zupdate(const double* __restrict__ c, i
   __syncthreads();
   if (threadIdx.x == 0) is_last = atomicAdd(&counters[b], 1u) == (unsigned)(ntiles - 1);
   __syncthreads();
-  if (is_last && threadIdx.x == 0) {
+  if (is_last) {
     __threadfence();
+    // the tiles' partial residuals summed in tile order by thread 0, read by the whole warp first (one L2
+    // latency per 32 tiles instead of one per tile)
+    __shared__ double rp[32];
     double r = 0.0;
-    for (int t = 0; t < ntiles; ++t) r += __ldcg(resid_part + b * ntiles + t);
-    r *= (double)n;
-    SolverState& st = state[b];
-    st.residual = r;
-    st.iters += 1;
-    if (tol > 0.0 && st.iters % check_every == 0 && r <= tol) {
-      st.active = 0;
-      st.converged = 1;
+    for (int t0 = 0; t0 < ntiles; t0 += 32) {
+      const int nt = min(32, ntiles - t0);
+      if (lane < nt) rp[lane] = __ldcg(resid_part + b * ntiles + t0 + lane);
+      __syncwarp();
+      if (threadIdx.x == 0)
+        for (int t = 0; t < nt; ++t) r += rp[t];
+      __syncwarp();
     }
-    counters[b] = 0u;
+    if (threadIdx.x == 0) {
+      r *= (double)n;
+      SolverState& st = state[b];
+      st.residual = r;
+      st.iters += 1;
+      if (tol > 0.0 && st.iters % check_every == 0 && r <= tol) {
+        st.active = 0;
+        st.converged = 1;
+      }
+      counters[b] = 0u;
+    }
   }
 }
 
