@@ -15,7 +15,9 @@
 // instead of 80), rho broadcast back by shuffles, the column sums of the 16 warps' fp64 partials in a fixed tree,
 // the q-update and the monitor -- no cluster barrier and no cross-SM hop on the per-iteration critical path (the
 // k_batch_cluster chain has two cluster barriers and a DSMEM column pass per iteration). Bound: the producers'
-// MUFU.EX2 (n*m^2 per problem per iteration on NCL-1 SMs); the chain CTA's SM runs no exponentials.
+// MUFU.EX2 (n*m^2 per problem per iteration on NCL-1 SMs); the chain CTA's SM runs no exponentials. For a batch
+// that fits one wave (latency-bound, C2) and m = 128, TWO chain CTAs split the rows (half the r-pass each) and swap
+// their halves of the column sums through DSMEM once per iteration (see chain_role).
 // Every sum has a fixed order (bitwise reproducible) and nothing is carried across launches but z_hat (the row
 // shift kM_i is the exact per-row maximum every iteration), so launch boundaries do not change the iterates.
 #include <cooperative_groups.h>
@@ -47,7 +49,8 @@ struct ChainParams {
   const double* eps;     // [B]
   SolverState* state;    // [B]
   double* zcache;        // [B][m][3]: z_hat as last written by this kernel, Fz, kz (exact split across launches)
-  int n, m, ncl, RB;     // CTAs per cluster (1 chain + ncl - 1 producers), rows per producer
+  int n, m, ncl, RB;     // CTAs per cluster (nch chain CTAs + ncl - nch producers), rows per producer
+  int nch;               // chain CTAs per cluster: 1, or 2 (m == 128: each holds half of the rows)
   int iters;
   double tol;
   long long check_every;
@@ -67,6 +70,11 @@ __device__ __forceinline__ void st_async_f4(uint32_t addr, float4 v, uint32_t re
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
                    addr),
                "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_b64(uint32_t addr, unsigned long long v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr), "l"(v),
+               "r"(remote_bar)
                : "memory");
 }
 __device__ __forceinline__ void st_cluster_release_u32(uint32_t addr, unsigned v) {
@@ -114,23 +122,32 @@ __device__ __forceinline__ double ldexp_biased(float f, int eb) {
   return __hiloint2double((int)((bits >> 3) + ((unsigned)eb << 20)), (int)(bits << 29));
 }
 
-// The chain CTA: every iteration of the problem on s' from the producers (FULL: m == 128, no masking).
-template <bool FULL>
-__device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b, unsigned char* smem,
+// A chain CTA: every iteration of the problem on s' from the producers (FULL: m == 128, no masking). NCH = 1: the
+// one chain CTA holds all m rows. NCH = 2 (FULL only; the latency-bound regime, C2): chain CTAs 0 and 1 hold rows
+// [0, m/2) and [m/2, m) -- four rows per warp, half the r-pass -- and swap their halves of the column sums once
+// per iteration through DSMEM (st.async + complete_tx on the peer's barrier); both add the halves in the same
+// order (CTA 0's + CTA 1's), so c_j, the q-update, the monitor and the stop decision are bitwise the same in both.
+template <bool FULL, int NCH>
+__device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b, const int crank, unsigned char* smem,
                                            uint64_t* bars, float* sb, const float c2, const SolverState st0) {
+  static_assert(NCH == 1 || (NCH == 2 && FULL), "two chain CTAs need m == 128");
+  constexpr int RPW = kChainRowsPerWarp / NCH;   // rows per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = p.n, m = FULL ? 128 : p.m, mv = m >> 2, NP = p.ncl - 1;   // FULL: compile-time offsets
+  const int n = p.n, m = FULL ? 128 : p.m, mv = m >> 2, NP = p.ncl - NCH;   // FULL: compile-time offsets
+  const int MH = m / NCH;                        // rows of this chain CTA: [row0, row0 + MH)
+  const int row0 = crank * MH;
   const int wps = m + 2;   // warp-partial row stride: the column pass's four row groups fall in two bank halves
   unsigned* stopf = reinterpret_cast<unsigned*>(smem + 64);
-  int* As = reinterpret_cast<int*>(sb + (size_t)2 * m * m);            // [m][m] a_ij
-  double* wpart = reinterpret_cast<double*>(As + (size_t)m * m);       // [16][m + 2] warp column partials
+  int* As = reinterpret_cast<int*>(sb + (size_t)2 * MH * m);           // [MH][m] a_ij
+  double* wpart = reinterpret_cast<double*>(As + (size_t)MH * m);      // [16][m + 2] warp column partials
   double* zf = wpart + (size_t)kChainWarps * wps;                      // [m] Fz_j
   double* bcol = zf + m;                                               // [m] beta_j
-  double* rstat = bcol + m;                                            // [m][2] kM_i ln2, r_i
-  double* red = rstat + 2 * m;                                         // [32]
+  double* rstat = bcol + m;                                            // [MH][2] kM_i ln2, r_i
+  double* red = rstat + 2 * MH;                                        // [32]
   int* zk = reinterpret_cast<int*>(red + 32);                          // [m] kz_j + 896 (biased: see ldexp_biased)
-  for (int idx = threadIdx.x; idx < m * m; idx += kChainThreads)
-    As[idx] = __float2int_rn(__ldg(p.G + (size_t)b * m * m + idx) * c2);
+  double* xh = reinterpret_cast<double*>(zk + m);                      // NCH = 2: [2][2][m] column-sum halves
+  for (int idx = threadIdx.x; idx < MH * m; idx += kChainThreads)
+    As[idx] = __float2int_rn(__ldg(p.G + ((size_t)b * m + row0) * m + idx) * c2);
   // z_hat_j log2e = kz_j + log2 Fz_j: the split this kernel left in the workspace when z_hat still holds exactly
   // what it wrote (a launch continuing the previous one: no rounding at launch boundaries), else split afresh
   double* zc = p.zcache + (size_t)b * m * 3;
@@ -150,13 +167,19 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     }
     bcol[j] = p.beta[b * m + j];
   }
-  // after the transposed butterfly lane l holds the sum of the warp's row kk = 4 b4 + 2 b3 + b2 (bits of l)
-  const int kk = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-  const int my_i = warp + kk * kChainWarps;
+  // after the transposed butterfly lane l holds the sum of the warp's row kk (RPW = 8: kk = 4 b4 + 2 b3 + b2,
+  // RPW = 4: kk = 2 b4 + b3, with bi the bits of l)
+  const int kk = RPW == 8 ? ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)
+                          : ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+  const int my_i = warp + kk * kChainWarps;   // local row
   const bool my_valid = FULL || my_i < m;
-  const double my_alpha = my_valid ? p.alpha[b * m + my_i] : 0.0;
+  const double my_alpha = my_valid ? p.alpha[b * m + row0 + my_i] : 0.0;
   const bool lane_ok = FULL || lane < mv;
   const int jc = lane_ok ? lane : 0;
+  // the peer chain CTA's copy of this CTA's column-sum half, and its barrier (NCH = 2)
+  const uint32_t peer = (uint32_t)(crank ^ 1);
+  const uint32_t xh_peer = NCH == 2 ? mapa_u32(smem_u32(xh), peer) : 0u;
+  const uint32_t xbar_peer = NCH == 2 ? mapa_u32(smem_u32(&bars[5]), peer) : 0u;
   __syncthreads();
   SolverState st = st0;
   bool underflow = false;
@@ -169,25 +192,35 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     while (!mbar_test_cta(&bars[q], (uint32_t)((t >> 1) & 1))) {
     }
     // arm buffer q for iteration t + 2 (its phase of iteration t has completed; the producers fill it only after
-    // the free signal below)
-    if (threadIdx.x == 0 && t + 2 < p.iters) mbar_arrive_expect_tx(&bars[q], (uint32_t)(m * m * 4));
+    // the free signal below); NCH = 2: arm this iteration's column-half exchange (the peer's bytes may land
+    // before the arming: the transaction count goes negative until then, and the phase cannot complete early
+    // since the arrival is still pending)
+    if (threadIdx.x == 0 && t + 2 < p.iters) mbar_arrive_expect_tx(&bars[q], (uint32_t)(MH * m * 4));
+    if (NCH == 2 && threadIdx.x == 0) mbar_arrive_expect_tx(&bars[5 + q], (uint32_t)(m * 8));
     const long long c1t = p.trace ? clock64() : 0;
     if (p.diag & 2) {   // diagnostics: producers alone
-      if (threadIdx.x < NP) mbar_arrive_cluster_relaxed(mapa_u32(smem_u32(&bars[2 + q]), (uint32_t)threadIdx.x + 1));
+      if (threadIdx.x < NP)
+        mbar_arrive_cluster_relaxed(mapa_u32(smem_u32(&bars[2 + q]), (uint32_t)(threadIdx.x + NCH)));
+      if (NCH == 2) {   // keep the exchange's phases moving: send zeros
+        if (threadIdx.x < m)
+          st_async_b64(xh_peer + (uint32_t)(((q * 2 + crank) * m + threadIdx.x) * 8), 0ull, xbar_peer + 8u * q);
+        while (!mbar_test_cta(&bars[5 + q], (uint32_t)((t >> 1) & 1))) {
+        }
+      }
       st.iters += 1;
       continue;
     }
-    // ---- r-pass: the warp's 8 rows, one float4 of columns per lane:
+    // ---- r-pass: the warp's RPW rows, one float4 of columns per lane:
     //      u_ij = s'_ij 2^{kz_j - a_ij - kM_i},  r_i = sum_j u_ij Fz_j,  P_j = Fz_j sum_i rho_i u_ij
     const int4 k4 = reinterpret_cast<const int4*>(zk)[jc];
     const double2 fa = reinterpret_cast<const double2*>(zf)[2 * jc];
     const double2 fb = reinterpret_cast<const double2*>(zf)[2 * jc + 1];
     const double fz[4] = {fa.x, fa.y, fb.x, fb.y};
-    const float* sq = sb + (size_t)q * m * m;
-    double uu[kChainRowsPerWarp][4], ls[kChainRowsPerWarp];
-    int kM[kChainRowsPerWarp];
+    const float* sq = sb + (size_t)q * MH * m;
+    double uu[RPW][4], ls[RPW];
+    int kM[RPW];
 #pragma unroll
-    for (int k = 0; k < kChainRowsPerWarp; ++k) {
+    for (int k = 0; k < RPW; ++k) {
       const int i = warp + k * kChainWarps;
       const bool ok = FULL || (i < m && lane < mv);
       const int ic = FULL || i < m ? i : 0;
@@ -206,30 +239,41 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
         ls[k] = fma(uu[k][v], fz[v], ls[k]);
       }
     }
-    // eight row sums by a transposed butterfly: each level keeps half of the rows and sends the other half
+    // the RPW row sums by a transposed butterfly: each level keeps half of the rows and sends the other half
     const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
-    double a4s[4], a2s[2];
+    double r;
+    if constexpr (RPW == 8) {
+      double a4s[4], a2s[2];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      a4s[k] = (h4 ? ls[k + 4] : ls[k]) + __shfl_xor_sync(0xffffffffu, h4 ? ls[k] : ls[k + 4], 16);
+      for (int k = 0; k < 4; ++k)
+        a4s[k] = (h4 ? ls[k + 4] : ls[k]) + __shfl_xor_sync(0xffffffffu, h4 ? ls[k] : ls[k + 4], 16);
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
-      a2s[k] = (h3 ? a4s[k + 2] : a4s[k]) + __shfl_xor_sync(0xffffffffu, h3 ? a4s[k] : a4s[k + 2], 8);
-    double r = (h2 ? a2s[1] : a2s[0]) + __shfl_xor_sync(0xffffffffu, h2 ? a2s[0] : a2s[1], 4);
+      for (int k = 0; k < 2; ++k)
+        a2s[k] = (h3 ? a4s[k + 2] : a4s[k]) + __shfl_xor_sync(0xffffffffu, h3 ? a4s[k] : a4s[k + 2], 8);
+      r = (h2 ? a2s[1] : a2s[0]) + __shfl_xor_sync(0xffffffffu, h2 ? a2s[0] : a2s[1], 4);
+    } else {
+      double a2s[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        a2s[k] = (h4 ? ls[k + 2] : ls[k]) + __shfl_xor_sync(0xffffffffu, h4 ? ls[k] : ls[k + 2], 16);
+      r = (h3 ? a2s[1] : a2s[0]) + __shfl_xor_sync(0xffffffffu, h3 ? a2s[0] : a2s[1], 8);
+      r += __shfl_xor_sync(0xffffffffu, r, 4);
+    }
     r += __shfl_xor_sync(0xffffffffu, r, 2);
     r += __shfl_xor_sync(0xffffffffu, r, 1);
     const double rho_my = my_valid ? my_alpha * __drcp_rn(r) : 0.0;   // alpha_i / r_i (this SM's MUFU is idle)
-    if (need && (lane & 3) == 0 && my_valid) {   // the row statistics of w_hat (kept for the last iteration)
+    if (need && (lane & (32 / RPW - 1)) == 0 && my_valid) {   // the row statistics of w_hat (last iteration)
       int km = 0;
 #pragma unroll
-      for (int k = 0; k < kChainRowsPerWarp; ++k) km = k == kk ? kM[k] : km;
+      for (int k = 0; k < RPW; ++k) km = k == kk ? kM[k] : km;
       rstat[2 * my_i] = (double)km * COT_LN2;
       rstat[2 * my_i + 1] = r;
     }
     double P[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int k = 0; k < kChainRowsPerWarp; ++k) {   // rows in order
-      const int src = ((k >> 2) & 1) * 16 + ((k >> 1) & 1) * 8 + (k & 1) * 4;
+    for (int k = 0; k < RPW; ++k) {   // rows in order
+      const int src = RPW == 8 ? ((k >> 2) & 1) * 16 + ((k >> 1) & 1) * 8 + (k & 1) * 4
+                               : ((k >> 1) & 1) * 16 + (k & 1) * 8;
       const double rho = __shfl_sync(0xffffffffu, rho_my, src);
 #pragma unroll
       for (int v = 0; v < 4; ++v) P[v] = fma(rho, uu[k][v], P[v]);
@@ -242,7 +286,8 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     __syncthreads();
     const long long c2t = p.trace ? clock64() : 0;
     // s' buffer q has been read: the producers may fill it with iteration t + 2
-    if (threadIdx.x < NP) mbar_arrive_cluster_relaxed(mapa_u32(smem_u32(&bars[2 + q]), (uint32_t)threadIdx.x + 1));
+    if (threadIdx.x < NP)
+      mbar_arrive_cluster_relaxed(mapa_u32(smem_u32(&bars[2 + q]), (uint32_t)(threadIdx.x + NCH)));
     // ---- column pass: 4 threads per column (4 warps' partials each, then a fixed xor tree) and the q-update
     //      z_hat_j += log beta_j - log c_j carried on the split: Fz_j beta_j / c_j = M 2^E, M in [2^-1/2, 2^1/2)
     //      -> kz_j += E, Fz_j = M (no log, no exp on the critical path)
@@ -255,6 +300,17 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     }
     c += __shfl_xor_sync(0xffffffffu, c, 1);   // (a0 + a1) + (a2 + a3) in every lane of the group: the
     c += __shfl_xor_sync(0xffffffffu, c, 2);   // additions commute bitwise
+    if constexpr (NCH == 2) {   // swap the halves: c_j = (CTA 0's half) + (CTA 1's half) in both CTAs
+      double* xq = xh + (size_t)q * 2 * m;
+      if (g == 0) {
+        xq[crank * m + col] = c;
+        st_async_b64(xh_peer + (uint32_t)(((q * 2 + crank) * m + col) * 8), (unsigned long long)__double_as_longlong(c),
+                     xbar_peer + 8u * q);
+      }
+      while (!mbar_test_cta(&bars[5 + q], (uint32_t)((t >> 1) & 1))) {
+      }
+      c = xq[col] + xq[m + col];
+    }
     double dev = 0.0;
     if (cok && g == 0) {
       const double bj = bcol[col];
@@ -302,20 +358,26 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     tp[1] = cr;
     tp[2] = cc;
   }
-  // stop the producers (they may be up to two iterations ahead, waiting for a buffer)
-  if (threadIdx.x < NP) st_cluster_release_u32(mapa_u32(smem_u32(stopf), (uint32_t)threadIdx.x + 1), 1u);
-  for (int i = threadIdx.x; i < m; i += kChainThreads)
-    if (t > 0) p.w_hat[b * m + i] = log(p.alpha[b * m + i]) - rstat[2 * i] - log(rstat[2 * i + 1]);
-  for (int j = threadIdx.x; j < m; j += kChainThreads) {   // z_hat_j = (kz_j + log2 Fz_j) ln 2, and its split
-    const int kz = zk[j] - 896;
-    const double z = (double)kz * COT_LN2 + log(zf[j]);
-    p.z_hat[b * m + j] = z;
-    zc[3 * j] = z;
-    zc[3 * j + 1] = zf[j];
-    zc[3 * j + 2] = (double)kz;
-  }
+  // stop the producers (they may be up to two iterations ahead, waiting for a buffer); with two chain CTAs both
+  // stop at the same iteration (identical decisions) and CTA 0 signals
+  if (crank == 0 && threadIdx.x < NP)
+    st_cluster_release_u32(mapa_u32(smem_u32(stopf), (uint32_t)(threadIdx.x + NCH)), 1u);
+  for (int i = threadIdx.x; i < MH; i += kChainThreads)
+    if (t > 0) {
+      const int64_t gi = b * m + row0 + i;
+      p.w_hat[gi] = log(p.alpha[gi]) - rstat[2 * i] - log(rstat[2 * i + 1]);
+    }
+  if (crank == 0)
+    for (int j = threadIdx.x; j < m; j += kChainThreads) {   // z_hat_j = (kz_j + log2 Fz_j) ln 2, and its split
+      const int kz = zk[j] - 896;
+      const double z = (double)kz * COT_LN2 + log(zf[j]);
+      p.z_hat[b * m + j] = z;
+      zc[3 * j] = z;
+      zc[3 * j + 1] = zf[j];
+      zc[3 * j + 2] = (double)kz;
+    }
   if (underflow) atomicOr(&p.state[b].flags, (int)STATE_UNDERFLOW);
-  if (threadIdx.x == 0) {
+  if (crank == 0 && threadIdx.x == 0) {
     SolverState out = p.state[b];
     out.iters = st.iters;
     out.residual = st.residual;
@@ -333,9 +395,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
   const int64_t b = blockIdx.x / ncl;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = p.n, m = p.m, mv = m >> 2;
-  // header: [0] [1] chain: s' buffer q full (one arrival -- the chain's own expect_tx of m*m*4 bytes -- and the
-  // producers' st.async transaction bytes per phase); [2] [3] producer: s' buffer q free (one arrival by the chain
-  // per phase); [4] producer: cost rows loaded; stop flag at byte 64
+  // header: [0] [1] chain: s' buffer q full (one arrival -- the chain's own expect_tx of its rows' bytes -- and the
+  // producers' st.async transaction bytes per phase); [2] [3] producer: s' buffer q free (one arrival by each chain
+  // CTA per phase); [4] producer: cost rows loaded; [5] [6] chain (nch = 2): the peer's column-sum half of
+  // iteration parity q arrived; stop flag at byte 64
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   unsigned* stopf = reinterpret_cast<unsigned*>(smem + 64);
   float* sbuf = reinterpret_cast<float*>(smem + kChainHeader);   // chain: [2][m][m] s'; producer: C rows
@@ -344,16 +407,20 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
   if (!st0.active) return;                                        // cluster-uniform
   const double inv_eps = 1.0 / p.eps[b];
   const float c2 = (float)(COT_LOG2E * inv_eps);
+  const int nch = p.nch;
   if (threadIdx.x == 0) {
-    if (crank == 0) {
+    if (crank < nch) {
+      const uint32_t bytes = (uint32_t)(m / nch * m * 4);
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
+      mbar_init(&bars[5], 1);
+      mbar_init(&bars[6], 1);
       // arm the buffers of iterations 0 and 1 (an armed phase that never receives data is never waited on)
-      if (p.iters > 0) mbar_arrive_expect_tx(&bars[0], (uint32_t)(m * m * 4));
-      if (p.iters > 1) mbar_arrive_expect_tx(&bars[1], (uint32_t)(m * m * 4));
+      if (p.iters > 0) mbar_arrive_expect_tx(&bars[0], bytes);
+      if (p.iters > 1) mbar_arrive_expect_tx(&bars[1], bytes);
     } else {
-      mbar_init(&bars[2], 1);
-      mbar_init(&bars[3], 1);
+      mbar_init(&bars[2], (uint32_t)nch);
+      mbar_init(&bars[3], (uint32_t)nch);
       mbar_init(&bars[4], 1);
     }
     *stopf = 0u;
@@ -361,9 +428,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
   }
   cluster.sync();
 
-  if (crank > 0) {
+  if (crank >= nch) {
     // ============================================================================ producer
-    const int i0 = (crank - 1) * p.RB;
+    const int i0 = (crank - nch) * p.RB;
     const int nrows = max(0, min(p.RB, m - i0));
     float* Cs = sbuf;                                             // [nrows][n][m]
     if (threadIdx.x == 0 && nrows > 0) {
@@ -392,8 +459,17 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
       }
     }
     if (nrows > 0) mbar_wait(&bars[4], 0);
-    const uint32_t rs_buf = mapa_u32(smem_u32(sbuf), 0);
-    const uint32_t rfull = mapa_u32(smem_u32(&bars[0]), 0);
+    // destination of each of the warp's rows: the chain CTA holding it (nch = 2: rows [0, m/2) in CTA 0, the rest
+    // in CTA 1), its local row there, that CTA's s' buffers and full barriers
+    const int mh = m / nch;
+    uint32_t rs_buf[2], rfull[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int gi = i0 + warp + rr * kChainWarps;
+      const int dc = min(gi / mh, nch - 1);
+      rs_buf[rr] = mapa_u32(smem_u32(sbuf), (uint32_t)dc) + (uint32_t)((gi - dc * mh) * m * 4);
+      rfull[rr] = mapa_u32(smem_u32(&bars[0]), (uint32_t)dc);
+    }
     long long tk = 0, tw = 0, tsv = 0;
     for (int t = 0; t < p.iters; ++t) {
       const long long c0t = p.trace ? clock64() : 0;
@@ -460,8 +536,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
       for (int rr = 0; rr < 2; ++rr) {
         const int i = warp + rr * kChainWarps;
         if (i < nrows && lane < mv)
-          st_async_f4(rs_buf + (uint32_t)((((size_t)q * m + i0 + i) * m + 4 * lane) * 4),
-                      make_float4(s[rr][0], s[rr][1], s[rr][2], s[rr][3]), rfull + 8u * (uint32_t)q);
+          st_async_f4(rs_buf[rr] + (uint32_t)(((size_t)q * mh * m + 4 * lane) * 4),
+                      make_float4(s[rr][0], s[rr][1], s[rr][2], s[rr][3]), rfull[rr] + 8u * (uint32_t)q);
       }
       if (p.trace) {
         const long long c3t = clock64();
@@ -478,35 +554,43 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
     }
   } else {
     // ============================================================================ chain
-    if (m == kChainWarps * kChainRowsPerWarp)
-      chain_role<true>(p, b, smem, bars, sbuf, c2, st0);
-    else
-      chain_role<false>(p, b, smem, bars, sbuf, c2, st0);
+    if (m == kChainWarps * kChainRowsPerWarp) {
+      if (nch == 2)
+        chain_role<true, 2>(p, b, crank, smem, bars, sbuf, c2, st0);
+      else
+        chain_role<true, 1>(p, b, crank, smem, bars, sbuf, c2, st0);
+    } else {
+      chain_role<false, 1>(p, b, crank, smem, bars, sbuf, c2, st0);
+    }
   }
   cluster.sync();   // no CTA leaves while another may still write into its shared memory
 }
 // ------------------------------------------------------------------------------------------ launcher
 namespace {
 struct ChainCfg {
-  int ncl, RB;
+  int ncl, RB, nch;
   size_t smem;
 };
 
-size_t chain_smem_chain(int64_t m) {   // s' x 2, a_ij, warp partials, Fz, beta, row stats, scratch, kz
-  return kChainHeader + (size_t)2 * m * m * 4 + (size_t)m * m * 4 + (size_t)kChainWarps * (m + 2) * 8 + (size_t)m * 8 +
-         (size_t)m * 8 + (size_t)m * 16 + 32 * 8 + (size_t)m * 4;
+// chain CTA: s' x 2 and a_ij of its mh rows, warp partials, Fz, beta, row stats, scratch, kz, column-sum halves
+size_t chain_smem_chain(int64_t m, int nch) {
+  const int64_t mh = m / nch;
+  return kChainHeader + (size_t)2 * mh * m * 4 + (size_t)mh * m * 4 + (size_t)kChainWarps * (m + 2) * 8 +
+         (size_t)m * 8 + (size_t)m * 8 + (size_t)mh * 16 + 32 * 8 + (size_t)m * 4 + (nch == 2 ? (size_t)4 * m * 8 : 0);
 }
 
-bool chain_shape(int64_t n, int64_t m, int ncl, ChainCfg* c) {
-  const int np = ncl - 1;
+bool chain_shape(int64_t n, int64_t m, int ncl, int nch, ChainCfg* c) {
+  const int np = ncl - nch;
   if (np < 1 || m < 1) return false;
+  if (nch == 2 && m != kChainWarps * kChainRowsPerWarp) return false;   // two chain CTAs: m == 128 only
   const int RB = (int)((m + np - 1) / np);
   if (RB > 2 * kChainWarps) return false;   // two rows per producer warp
   const size_t prod = kChainHeader + (size_t)RB * n * m * 4;
-  const size_t smem = std::max(prod, chain_smem_chain(m));
+  const size_t smem = std::max(prod, chain_smem_chain(m, nch));
   if (smem > 226 * 1024) return false;
   c->ncl = ncl;
   c->RB = RB;
+  c->nch = nch;
   c->smem = smem;
   return true;
 }
@@ -538,18 +622,23 @@ int chain_active_clusters(const ChainCfg& c) {
   return nact;
 }
 
-// Shape: 8-CTA clusters (7 producers: the shortest producer pass) while the batch fits one wave of them (latency:
-// C2), else 6-CTA clusters (22 co-resident vs 15: throughput, C5), else any feasible size. COT_CHAIN_NCL forces.
+// Shape: 8-CTA clusters while the batch fits one wave of them (latency: C2) -- with two chain CTAs splitting the
+// rows when m == 128 (6 producers), else one (7 producers) --, else 6-CTA clusters with one chain CTA (22
+// co-resident vs 15: throughput, C5), else any feasible size. COT_CHAIN_NCL / COT_CHAIN_NCH force.
 bool chain_config(int64_t n, int64_t m, int64_t B, ChainCfg* c) {
-  if (const char* ev = getenv("COT_CHAIN_NCL")) return chain_shape(n, m, atoi(ev), c);
+  const char* nchv = getenv("COT_CHAIN_NCH");
+  const int nch_forced = nchv ? std::max(1, std::min(2, atoi(nchv))) : 0;
+  if (const char* ev = getenv("COT_CHAIN_NCL")) return chain_shape(n, m, atoi(ev), nch_forced ? nch_forced : 1, c);
   ChainCfg c8;
-  const bool h8 = chain_shape(n, m, 8, &c8);
+  const int nch8 = nch_forced ? nch_forced : (m == kChainWarps * kChainRowsPerWarp ? 2 : 1);
+  const bool h8 = chain_shape(n, m, 8, nch8, &c8) || (nch8 == 2 && !nch_forced && chain_shape(n, m, 8, 1, &c8));
   if (h8 && B > 0 && B <= chain_active_clusters(c8)) {
     *c = c8;
     return true;
   }
   for (int ncl : {6, 7, 5, 8, 4, 3, 2})
-    if (chain_shape(n, m, ncl, c) && (B <= 0 || chain_active_clusters(*c) > 0)) return true;
+    if (chain_shape(n, m, ncl, nch_forced ? nch_forced : 1, c) && (B <= 0 || chain_active_clusters(*c) > 0))
+      return true;
   return false;
 }
 }  // namespace
@@ -581,6 +670,7 @@ cudaError_t launch_batch_chain(const IterArgs& a, const Workspace& ws, int iters
   p.m = (int)a.m;
   p.ncl = cc.ncl;
   p.RB = cc.RB;
+  p.nch = cc.nch;
   p.iters = iters;
   p.tol = a.tol;
   p.check_every = a.check_every > 0 ? a.check_every : 1;
@@ -619,10 +709,10 @@ cudaError_t launch_batch_chain(const IterArgs& a, const Workspace& ws, int iters
     for (int c = 0; c < nb * cc.ncl; ++c)
       for (int k = 0; k < 3; ++k) {
         const double v = (double)h[(size_t)c * 8 + k] / std::max(iters, 1);
-        if (c % cc.ncl == 0) ch[k] += v / nb; else pr[k] += v / nb / (cc.ncl - 1);
+        if (c % cc.ncl < cc.nch) ch[k] += v / nb / cc.nch; else pr[k] += v / nb / (cc.ncl - cc.nch);
       }
-    fprintf(stderr, "[cot chain trace] cluster %d, %d problems traced; per-iter cycles: chain wait %.0f r-pass %.0f "
-            "col-pass %.0f | producer k-sum %.0f wait-free %.0f store %.0f\n", cc.ncl, nb, ch[0], ch[1], ch[2],
+    fprintf(stderr, "[cot chain trace] cluster %d (%d chain CTAs), %d problems traced; per-iter cycles: chain wait %.0f "
+            "r-pass %.0f col-pass %.0f | producer k-sum %.0f wait-free %.0f store %.0f\n", cc.ncl, cc.nch, nb, ch[0], ch[1], ch[2],
             pr[0], pr[1], pr[2]);
   }
   return e;

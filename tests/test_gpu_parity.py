@@ -505,6 +505,32 @@ def test_chain_kernel_launch_boundaries_bitwise():
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
+@pytest.mark.parametrize("nch", [1, 2])
+def test_chain_kernel_one_or_two_chain_ctas(nch):
+    """k_batch_chain with one chain CTA per problem and with two (rows split in halves, the column-sum halves
+    swapped through DSMEM every iteration: the default while a batch of m = 128 problems fits one wave of
+    8-CTA clusters, as C2): the C2 sweep batch against the oracle after 40 iterations, and launch boundaries
+    (40 = 13 + 27) bitwise."""
+    p = synthetic.c2_sweep()
+    out = []
+    with _env(COT_CHAIN_NCH=str(nch)):
+        assert cot.lib().cot_iter_path(p.B, p.n, p.m, 0, 0) == 3
+        for split in ([40], [13, 27]):
+            prob = cot.CerotProblem(_dev(p.C), _dev(p.alpha), _dev(p.beta), _dev(p.eps)).init()
+            for k in split:
+                prob.iterate(k)
+            T, rep = prob.plan(T_blocks=True)
+            torch.cuda.synchronize()
+            out.append((prob.w_hat.cpu().numpy(), prob.z_hat.cpu().numpy(), T.cpu().numpy(), rep.cpu().numpy()))
+    for a, b in zip(out[0][:2], out[1][:2]):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    T, rep = out[0][2], out[0][3]
+    for b in range(p.B):
+        q = p.single(b)
+        w, z, _, _ = oracle.cyclic_sinkhorn(q.alpha, q.beta, q.C, float(q.eps[0]), 40, form="kernel")
+        _compare(q, rep[b], T[b], w, z)
+
+
 @pytest.mark.parametrize("maker,path", [(lambda: synthetic.c1_tiny(), 0), (lambda: synthetic.c3_image(pair=1), 1),
                                         (lambda: synthetic.c2_ring(eps_factor=1e-1), 3)],
                          ids=["C1_ldg_graph_loop", "C3_tma_one_launch", "C2_chain_one_launch"])
