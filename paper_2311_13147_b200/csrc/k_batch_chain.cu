@@ -16,8 +16,8 @@
 // the q-update and the monitor -- no cluster barrier and no cross-SM hop on the per-iteration critical path (the
 // k_batch_cluster chain has two cluster barriers and a DSMEM column pass per iteration). Bound: the producers'
 // MUFU.EX2 (n*m^2 per problem per iteration on NCL-1 SMs); the chain CTA's SM runs no exponentials. For a batch
-// that fits one wave (latency-bound, C2) and m = 128, TWO chain CTAs split the rows (half the r-pass each) and swap
-// their halves of the column sums through DSMEM once per iteration (see chain_role).
+// that fits one wave (latency-bound, C2) and m = 128, two or four chain CTAs split the rows (a half or a quarter
+// of the r-pass each) and exchange their parts of the column sums through DSMEM once per iteration (chain_role).
 // Every sum has a fixed order (bitwise reproducible) and nothing is carried across launches but z_hat (the row
 // shift kM_i is the exact per-row maximum every iteration), so launch boundaries do not change the iterates.
 #include <cooperative_groups.h>
@@ -123,14 +123,15 @@ __device__ __forceinline__ double ldexp_biased(float f, int eb) {
 }
 
 // A chain CTA: every iteration of the problem on s' from the producers (FULL: m == 128, no masking). NCH = 1: the
-// one chain CTA holds all m rows. NCH = 2 (FULL only; the latency-bound regime, C2): chain CTAs 0 and 1 hold rows
-// [0, m/2) and [m/2, m) -- four rows per warp, half the r-pass -- and swap their halves of the column sums once
-// per iteration through DSMEM (st.async + complete_tx on the peer's barrier); both add the halves in the same
-// order (CTA 0's + CTA 1's), so c_j, the q-update, the monitor and the stop decision are bitwise the same in both.
+// one chain CTA holds all m rows. NCH = 2 or 4 (FULL only; the latency-bound regime, C2): chain CTA c holds rows
+// [c m/NCH, (c+1) m/NCH) -- 8/NCH rows per warp, 1/NCH of the r-pass -- and sends its part of the column sums to
+// the other chain CTAs once per iteration through DSMEM (st.async + complete_tx on their barriers); all add the
+// parts in the same order (((part 0 + part 1) + part 2) + part 3), so c_j, the q-update, the monitor and the stop
+// decision are bitwise the same in every chain CTA.
 template <bool FULL, int NCH>
 __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b, const int crank, unsigned char* smem,
                                            uint64_t* bars, float* sb, const float c2, const SolverState st0) {
-  static_assert(NCH == 1 || (NCH == 2 && FULL), "two chain CTAs need m == 128");
+  static_assert(NCH == 1 || ((NCH == 2 || NCH == 4) && FULL), "several chain CTAs need m == 128");
   constexpr int RPW = kChainRowsPerWarp / NCH;   // rows per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = p.n, m = FULL ? 128 : p.m, mv = m >> 2, NP = p.ncl - NCH;   // FULL: compile-time offsets
@@ -145,7 +146,7 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
   double* rstat = bcol + m;                                            // [MH][2] kM_i ln2, r_i
   double* red = rstat + 2 * MH;                                        // [32]
   int* zk = reinterpret_cast<int*>(red + 32);                          // [m] kz_j + 896 (biased: see ldexp_biased)
-  double* xh = reinterpret_cast<double*>(zk + m);                      // NCH = 2: [2][2][m] column-sum halves
+  double* xh = reinterpret_cast<double*>(zk + m);                      // NCH > 1: [2][NCH][m] column-sum parts
   for (int idx = threadIdx.x; idx < MH * m; idx += kChainThreads)
     As[idx] = __float2int_rn(__ldg(p.G + ((size_t)b * m + row0) * m + idx) * c2);
   // z_hat_j log2e = kz_j + log2 Fz_j: the split this kernel left in the workspace when z_hat still holds exactly
@@ -168,18 +169,21 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     bcol[j] = p.beta[b * m + j];
   }
   // after the transposed butterfly lane l holds the sum of the warp's row kk (RPW = 8: kk = 4 b4 + 2 b3 + b2,
-  // RPW = 4: kk = 2 b4 + b3, with bi the bits of l)
-  const int kk = RPW == 8 ? ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)
-                          : ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+  // RPW = 4: kk = 2 b4 + b3, RPW = 2: kk = b4, with bi the bits of l)
+  const int kk = RPW == 8   ? ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)
+                 : RPW == 4 ? ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1)
+                            : ((lane >> 4) & 1);
   const int my_i = warp + kk * kChainWarps;   // local row
   const bool my_valid = FULL || my_i < m;
   const double my_alpha = my_valid ? p.alpha[b * m + row0 + my_i] : 0.0;
   const bool lane_ok = FULL || lane < mv;
   const int jc = lane_ok ? lane : 0;
-  // the peer chain CTA's copy of this CTA's column-sum half, and its barrier (NCH = 2)
-  const uint32_t peer = (uint32_t)(crank ^ 1);
-  const uint32_t xh_peer = NCH == 2 ? mapa_u32(smem_u32(xh), peer) : 0u;
-  const uint32_t xbar_peer = NCH == 2 ? mapa_u32(smem_u32(&bars[5]), peer) : 0u;
+  // NCH > 1: thread g < NCH - 1 of a column group sends this CTA's part of the column sums to chain CTA
+  // (crank + 1 + g) % NCH: that CTA's copy of the parts, and its barrier
+  const int gsend = threadIdx.x & 3;
+  const uint32_t peer = (uint32_t)((crank + 1 + gsend) % NCH);
+  const uint32_t xh_peer = NCH > 1 ? mapa_u32(smem_u32(xh), peer) : 0u;
+  const uint32_t xbar_peer = NCH > 1 ? mapa_u32(smem_u32(&bars[5]), peer) : 0u;
   __syncthreads();
   SolverState st = st0;
   bool underflow = false;
@@ -196,14 +200,15 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     // before the arming: the transaction count goes negative until then, and the phase cannot complete early
     // since the arrival is still pending)
     if (threadIdx.x == 0 && t + 2 < p.iters) mbar_arrive_expect_tx(&bars[q], (uint32_t)(MH * m * 4));
-    if (NCH == 2 && threadIdx.x == 0) mbar_arrive_expect_tx(&bars[5 + q], (uint32_t)(m * 8));
+    if (NCH > 1 && threadIdx.x == 0) mbar_arrive_expect_tx(&bars[5 + q], (uint32_t)((NCH - 1) * m * 8));
     const long long c1t = p.trace ? clock64() : 0;
     if (p.diag & 2) {   // diagnostics: producers alone
       if (threadIdx.x < NP)
         mbar_arrive_cluster_relaxed(mapa_u32(smem_u32(&bars[2 + q]), (uint32_t)(threadIdx.x + NCH)));
-      if (NCH == 2) {   // keep the exchange's phases moving: send zeros
-        if (threadIdx.x < m)
-          st_async_b64(xh_peer + (uint32_t)(((q * 2 + crank) * m + threadIdx.x) * 8), 0ull, xbar_peer + 8u * q);
+      if (NCH > 1) {   // keep the exchange's phases moving: send zeros
+        if (gsend < NCH - 1)
+          st_async_b64(xh_peer + (uint32_t)(((q * NCH + crank) * m + (threadIdx.x >> 2)) * 8), 0ull,
+                       xbar_peer + 8u * q);
         while (!mbar_test_cta(&bars[5 + q], (uint32_t)((t >> 1) & 1))) {
         }
       }
@@ -251,12 +256,16 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
       for (int k = 0; k < 2; ++k)
         a2s[k] = (h3 ? a4s[k + 2] : a4s[k]) + __shfl_xor_sync(0xffffffffu, h3 ? a4s[k] : a4s[k + 2], 8);
       r = (h2 ? a2s[1] : a2s[0]) + __shfl_xor_sync(0xffffffffu, h2 ? a2s[0] : a2s[1], 4);
-    } else {
+    } else if constexpr (RPW == 4) {
       double a2s[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k)
         a2s[k] = (h4 ? ls[k + 2] : ls[k]) + __shfl_xor_sync(0xffffffffu, h4 ? ls[k] : ls[k + 2], 16);
       r = (h3 ? a2s[1] : a2s[0]) + __shfl_xor_sync(0xffffffffu, h3 ? a2s[0] : a2s[1], 8);
+      r += __shfl_xor_sync(0xffffffffu, r, 4);
+    } else {
+      r = (h4 ? ls[1] : ls[0]) + __shfl_xor_sync(0xffffffffu, h4 ? ls[0] : ls[1], 16);
+      r += __shfl_xor_sync(0xffffffffu, r, 8);
       r += __shfl_xor_sync(0xffffffffu, r, 4);
     }
     r += __shfl_xor_sync(0xffffffffu, r, 2);
@@ -272,8 +281,9 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     double P[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int k = 0; k < RPW; ++k) {   // rows in order
-      const int src = RPW == 8 ? ((k >> 2) & 1) * 16 + ((k >> 1) & 1) * 8 + (k & 1) * 4
-                               : ((k >> 1) & 1) * 16 + (k & 1) * 8;
+      const int src = RPW == 8   ? ((k >> 2) & 1) * 16 + ((k >> 1) & 1) * 8 + (k & 1) * 4
+                      : RPW == 4 ? ((k >> 1) & 1) * 16 + (k & 1) * 8
+                                 : k * 16;
       const double rho = __shfl_sync(0xffffffffu, rho_my, src);
 #pragma unroll
       for (int v = 0; v < 4; ++v) P[v] = fma(rho, uu[k][v], P[v]);
@@ -300,16 +310,19 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     }
     c += __shfl_xor_sync(0xffffffffu, c, 1);   // (a0 + a1) + (a2 + a3) in every lane of the group: the
     c += __shfl_xor_sync(0xffffffffu, c, 2);   // additions commute bitwise
-    if constexpr (NCH == 2) {   // swap the halves: c_j = (CTA 0's half) + (CTA 1's half) in both CTAs
-      double* xq = xh + (size_t)q * 2 * m;
-      if (g == 0) {
-        xq[crank * m + col] = c;
-        st_async_b64(xh_peer + (uint32_t)(((q * 2 + crank) * m + col) * 8), (unsigned long long)__double_as_longlong(c),
-                     xbar_peer + 8u * q);
-      }
+    if constexpr (NCH > 1) {   // swap the parts: c_j = ((part 0 + part 1) + part 2) + part 3 in every chain CTA
+      double* xq = xh + (size_t)q * NCH * m;
+      if (g == 0) xq[crank * m + col] = c;
+      if (g < NCH - 1)
+        st_async_b64(xh_peer + (uint32_t)(((q * NCH + crank) * m + col) * 8),
+                     (unsigned long long)__double_as_longlong(c), xbar_peer + 8u * q);
       while (!mbar_test_cta(&bars[5 + q], (uint32_t)((t >> 1) & 1))) {
       }
-      c = xq[col] + xq[m + col];
+      if (g == 0) {
+        c = xq[col];
+#pragma unroll
+        for (int h = 1; h < NCH; ++h) c += xq[h * m + col];
+      }
     }
     double dev = 0.0;
     if (cok && g == 0) {
@@ -358,8 +371,8 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     tp[1] = cr;
     tp[2] = cc;
   }
-  // stop the producers (they may be up to two iterations ahead, waiting for a buffer); with two chain CTAs both
-  // stop at the same iteration (identical decisions) and CTA 0 signals
+  // stop the producers (they may be up to two iterations ahead, waiting for a buffer); with several chain CTAs
+  // all stop at the same iteration (identical decisions) and CTA 0 signals
   if (crank == 0 && threadIdx.x < NP)
     st_cluster_release_u32(mapa_u32(smem_u32(stopf), (uint32_t)(threadIdx.x + NCH)), 1u);
   for (int i = threadIdx.x; i < MH; i += kChainThreads)
@@ -555,7 +568,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
   } else {
     // ============================================================================ chain
     if (m == kChainWarps * kChainRowsPerWarp) {
-      if (nch == 2)
+      if (nch == 4)
+        chain_role<true, 4>(p, b, crank, smem, bars, sbuf, c2, st0);
+      else if (nch == 2)
         chain_role<true, 2>(p, b, crank, smem, bars, sbuf, c2, st0);
       else
         chain_role<true, 1>(p, b, crank, smem, bars, sbuf, c2, st0);
@@ -576,13 +591,14 @@ struct ChainCfg {
 size_t chain_smem_chain(int64_t m, int nch) {
   const int64_t mh = m / nch;
   return kChainHeader + (size_t)2 * mh * m * 4 + (size_t)mh * m * 4 + (size_t)kChainWarps * (m + 2) * 8 +
-         (size_t)m * 8 + (size_t)m * 8 + (size_t)mh * 16 + 32 * 8 + (size_t)m * 4 + (nch == 2 ? (size_t)4 * m * 8 : 0);
+         (size_t)m * 8 + (size_t)m * 8 + (size_t)mh * 16 + 32 * 8 + (size_t)m * 4 + (nch > 1 ? (size_t)2 * nch * m * 8 : 0);
 }
 
 bool chain_shape(int64_t n, int64_t m, int ncl, int nch, ChainCfg* c) {
   const int np = ncl - nch;
   if (np < 1 || m < 1) return false;
-  if (nch == 2 && m != kChainWarps * kChainRowsPerWarp) return false;   // two chain CTAs: m == 128 only
+  if (nch > 1 && m != kChainWarps * kChainRowsPerWarp) return false;   // several chain CTAs: m == 128 only
+  if (nch != 1 && nch != 2 && nch != 4) return false;
   const int RB = (int)((m + np - 1) / np);
   if (RB > 2 * kChainWarps) return false;   // two rows per producer warp
   const size_t prod = kChainHeader + (size_t)RB * n * m * 4;
@@ -627,11 +643,15 @@ int chain_active_clusters(const ChainCfg& c) {
 // co-resident vs 15: throughput, C5), else any feasible size. COT_CHAIN_NCL / COT_CHAIN_NCH force.
 bool chain_config(int64_t n, int64_t m, int64_t B, ChainCfg* c) {
   const char* nchv = getenv("COT_CHAIN_NCH");
-  const int nch_forced = nchv ? std::max(1, std::min(2, atoi(nchv))) : 0;
+  const int nch_forced = nchv ? atoi(nchv) : 0;
   if (const char* ev = getenv("COT_CHAIN_NCL")) return chain_shape(n, m, atoi(ev), nch_forced ? nch_forced : 1, c);
   ChainCfg c8;
-  const int nch8 = nch_forced ? nch_forced : (m == kChainWarps * kChainRowsPerWarp ? 2 : 1);
-  const bool h8 = chain_shape(n, m, 8, nch8, &c8) || (nch8 == 2 && !nch_forced && chain_shape(n, m, 8, 1, &c8));
+  bool h8 = false;
+  if (nch_forced)
+    h8 = chain_shape(n, m, 8, nch_forced, &c8);
+  else   // as many chain CTAs as the producers' shared memory allows (4 producers x 32 rows, 6 x 22, 7 x 19)
+    for (int nch : {4, 2, 1})
+      if ((h8 = chain_shape(n, m, 8, nch, &c8))) break;
   if (h8 && B > 0 && B <= chain_active_clusters(c8)) {
     *c = c8;
     return true;

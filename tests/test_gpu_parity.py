@@ -505,10 +505,10 @@ def test_chain_kernel_launch_boundaries_bitwise():
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
-@pytest.mark.parametrize("nch", [1, 2])
+@pytest.mark.parametrize("nch", [1, 2, 4])
 def test_chain_kernel_one_or_two_chain_ctas(nch):
-    """k_batch_chain with one chain CTA per problem and with two (rows split in halves, the column-sum halves
-    swapped through DSMEM every iteration: the default while a batch of m = 128 problems fits one wave of
+    """k_batch_chain with one chain CTA per problem and with two or four (rows split, the parts of the column
+    sums exchanged through DSMEM every iteration: the default while a batch of m = 128 problems fits one wave of
     8-CTA clusters, as C2): the C2 sweep batch against the oracle after 40 iterations, and launch boundaries
     (40 = 13 + 27) bitwise."""
     p = synthetic.c2_sweep()
