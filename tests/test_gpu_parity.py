@@ -506,7 +506,7 @@ def test_chain_kernel_launch_boundaries_bitwise():
 
 
 @pytest.mark.parametrize("nch", [1, 2, 4])
-def test_chain_kernel_one_or_two_chain_ctas(nch):
+def test_chain_kernel_split_chain_ctas(nch):
     """k_batch_chain with one chain CTA per problem and with two or four (rows split, the parts of the column
     sums exchanged through DSMEM every iteration: the default while a batch of m = 128 problems fits one wave of
     8-CTA clusters, as C2): the C2 sweep batch against the oracle after 40 iterations, and launch boundaries
