@@ -617,6 +617,7 @@ int chain_active_clusters(const ChainCfg& c) {
   const int64_t key = (int64_t)c.smem * 32 + c.ncl;
   if (key == key_c) return val_c;
   cudaFuncSetAttribute((void*)k_batch_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  if (c.ncl > 8) cudaFuncSetAttribute((void*)k_batch_chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(c.ncl * 64));
   cfg.blockDim = dim3(kChainThreads);
@@ -645,11 +646,14 @@ bool chain_config(int64_t n, int64_t m, int64_t B, ChainCfg* c) {
   const char* nchv = getenv("COT_CHAIN_NCH");
   const int nch_forced = nchv ? atoi(nchv) : 0;
   if (const char* ev = getenv("COT_CHAIN_NCL")) return chain_shape(n, m, atoi(ev), nch_forced ? nch_forced : 1, c);
+  // one wave of 8-CTA clusters with as many chain CTAs as the producers' shared memory allows (4 producers x 32
+  // rows, 6 x 22, 7 x 19). (16-CTA clusters, 4 chain CTAs + 12 producers, measured slower on C2: 1.79 vs 1.69 us
+  // per iteration, the exchange between the chain CTAs takes longer; COT_CHAIN_NCL=16 still runs them.)
   ChainCfg c8;
   bool h8 = false;
   if (nch_forced)
     h8 = chain_shape(n, m, 8, nch_forced, &c8);
-  else   // as many chain CTAs as the producers' shared memory allows (4 producers x 32 rows, 6 x 22, 7 x 19)
+  else
     for (int nch : {4, 2, 1})
       if ((h8 = chain_shape(n, m, 8, nch, &c8))) break;
   if (h8 && B > 0 && B <= chain_active_clusters(c8)) {
@@ -698,6 +702,8 @@ cudaError_t launch_batch_chain(const IterArgs& a, const Workspace& ws, int iters
   p.diag = getenv("COT_CHAIN_DIAG") ? (atoi(getenv("COT_CHAIN_DIAG")) & 2) : 0;
   cudaError_t e = cudaFuncSetAttribute((void*)k_batch_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)cc.smem);
+  if (e == cudaSuccess && cc.ncl > 8)
+    e = cudaFuncSetAttribute((void*)k_batch_chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.B * cc.ncl));
