@@ -410,8 +410,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
   const int n = p.n, m = p.m, mv = m >> 2;
   // header: [0] [1] chain: s' buffer q full (one arrival -- the chain's own expect_tx of its rows' bytes -- and the
   // producers' st.async transaction bytes per phase); [2] [3] producer: s' buffer q free (one arrival by each chain
-  // CTA per phase); [4] producer: cost rows loaded; [5] [6] chain (nch = 2): the peer's column-sum half of
-  // iteration parity q arrived; stop flag at byte 64
+  // CTA per phase); [4] producer: cost rows loaded; [5] [6] chain (nch > 1): the other chain CTAs' parts of the
+  // column sums of iteration parity q arrived; stop flag at byte 64
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   unsigned* stopf = reinterpret_cast<unsigned*>(smem + 64);
   float* sbuf = reinterpret_cast<float*>(smem + kChainHeader);   // chain: [2][m][m] s'; producer: C rows
@@ -472,8 +472,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_c
       }
     }
     if (nrows > 0) mbar_wait(&bars[4], 0);
-    // destination of each of the warp's rows: the chain CTA holding it (nch = 2: rows [0, m/2) in CTA 0, the rest
-    // in CTA 1), its local row there, that CTA's s' buffers and full barriers
+    // destination of each of the warp's rows: the chain CTA holding it (chain CTA c holds rows [c m/nch,
+    // (c+1) m/nch)), its local row there, that CTA's s' buffers and full barriers
     const int mh = m / nch;
     uint32_t rs_buf[2], rfull[2];
 #pragma unroll
@@ -587,7 +587,7 @@ struct ChainCfg {
   size_t smem;
 };
 
-// chain CTA: s' x 2 and a_ij of its mh rows, warp partials, Fz, beta, row stats, scratch, kz, column-sum halves
+// chain CTA: s' x 2 and a_ij of its mh rows, warp partials, Fz, beta, row stats, scratch, kz, column-sum parts
 size_t chain_smem_chain(int64_t m, int nch) {
   const int64_t mh = m / nch;
   return kChainHeader + (size_t)2 * mh * m * 4 + (size_t)mh * m * 4 + (size_t)kChainWarps * (m + 2) * 8 +
