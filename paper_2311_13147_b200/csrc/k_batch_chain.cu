@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -612,10 +613,16 @@ bool chain_shape(int64_t n, int64_t m, int ncl, int nch, ChainCfg* c) {
 }
 
 int chain_active_clusters(const ChainCfg& c) {
-  static int64_t key_c = -1;
-  static int val_c = 0;
+  // a few shapes per process (the launcher may probe two per call): cached, the occupancy query is not free;
+  // calls on distinct streams may run concurrently (include/cyclicot.h)
+  static std::mutex mu;
+  static int64_t keys[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  static int vals[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  static int next = 0;
   const int64_t key = (int64_t)c.smem * 32 + c.ncl;
-  if (key == key_c) return val_c;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < 8; ++i)
+    if (keys[i] == key) return vals[i];
   cudaFuncSetAttribute((void*)k_batch_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (c.ncl > 8) cudaFuncSetAttribute((void*)k_batch_chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
@@ -634,8 +641,9 @@ int chain_active_clusters(const ChainCfg& c) {
     cudaGetLastError();
     nact = 0;
   }
-  key_c = key;
-  val_c = nact;
+  keys[next] = key;
+  vals[next] = nact;
+  next = (next + 1) & 7;
   return nact;
 }
 

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -803,9 +804,11 @@ static bool shape_config(int k, int64_t n, int64_t m, BatchCfg* out) {
 
 // co-resident clusters of a configuration (cached per shared-memory size)
 static int active_clusters(const BatchCfg& c) {
+  static std::mutex mu;   // calls on distinct streams may run concurrently (include/cyclicot.h)
   static int64_t cached_key = -1;
   static int cached = 0;
   const int64_t key = ((int64_t)c.smem * 64 + c.sh.ncl) * 2 + (c.ws ? 1 : 0);
+  std::lock_guard<std::mutex> lock(mu);
   if (key == cached_key) return cached;
   cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (c.sh.ncl > 8) cudaFuncSetAttribute(c.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
