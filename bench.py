@@ -174,7 +174,7 @@ class Runner:
         # which iteration kernel the library runs: 1 = persistent TMA stream (all iterations in one launch),
         # 2 = cluster-resident (all iterations in one launch, whole problems on chip), 0 = launch pair / iteration
         self.path = int(self.L.cot_iter_path(self.B, 1 if self.pre else self.n, self.m, self.dt, self.flags))
-        self.persistent = self.path in (1, 2, 3)
+        self.persistent = self.path in (1, 2, 3, 4)
         self.launches_per_step = 1 + 1 + (1 if self.persistent else 2 * iters) + 3 + 1 + (1 if self.pre else 0)
         self.bytes_iter = float(p.B) * ((2 if self.pre else p.n + 1) * p.m * p.m) * p.C.itemsize
 
@@ -322,6 +322,7 @@ class ShardedRunner:
         self.nf = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ev = []
         self.persistent = self.fused
+        self.path = (int(self.L.cot_fused_path(p.n, p.m, self.R, world, 0, self.flags)) if self.fused else 0)
         self.launches_per_step = 1 + 1 + (1 if self.fused else 3 * iters) + 3 + 1
         self.bytes_iter = float(p.n + 1) * self.R * p.m * p.C.itemsize
         q = lambda t: t.data_ptr()
@@ -465,19 +466,23 @@ def run_ours(args, rank, world, local_rank):
     achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
     dom_share = it_mean / ms_step
     clocks = clk.summary()
-    cluster = getattr(R, "path", None) in (2, 3)
+    cluster = getattr(R, "path", None) in (2, 3, 4)
     if cluster:   # whole problems on chip: the bound is the SFU (one MUFU.EX2 per Gibbs evaluation), DESIGN.md §6
         ex2_launch = float(B_local_evals(p, iters))
         achieved_sfu = ex2_launch / (per_launch_ms / 1e3)
         mhz = clocks.get("sm_mhz") or 1965.0
         peak_sfu = 148 * 16 * mhz * 1e6
     if mode == "row_sharded":
-        kernel = ("k_iter_tma fused (persistent, all iterations in one launch per rank; column sums exchanged "
+        kernel = (("k_iter_res fused (on-chip resident shard in TMEM + shared memory, all iterations in one launch "
+                   "per rank; integer column sums reduced in-kernel, exchanged through peer-mapped buffers)")
+                  if R.fused and getattr(R, "path", 1) == 4 else
+                  "k_iter_tma fused (persistent, all iterations in one launch per rank; column sums exchanged "
                   "in-kernel through peer-mapped LL lines)" if R.fused else
                   "per iteration: k_iter_tma rows-only + k_colsum + ncclAllReduce + k_zupdate" +
                   (f" [{R.fused_note}]" if R.fused_note else ""))
     else:
         kernel = {1: "k_iter_tma (persistent: all iterations in one launch)",
+                  4: "k_iter_res (persistent, on-chip resident: the cost in TMEM + shared memory, loaded once per launch; every Gibbs term re-evaluated every iteration; integer column sums reduced in-kernel)",
                   2: "k_batch_cluster (one thread-block cluster per problem: 8 CTAs while the batch fits one wave, else 6; all iterations in one launch, on chip)",
                   3: "k_batch_chain (one thread-block cluster per problem, 8 CTAs while the batch fits one wave, else 6: one CTA runs the iteration chain, the others evaluate the n*m^2 Gibbs terms every iteration into its shared memory; all iterations in one launch, on chip)"}.get(
                       getattr(R, "path", 0), "k_rows_ldg + k_cols (one launch pair per iteration)")

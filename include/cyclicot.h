@@ -165,8 +165,16 @@ int cerot_iter(const double* alpha, const double* beta, const void* C, const voi
 /* (k_batch_cluster: fp32, m % 4 == 0, 8 <= m <= 256; whole problem on chip, SFU-bound), 3 = the          */
 /* cluster-resident chain kernel (k_batch_chain: fp32, m % 4 == 0, m <= 128; one CTA per cluster runs the  */
 /* iteration chain, the others stream the Gibbs terms; COT_BATCH_CHAIN=0 in the environment disables it);  */
+/* 4 = the on-chip-resident kernel (k_iter_res: B == 1, fp32, m % 128 == 0, m <= 1024, the n*m^2 costs fit */
+/* in the TMEM + shared memory of one CTA per SM, e.g. C3; SFU-bound; COT_RES=0 in the environment        */
+/* disables it; not with COT_DETERMINISTIC, COT_PRECOMPUTED, COT_FORCE_TMA or COT_FORCE_LDG);              */
 /* -1: bad shape.                                                                                          */
 int cot_iter_path(int64_t B, int64_t n, int64_t m, int dtype, uint32_t flags);
+/* The kernel cerot_iter_fused runs for a rank holding R rows of an nranks-way balanced row partition of a */
+/* fp32 problem: 4 = k_iter_res (the rank's shard fits on chip: the C4 shards of 8-GPU    */
+/* partitions), 1 = k_iter_tma (the streaming persistent kernel); emulated = 1 asks for the one-GPU       */
+/* emulation (cerot_iter_fused_emulated: each virtual rank on 1/nranks of the SMs). -1: bad arguments.     */
+int cot_fused_path(int64_t n, int64_t m, int64_t R, int nranks, int emulated, uint32_t flags);
 /* The two halves of one cerot_iter iteration, for callers that interleave work between them (the
  * row-sharded multi-GPU path reduces the column sums across ranks in between; bench.py times the row
  * pass alone). `parity` (0/1) selects the column-partial buffer; use the iteration index & 1.

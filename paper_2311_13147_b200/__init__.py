@@ -49,6 +49,7 @@ _SIGS = {
     "clot_expand": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp]),
     "cerot_init": (ctypes.c_int, [_vp, _vp, _i64, _i64, _u32, _vp, _vp, _sz, _vp]),
     "cot_iter_path": (ctypes.c_int, [_i64, _i64, _i64, ctypes.c_int, _u32]),
+    "cot_fused_path": (ctypes.c_int, [_i64, _i64, _i64, ctypes.c_int, ctypes.c_int, _u32]),
     "cot_expand_path": (ctypes.c_int, [_i64, _i64, ctypes.c_int]),
     "cot_set_device": (ctypes.c_int, [ctypes.c_int]),
     "cerot_iter": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl, _i64, _u32,

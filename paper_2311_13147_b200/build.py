@@ -7,7 +7,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcyclicot.so")
-SOURCES = ["abi.cu", "k_aggregate.cu", "k_expand.cu", "k_iter.cu", "k_iter_tma.cu", "k_plan.cu", "k_shard.cu", "k_batch_cluster.cu", "k_batch_chain.cu", "k_srot.cu", "k_full.cu", "netsimplex.cpp"]
+SOURCES = ["abi.cu", "k_aggregate.cu", "k_expand.cu", "k_iter.cu", "k_iter_tma.cu", "k_iter_res.cu", "k_plan.cu", "k_shard.cu", "k_batch_cluster.cu", "k_batch_chain.cu", "k_srot.cu", "k_full.cu", "netsimplex.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 OBJDIR = os.path.join(HERE, "build_obj")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

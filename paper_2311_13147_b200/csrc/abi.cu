@@ -72,6 +72,8 @@ size_t carve_workspace(void* base, int64_t B, int64_t n, int64_t m, int64_t R, i
     w.rlines = reinterpret_cast<uint4*>(take((size_t)2 * sm_count * 16));
     w.plines = reinterpret_cast<uint4*>(take((size_t)2 * sm_count * (2 * m) * 16));   // 2 lines / value (deterministic)
     w.lcap = sm_count;
+    w.rcnt = reinterpret_cast<unsigned*>(take(64));
+    w.rsum = reinterpret_cast<unsigned long long*>(take((size_t)3 * m * 8));
     w.ll_base = base ? static_cast<char*>(base) + o0 : nullptr;
     w.ll_bytes = off - o0;
   }
@@ -123,6 +125,9 @@ static NcclApi& nccl() {
   return api;
 }
 
+size_t xchg_res_offset(int64_t m, int nranks) {
+  return kXchgHeader + (size_t)2 * nranks * (2 * m) * sizeof(uint4);   // 2 lines per value in the deterministic mode
+}
 }  // namespace cot
 
 using namespace cot;
@@ -314,7 +319,11 @@ int cerot_iter(const double* alpha, const double* beta, const void* C, const voi
     COT_CHECK_CUDA(launch_batch_cluster(a, ws, (int)iters, s));
     return COT_OK;
   }
-  if (iters > 0 && tma_eligible(a)) {              // large problem: persistent TMA stream (C3, C4)
+  if (iters > 0 && res_eligible(a)) {              // cost fits on chip (C3): TMEM + shared-memory resident
+    COT_CHECK_CUDA(launch_iter_res(a, ws, (int)iters, s));
+    return COT_OK;
+  }
+  if (iters > 0 && tma_eligible(a)) {              // large problem: persistent TMA stream (C4)
     COT_CHECK_CUDA(launch_iter_tma(a, ws, (int)iters, false, 0, s));
     return COT_OK;
   }
@@ -336,8 +345,18 @@ int cot_iter_path(int64_t B, int64_t n, int64_t m, int dtype, uint32_t flags) {
                                nullptr);
   if (batch_chain_eligible(a)) return 3;
   if (batch_cluster_eligible(a)) return 2;
+  if (res_eligible(a)) return 4;
   if (tma_eligible(a)) return 1;
   return 0;
+}
+
+int cot_fused_path(int64_t n, int64_t m, int64_t R, int nranks, int emulated, uint32_t flags) {
+  if (n < 1 || m < 1 || R < 1 || R > m || nranks < 1 || nranks > kMaxRanks) return -1;
+  FusedRank fr{};
+  fr.a = make_args(nullptr, nullptr, nullptr, nullptr, 1, n, m, COT_F32, nullptr, 0.0, 1, flags, nullptr, nullptr, 0,
+                   R);
+  for (int q = 0; q < nranks; ++q) fr.xres[q] = reinterpret_cast<unsigned char*>(1);   // shape query only
+  return res_fused_config(fr, nranks, emulated != 0, nullptr) ? 4 : 1;
 }
 
 int cerot_rows(const double* alpha, const void* C, const void* G, int64_t B, int64_t n, int64_t m, int dtype,
@@ -449,11 +468,13 @@ int cerot_solve(const double* alpha, const double* beta, const void* C, int64_t 
   // in one launch and apply the freeze rule themselves; the generic kernels run as one CUDA graph
   // with a device-side while loop. No host round trip until the report.
   if (max_iter > 0) {
-    if (batch_cluster_eligible(a) || tma_eligible(a)) {
+    if (batch_cluster_eligible(a) || res_eligible(a) || tma_eligible(a)) {
       for (int64_t done = 0; done < max_iter;) {   // int-sized launches (one launch unless max_iter >= 2^31)
         const int chunk = (int)std::min<int64_t>(max_iter - done, 0x7fffffff);
         if (batch_cluster_eligible(a))
           COT_CHECK_CUDA(launch_batch_cluster(a, ws, chunk, s));
+        else if (res_eligible(a))
+          COT_CHECK_CUDA(launch_iter_res(a, ws, chunk, s));
         else
           COT_CHECK_CUDA(launch_iter_tma(a, ws, chunk, false, 0, s));
         done += chunk;
@@ -525,6 +546,8 @@ static int iterate_reduced(const IterArgs& a, const Workspace& ws, void* workspa
     const int64_t chunk = std::min<int64_t>(check_every, max_iter - done);
     if (batch_cluster_eligible(a)) {
       COT_CHECK_CUDA(launch_batch_cluster(a, ws, (int)chunk, s));
+    } else if (res_eligible(a)) {
+      COT_CHECK_CUDA(launch_iter_res(a, ws, (int)chunk, s));
     } else if (tma_eligible(a)) {
       COT_CHECK_CUDA(launch_iter_tma(a, ws, (int)chunk, false, 0, s));
     } else {
@@ -835,7 +858,7 @@ int cerot_iter_sharded(const double* alpha, const double* beta, const void* C_lo
 // ------------------------------------------------------------------------------ fused row sharding
 size_t cot_xchg_bytes(int64_t m, int nranks) {
   if (m < 1 || nranks < 1 || nranks > kMaxRanks) return 0;
-  return kXchgHeader + (size_t)2 * nranks * (2 * m) * sizeof(uint4);   // 2 lines per value in the deterministic mode
+  return cot::xchg_res_offset(m, nranks) + kXchgResHeader + (size_t)3 * m * 8;   // + K-ITER-RES counters and sums
 }
 
 int cot_xchg_alloc(int64_t m, int nranks, void** xbuf, void* ipc_handle) {
@@ -907,6 +930,8 @@ static int fused_rank_args(const double* alpha, const double* beta, const void* 
     fr->xpeer[q] = q < nranks ? reinterpret_cast<uint4*>(static_cast<char*>(xbufs[q]) + kXchgHeader) : nullptr;
   fr->xepoch = static_cast<unsigned long long*>(xbufs[rank]);
   fr->rank = rank;
+  for (int q = 0; q < kMaxRanks; ++q)
+    fr->xres[q] = q < nranks ? static_cast<unsigned char*>(xbufs[q]) + cot::xchg_res_offset(m, nranks) : nullptr;
   return COT_OK;
 }
 
@@ -920,6 +945,10 @@ int cerot_iter_fused(const double* alpha, const double* beta, const void* C_loca
                            w_hat, z_hat, workspace, ws_bytes, nranks, rank, xbufs, &fr);
   if (st) return st;
   if (iters == 0) return COT_OK;
+  if (res_fused_config(fr, nranks, false, nullptr)) {
+    COT_CHECK_CUDA(launch_iter_res_fused(&fr, 1, nranks, false, (int)iters, (cudaStream_t)stream));
+    return COT_OK;
+  }
   COT_CHECK_CUDA(launch_iter_tma_fused(&fr, 1, nranks, false, (int)iters, (cudaStream_t)stream));
   return COT_OK;
 }
@@ -940,6 +969,10 @@ int cerot_iter_fused_emulated(int nranks, const double* alpha, const double* bet
     if (st) return st;
   }
   if (iters == 0) return COT_OK;
+  if (res_fused_config(fr[0], nranks, true, nullptr)) {
+    COT_CHECK_CUDA(launch_iter_res_fused(fr, nranks, nranks, true, (int)iters, (cudaStream_t)stream));
+    return COT_OK;
+  }
   COT_CHECK_CUDA(launch_iter_tma_fused(fr, nranks, nranks, true, (int)iters, (cudaStream_t)stream));
   return COT_OK;
 }

@@ -26,6 +26,9 @@ constexpr double kDetAlphaMax = 128.0;   // 2^7: every fixed-point column partia
 
 constexpr int kMaxRanks = 8;   // fused multi-GPU exchange: ranks of one row partition (one 8-GPU node)
 constexpr size_t kXchgHeader = 256;   // exchange buffer: epoch counter, then the LL lines
+// ... then the region of K-ITER-RES's exchange: [8] arrival counters + epoch (u64), then [3][m] integer sums
+constexpr size_t kXchgResHeader = 64;
+size_t xchg_res_offset(int64_t m, int nranks);
 
 // Rows of each problem are cut into units of `rpu` consecutive rows; units are the work items of the
 // row kernels (K-ITER, K-PLAN) and each unit writes one fp64 column-partial row. `upp` units per
@@ -66,6 +69,10 @@ struct Workspace {
   uint4* rlines;                // [2][lcap]
   uint4* plines;                // [2][lcap][m]
   int lcap;                     // = SM count
+  // K-ITER-RES (k_iter_res.cu): integer column sums [3][m] and arrival counters [8] + reduction epoch (u64);
+  // inside the LL region, so cerot_init zeroes them too
+  unsigned long long* rsum;
+  unsigned* rcnt;
 };
 // Lays the workspace out from `base` (may be NULL to only size it). Returns the byte count. R = rows held
 // per problem (m unless row-sharded).
@@ -132,7 +139,20 @@ struct FusedRank {
   uint4* xpeer[kMaxRanks];             // every rank's line array, as addressed by this rank
   unsigned long long* xepoch;          // this rank's epoch counter
   int rank;
+  unsigned char* xres[kMaxRanks];      // every rank's K-ITER-RES exchange region, as addressed by this rank
 };
+// K-ITER-RES (k_iter_res.cu): the iteration of a problem or row shard whose cost fits on chip (TMEM + shared
+// memory of one CTA per SM): C3 and the C4 shards of 4- and 8-GPU partitions.
+struct ResCfg {
+  int h, W, ncl, MR, nq_max, tq, nsq;
+  size_t smem;
+};
+bool res_config(int64_t n, int64_t m, int64_t R, int64_t Rlo, int sms, int nranks_emulated, ResCfg* out);
+bool res_eligible(const IterArgs& a, int sms = 0);
+cudaError_t launch_iter_res(const IterArgs& a, const Workspace& ws, int iters, cudaStream_t s);
+bool res_fused_config(const FusedRank& r, int nranks, bool emulate, ResCfg* c);
+cudaError_t launch_iter_res_fused(const FusedRank* r, int nv, int nranks, bool emulate, int iters, cudaStream_t s);
+int res_path_h(int64_t n, int64_t m, int64_t R);
 int fused_column_slices(int64_t m, int nranks, int sms);
 cudaError_t launch_iter_tma_fused(const FusedRank* r, int nv, int nranks, bool emulate, int iters, cudaStream_t s);
 // Plan pass over the held rows: T blocks (optional) + unit partials in the workspace (no finalisation).

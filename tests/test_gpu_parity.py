@@ -190,9 +190,14 @@ def test_c2_500_iterations(eps_factor, path):
     _compare(p, rep[0], T, w, z)
 
 
-def test_c3_image_500_iterations():
-    """C3 (configs[2]): 64x64 rotation-symmetric histograms (stand-in for Table 2's NYU images), eps = 1e-2."""
+@pytest.mark.parametrize("kernel", ["res", "tma"])
+def test_c3_image_500_iterations(kernel, monkeypatch):
+    """C3 (configs[2]): 64x64 rotation-symmetric histograms (stand-in for Table 2's NYU images), eps = 1e-2; on the
+    on-chip-resident kernel (k_iter_res, the default) and the streaming persistent kernel (COT_RES=0)."""
+    if kernel == "tma":
+        monkeypatch.setenv("COT_RES", "0")
     p = synthetic.c3_image(pair=0)
+    assert cot.lib().cot_iter_path(1, p.n, p.m, 0, 0) == (4 if kernel == "res" else 1)
     w, z, _, _ = oracle.cyclic_sinkhorn(p.alpha, p.beta, p.C, float(p.eps[0]), 500, form="kernel")
     _, T, rep, _, _ = _gpu_run(p, 500)
     _compare(p, rep[0], T, w, z)
@@ -531,13 +536,18 @@ def test_chain_kernel_split_chain_ctas(nch):
         _compare(q, rep[b], T[b], w, z)
 
 
-@pytest.mark.parametrize("maker,path", [(lambda: synthetic.c1_tiny(), 0), (lambda: synthetic.c3_image(pair=1), 1),
-                                        (lambda: synthetic.c2_ring(eps_factor=1e-1), 3)],
-                         ids=["C1_ldg_graph_loop", "C3_tma_one_launch", "C2_chain_one_launch"])
-def test_solve_to_tolerance_on_device(maker, path):
+@pytest.mark.parametrize("maker,path,env", [(lambda: synthetic.c1_tiny(), 0, None),
+                                            (lambda: synthetic.c3_image(pair=1), 4, None),
+                                            (lambda: synthetic.c3_image(pair=1), 1, "0"),
+                                            (lambda: synthetic.c2_ring(eps_factor=1e-1), 3, None)],
+                         ids=["C1_ldg_graph_loop", "C3_res_one_launch", "C3_tma_one_launch", "C2_chain_one_launch"])
+def test_solve_to_tolerance_on_device(maker, path, env, monkeypatch):
     """cerot_solve: "until convergence" on the device -- one persistent launch, or (fp64 / generic path) one
     CUDA graph with a device-side while loop -- stops at the oracle's stopping iteration with the freeze rule
-    checked every check_every iterations, and the report matches the oracle there."""
+    checked every check_every iterations, and the report matches the oracle there. C3 on the on-chip-resident
+    kernel (default) and on the streaming persistent kernel (COT_RES=0)."""
+    if env is not None:
+        monkeypatch.setenv("COT_RES", env)
     p = maker()
     tol = p.tol if p.tol > 0 else 1e-7
     ce = 1 if path == 0 else 5
