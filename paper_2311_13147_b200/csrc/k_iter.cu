@@ -316,6 +316,12 @@ __global__ void __launch_bounds__(256) k_init(const double* __restrict__ alpha, 
 // ------------------------------------------------------------------------------------ launchers
 cudaError_t launch_init(const double* alpha, const double* beta, int64_t B, int64_t m, uint32_t flags, double* z_hat,
                         const Workspace& ws, cudaStream_t s) {
+  // the persistent kernels' device-wide state (LL lines, K-ITER-RES sums and counters) starts from zero on every
+  // (re)initialisation of the workspace
+  if (ws.ll_base) {
+    const cudaError_t e = cudaMemsetAsync(ws.ll_base, 0, ws.ll_bytes, s);
+    if (e != cudaSuccess) return e;
+  }
   k_init<<<(unsigned)B, 256, 0, s>>>(alpha, beta, m, flags, z_hat, ws.state, ws.counters, ws.grid_bar);
   return cudaGetLastError();
 }

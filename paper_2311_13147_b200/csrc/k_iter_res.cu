@@ -162,24 +162,26 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// Column sums: value in the low 56 bits (fixed point), contribution count in the top byte.
-constexpr unsigned long long kCntOne = 1ull << 56;
-constexpr unsigned long long kValMask = kCntOne - 1ull;
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-// poll one column sum until its count is `want`; false after the timeout
-__device__ __forceinline__ bool poll_sum(const unsigned long long* p, unsigned want, unsigned long long& v) {
-  v = ld_acquire_sys(p);
-  if ((unsigned)(v >> 56) == want) return true;
+// spin until the cumulative counter reaches `want` (wrap-safe); false after the timeout
+__device__ __forceinline__ bool wait_count(const unsigned* c, unsigned want) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+  if ((int)(v - want) >= 0) return true;
   const unsigned long long t0 = res_timer();
   while (true) {
-    v = ld_acquire_sys(p);
-    if ((unsigned)(v >> 56) == want) return true;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    if ((int)(v - want) >= 0) return true;
     if (res_timer() - t0 > kResTimeoutNs) return false;
   }
+}
+// Exchange sums (multi-GPU level): value in the low 56 bits, contribution count in the top byte.
+constexpr unsigned long long kCntOne = 1ull << 56;
+constexpr unsigned long long kValMask = kCntOne - 1ull;
+// the exchange sums are self-validating (count byte): a relaxed load of this GPU's own memory is enough
+__device__ __forceinline__ unsigned long long ld_poll(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 // the thread's columns j = et + k * kResET < W (k < 4), polled together until every count is `want`
 __device__ __forceinline__ bool poll_sums4(const unsigned long long* base, int et, int W, unsigned want,
@@ -192,7 +194,7 @@ __device__ __forceinline__ bool poll_sums4(const unsigned long long* base, int e
   while (true) {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (todo & (1u << k)) v[k] = ld_acquire_sys(base + et + k * kResET);
+      if (todo & (1u << k)) v[k] = ld_poll(base + et + k * kResET);
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       if ((todo & (1u << k)) && (unsigned)(v[k] >> 56) == want) todo &= ~(1u << k);
@@ -251,7 +253,7 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
   double* red = reinterpret_cast<double*>(smem + L.red);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* sfull = bars;        // [2] k-sums of an iteration written (one arrival per k-sum warp)
-  uint64_t* sempty = bars + 2;   // [2] the epilogue has finished with a buffer
+  uint64_t* sgo = bars + 2;      // the epilogue has issued an iteration's reduction: the next k-sums may start
   uint64_t* rbar = bars + 4;     // row-piece sums of the cluster arrived (h arrivals per iteration)
   unsigned* ctl = reinterpret_cast<unsigned*>(smem + L.ctl);
 
@@ -260,8 +262,7 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
   if (threadIdx.x == 0) {
     mbar_init(&sfull[0], kResNK);
     mbar_init(&sfull[1], kResNK);
-    mbar_init(&sempty[0], 1);
-    mbar_init(&sempty[1], 1);
+    mbar_init(sgo, 1);
     mbar_init(rbar, 1);
     for (int k = 0; k < 16; ++k) ctl[k] = 0;
     fence_mbar_init();
@@ -318,8 +319,9 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
     for (int t = 0; active0 && t < p.iters; ++t) {
       const int buf = t & 1;
       const long long tk0 = p.trace ? clock64() : 0;
-      if (t >= 2) {   // the epilogue released this buffer (iteration t - 2); a halted epilogue never will
-        const uint32_t par = (uint32_t)((t - 2) >> 1) & 1u;
+      if (t >= 1) {   // iteration t - 1 is being reduced (its s' buffer, and t - 2's, are free); a halted epilogue
+                      // never signals
+        const uint32_t par = (uint32_t)(t - 1) & 1u;
         bool halt = false;
         while (true) {
           uint32_t ok;
@@ -327,7 +329,7 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
               "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
               "selp.u32 %0, 1, 0, p;\n\t}"
               : "=r"(ok)
-              : "r"(smem_u32(&sempty[buf])), "r"(par)
+              : "r"(smem_u32(sgo)), "r"(par)
               : "memory");
           if (ok) break;
           if (*(volatile unsigned*)&ctl[RCTL_HALT]) {
@@ -451,7 +453,7 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
     ebar();
     asum = ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
     int ea;
-    frexp(asum, &ea);   // sum alpha <= 2^ea: every column sum (<= sum alpha) stays below 2^53 < 2^56
+    frexp(asum, &ea);   // sum alpha <= 2^ea: every column sum (<= sum alpha) stays below 2^53 < 2^56 (count byte)
     const int S = 53 - ea;
     const double scale = ldexp(1.0, S), iscale = ldexp(1.0, -S);
     ebar();
@@ -589,50 +591,64 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
           P3 = fma(f, ldexp_pos(s4.w, k4.w - a4.w - kM) * fb.y, P3);
         }
         ulonglong2* cb2 = reinterpret_cast<ulonglong2*>(colbuf + 4 * cq);
-        cb2[0] = make_ulonglong2(kCntOne | (P0 > 0.0 ? __double2ull_rz(P0 * scale) : 0ull),
-                                 kCntOne | (P1 > 0.0 ? __double2ull_rz(P1 * scale) : 0ull));
-        cb2[1] = make_ulonglong2(kCntOne | (P2 > 0.0 ? __double2ull_rz(P2 * scale) : 0ull),
-                                 kCntOne | (P3 > 0.0 ? __double2ull_rz(P3 * scale) : 0ull));
+        cb2[0] = make_ulonglong2(P0 > 0.0 ? __double2ull_rz(P0 * scale) : 0ull, P1 > 0.0 ? __double2ull_rz(P1 * scale) : 0ull);
+        cb2[1] = make_ulonglong2(P2 > 0.0 ? __double2ull_rz(P2 * scale) : 0ull, P3 > 0.0 ? __double2ull_rz(P3 * scale) : 0ull);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the partials are visible to the bulk copy
       ebar();
       mark(3);
-      // ---- device-wide step: ONE bulk reduction (TMA, cp.reduce.async.bulk .add.u64) of the W partials into the
-      // iteration's column sums. Every partial carries 1 in its top byte (kCntOne), so each 64-bit column sum
-      // counts its own contributions: a column is complete when its count is the group's CTA count -- no
-      // arrival counter, no fence or completion wait between the reduction and the readers' polls.
-      if (et == 0) {
-        mbar_arrive(&sempty[buf]);   // the k-sum warps may overwrite this buffer (iteration t + 2)
-        // the zeroing stores of the previous iteration (other threads, ordered by the barrier) precede this
-        // reduction for every CTA that observes it (they reuse that slot two iterations later)
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(dst),
-                     "r"(smem_u32(colbuf)), "r"((unsigned)(W * 8))
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // colbuf may be rewritten
+      // ---- device-wide step: the W partials are added into the iteration's column sums with coalesced 64-bit
+      // integer reductions (red.global.add.u64: exact, so the order in which CTAs arrive does not matter); one
+      // thread then releases the CTA's arrival on the group's cumulative counter and waits for the group's
+      // ncl arrivals [multi-GPU: each CTA pushes its 1/ncl slice of the group's rank-local sums to every rank and
+      // the ranks' pushes are counted the same way].
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = et + k * kResET;
+        if (j < W) red_add_gpu(dst + j, colbuf[j]);
       }
+      ebar();
+      if (et == 0) {
+        mbar_arrive(sgo);   // the k-sum warps compute the next iteration's s' while this one is reduced
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.lcnt + q) : "memory");
+        if (!wait_count(p.lcnt + q, (unsigned)p.ncl * (unsigned)(T + 1ull))) ctl[RCTL_TIMEOUT] = 1u;
+      }
+      ebar();
       mark(4);
-      const unsigned long long* src = fused ? xown + (size_t)sX * m : lsum + (size_t)sT * m;
-      const unsigned want_l = (unsigned)p.ncl, want_x = (unsigned)nr;
-      if (fused) {   // push this CTA's slice of the group's rank-local sums to every rank (count 1 per rank)
-        if (js0 + et < js1) asm volatile("fence.acq_rel.sys;" ::: "memory");   // this thread's zeroing, before its pushes
-        for (int jj = js0 + et; jj < js1 && !timeout; jj += kResET) {
+      // [multi-GPU] push this CTA's 1/ncl slice of the group's rank-local sums into every rank's exchange sums
+      // with system-scope reductions; each pushed value carries 1 in its top byte, so a rank's exchange sum of a
+      // column is complete when its count is nranks: no counter, no fence between the pushes and the readers
+      if (fused) {
+        // this thread's zeroing of its slice (previous iteration) precedes its pushes for every observer
+        if (js0 + et < js1) {
+          if (nr > 1) asm volatile("fence.acq_rel.sys;" ::: "memory");
+          else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        for (int jj = js0 + et; jj < js1; jj += kResET) {
           const int j = col0 + jj;
-          unsigned long long v = 0;
-          timeout |= !poll_sum(lsum + (size_t)sT * m + j, want_l, v);
+          unsigned long long v;
+          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(lsum + (size_t)sT * m + j) : "memory");
           v = (v & kValMask) | kCntOne;
-          for (int r = 0; r < nr; ++r) red_add_sys(p.xsum[r] + (size_t)sX * m + j, v);
+          for (int r = 0; r < nr; ++r) {   // the own rank's copy at GPU scope, the peers' at system scope
+            if (r == p.rank) red_add_gpu(p.xsum[r] + (size_t)sX * m + j, v);
+            else red_add_sys(p.xsum[r] + (size_t)sX * m + j, v);
+          }
         }
       }
+      timeout = ctl[RCTL_TIMEOUT] != 0u;
+      const unsigned long long* src = fused ? xown + (size_t)sX * m : lsum + (size_t)sT * m;
       // ---- q-update of the own columns: z_j += log beta_j - log c_j (every CTA of the group, same bits)
       // in split form, multiplicatively: 2^{kz_j} Fz_j <- 2^{kz_j} Fz_j beta_j / c_j, renormalised by exponent bits
       // (no log / exp per column); the thread's <= 4 columns are polled together until complete
-      {
+      if (!timeout) {
         unsigned long long v[4];
-        const unsigned want = fused ? want_x : want_l;
-        timeout |= !poll_sums4(src + col0, et, W, want, v);
+        if (fused) {
+          timeout |= !poll_sums4(src + col0, et, W, (unsigned)nr, v);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (et + k * kResET < W) v[k] = ld_relaxed_sys(src + col0 + et + k * kResET);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int j = et + k * kResET;
@@ -657,16 +673,27 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
       // ---- monitor n sum_j |c_j - beta_j| from all m sums, fixed order: same value everywhere
       const bool need = (p.tol > 0.0 && st.iters % p.check_every == 0) || t == p.iters - 1;
       if (need && !timeout) {
+        if (et == 0 && !fused)   // every column group's sums of this iteration are complete
+          for (int g = 0; g < h; ++g)
+            if (!wait_count(p.lcnt + g, (unsigned)p.ncl * (unsigned)(T + 1ull))) ctl[RCTL_TIMEOUT] = 1u;
+        ebar();
         double dev = 0.0;
         {
           unsigned long long v[4];
-          timeout |= !poll_sums4(src, et, m, fused ? want_x : want_l, v);
+          if (fused) {
+            timeout |= !poll_sums4(src, et, m, (unsigned)nr, v);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (et + k * kResET < m) v[k] = ld_relaxed_sys(src + et + k * kResET);
+          }
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            if (et + k * kResET < m) dev += fabs((double)(v[k] & kValMask) * iscale - p.beta[et + k * kResET]);
+            if (et + k * kResET < m && !timeout) dev += fabs((double)(v[k] & kValMask) * iscale - p.beta[et + k * kResET]);
         }
         dev = warp_sum(dev);
         if (lane == 0) red[8 + ew] = dev;
+        if (ctl[RCTL_TIMEOUT]) timeout = true;
         timeout = bar_or(timeout);
         st.residual = (((red[8] + red[9]) + (red[10] + red[11])) + ((red[12] + red[13]) + (red[14] + red[15]))) * (double)n;
         if (p.tol > 0.0 && st.iters % p.check_every == 0 && st.residual <= p.tol) {
@@ -682,7 +709,6 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
     if (p.trace && et == 0)
       for (int k = 0; k < 7; ++k) p.trace[(size_t)blockIdx.x * 16 + 2 + k] = tr[k];
     if (halted && et == 0) *(volatile unsigned*)&ctl[RCTL_HALT] = 1u;
-    if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // the last reduction has landed
     ebar();
     // ---- outputs: z of the own columns (cluster 0's CTAs), w_hat of the own rows (piece 0's CTAs), state
     if (active0 && done > 0) {

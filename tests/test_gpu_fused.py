@@ -71,12 +71,17 @@ def _check_against_oracle(p, shards, iters):
         assert it == iters
 
 
+@pytest.mark.parametrize("kernel", ["res", "tma"])
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
 @pytest.mark.parametrize("maker", [lambda: synthetic.c2_ring(eps_factor=1e-2),
                                    lambda: synthetic.c4_large(m=512, n=16),
                                    lambda: synthetic.c3_image()],
                          ids=["C2", "C4_m512_n16", "C3"])
-def test_emulated_fused_matches_oracle(world, maker):
+def test_emulated_fused_matches_oracle(world, maker, kernel, monkeypatch):
+    """Both per-rank kernels of the fused path: the on-chip-resident one (k_iter_res, where the shard fits) and the
+    streaming one (k_iter_tma, COT_RES=0)."""
+    if kernel == "tma":
+        monkeypatch.setenv("COT_RES", "0")
     p = maker()
     iters = 30
     shards = _shards(p, world)

@@ -195,6 +195,20 @@ def run_srot(A):
     return [w, z, T]
 
 
+def _env(kv, fn):
+    import os
+    old = {k: os.environ.get(k) for k in kv}
+    os.environ.update(kv)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
 CASES = {
     "aggregate_f32": lambda A: run_aggregate(A, synthetic.c2_ring().C),
     "aggregate_f64": lambda A: run_aggregate(A, synthetic.c1_tiny().C),
@@ -209,12 +223,18 @@ CASES = {
                                                                           eps=0.05, B=2), 5),
     "tma_forced_small": lambda A: run_cerot(A, synthetic.random_cyclic(seed=5, n=9, m=256, dtype=np.float32,
                                                                        eps=0.05), 5, flags=cot.COT_FORCE_TMA),
-    "tma_c3": lambda A: run_cerot(A, synthetic.c3_image(), 4),
+    "res_c3": lambda A: run_cerot(A, synthetic.c3_image(), 4),
+    "res_h2_ragged": lambda A: _env({"COT_RES_H": "2"}, lambda: run_cerot(A, synthetic.c4_large(m=768, n=8), 4)),
+    "res_h4": lambda A: _env({"COT_RES_H": "4"}, lambda: run_cerot(A, synthetic.c4_large(m=512, n=12), 4)),
+    "res_smem_only": lambda A: run_cerot(A, synthetic.random_cyclic(seed=9, n=6, m=256, dtype=np.float32,
+                                                                    eps=0.05), 5),
+    "tma_c3": lambda A: run_cerot(A, synthetic.c3_image(), 4, flags=cot.COT_FORCE_TMA),
     "tma_deterministic": lambda A: run_cerot(A, synthetic.c4_large(m=256, n=8), 4, flags=cot.COT_DETERMINISTIC),
     "ldg_fp64": lambda A: run_cerot(A, synthetic.c1_tiny(), 6),
     "ldg_forced_f32": lambda A: run_cerot(A, synthetic.c2_ring(), 4, flags=cot.COT_FORCE_LDG),
     "precomputed": lambda A: run_cerot(A, synthetic.c2_ring(), 4, pre=True),
     "fused_emulated_2": lambda A: run_fused(A, 2),
+    "fused_emulated_2_tma": lambda A: _env({"COT_RES": "0"}, lambda: run_fused(A, 2)),
     "two_stage": run_two_stage,
     "srot": run_srot,
 }
