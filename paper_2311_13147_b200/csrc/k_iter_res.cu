@@ -66,6 +66,7 @@ struct ResParams {
   int h, W, ncl;         // pieces per row (= cluster size), piece width, clusters of this rank
   int MR, nq_max;        // max rows per cluster, max quads per CTA
   int tq, nsq;           // quads per k-sum thread held in TMEM, shared-memory quad slots
+  int throttle;          // k-sums of iteration t start while t - 1 is reduced (else as soon as a buffer is free)
   int iters;
   double tol;
   long long check_every;
@@ -254,6 +255,7 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* sfull = bars;        // [2] k-sums of an iteration written (one arrival per k-sum warp)
   uint64_t* sgo = bars + 2;      // the epilogue has issued an iteration's reduction: the next k-sums may start
+  uint64_t* sempty = bars + 5;   // [2] the epilogue has finished with an s' buffer
   uint64_t* rbar = bars + 4;     // row-piece sums of the cluster arrived (h arrivals per iteration)
   unsigned* ctl = reinterpret_cast<unsigned*>(smem + L.ctl);
 
@@ -263,6 +265,8 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
     mbar_init(&sfull[0], kResNK);
     mbar_init(&sfull[1], kResNK);
     mbar_init(sgo, 1);
+    mbar_init(&sempty[0], 1);
+    mbar_init(&sempty[1], 1);
     mbar_init(rbar, 1);
     for (int k = 0; k < 16; ++k) ctl[k] = 0;
     fence_mbar_init();
@@ -275,7 +279,7 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
                        __float2int_rn(g4.w * c2));
   }
   // shared-memory quads: [k][nsq] float4, quad Q = 256 tq + sq
-  const int nsq_used = max(0, nq - kResKT * p.tq);
+  const int nsq_used = min(p.nsq, max(0, nq - kResKT * p.tq));   // the rest (if any) is streamed from L2
   for (int idx = threadIdx.x; idx < nsq_used * n; idx += kResThreads) {
     const int k = idx / nsq_used, sq = idx - k * nsq_used;
     const int Q = kResKT * p.tq + sq, lr = Q / W4, cq = Q - lr * W4;
@@ -319,9 +323,12 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
     for (int t = 0; active0 && t < p.iters; ++t) {
       const int buf = t & 1;
       const long long tk0 = p.trace ? clock64() : 0;
-      if (t >= 1) {   // iteration t - 1 is being reduced (its s' buffer, and t - 2's, are free); a halted epilogue
-                      // never signals
-        const uint32_t par = (uint32_t)(t - 1) & 1u;
+      // throttled (k-sums shorter than the device-wide step): start once iteration t - 1 is being reduced, so the
+      // k-sums fill that wait instead of competing with the epilogue's passes; otherwise as soon as the buffer of
+      // iteration t - 2 is free. A halted epilogue never signals.
+      if (p.throttle ? t >= 1 : t >= 2) {
+        const uint32_t par = p.throttle ? (uint32_t)(t - 1) & 1u : (uint32_t)((t - 2) >> 1) & 1u;
+        uint64_t* wb = p.throttle ? sgo : &sempty[buf];
         bool halt = false;
         while (true) {
           uint32_t ok;
@@ -329,7 +336,7 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
               "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
               "selp.u32 %0, 1, 0, p;\n\t}"
               : "=r"(ok)
-              : "r"(smem_u32(sgo)), "r"(par)
+              : "r"(smem_u32(wb)), "r"(par)
               : "memory");
           if (ok) break;
           if (*(volatile unsigned*)&ctl[RCTL_HALT]) {
@@ -386,9 +393,40 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
         }
         out[Q] = make_float4(s0, s1, s2, s3);
       }
+      // quads beyond the on-chip capacity (streamed from L2 every iteration, a shard that does not quite fit:
+      // the 4-GPU C4 shard): eight k-rows per step, the next eight loaded while these are summed
+      for (int Q = kt + kResKT * p.tq; Q < nq; Q += kResKT) {
+        if (Q - kResKT * p.tq < p.nsq) continue;
+        const int lr = Q / W4, cq = Q - lr * W4;
+        const float4* src = reinterpret_cast<const float4*>(p.C + ((size_t)lr0 + lr) * m + col0) + cq;
+        const size_t ks = (size_t)p.R * (m / 4);
+        const int4 a4 = ash[Q];
+        const float g0 = (float)a4.x, g1 = (float)a4.y, g2 = (float)a4.z, g3 = (float)a4.w;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        float4 A[8], Bn[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) A[kk] = kk < n ? __ldcg(src + kk * ks) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k0 = 0; k0 < n; k0 += 8) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            Bn[kk] = k0 + 8 + kk < n ? __ldcg(src + (size_t)(k0 + 8 + kk) * ks) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            if (k0 + kk < n) {
+              s0 += ex2(fmaf(-A[kk].x, c2, g0));
+              s1 += ex2(fmaf(-A[kk].y, c2, g1));
+              s2 += ex2(fmaf(-A[kk].z, c2, g2));
+              s3 += ex2(fmaf(-A[kk].w, c2, g3));
+            }
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) A[kk] = Bn[kk];
+        }
+        out[Q] = make_float4(s0, s1, s2, s3);
+      }
       // shared-memory quads: four k-rows per step, loads first
       for (int Q = kt + kResKT * nt; Q < nq; Q += kResKT) {
         const int sq = Q - kResKT * p.tq;
+        if (sq >= p.nsq) break;   // streamed (above)
         const int4 a4 = ash[Q];
         const float g0 = (float)a4.x, g1 = (float)a4.y, g2 = (float)a4.z, g3 = (float)a4.w;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
@@ -532,44 +570,48 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
       }
       ebar();
       mark(1);
-      for (int lr = et; lr < nrows; lr += kResET) {
-        const double2* ch = chunk + lr * cpp;
-        int mx = INT_MIN;
-        for (int k = 0; k < cpp; ++k) mx = max(mx, (int)ch[k].y);
-        double r = 0.0;
-        for (int k = 0; k < cpp; ++k) r += ch[k].x * pow2i((int)ch[k].y - mx);
+      // piece combine, one warp per row (rows ew, ew + 8, ...): lane k < cpp holds the warp partial k; exact
+      // power-of-two rescaling to the piece maximum (REDUX), then a fixed shuffle tree over lanes 0..7
+      for (int lr = ew; lr < nrows; lr += kResNE) {
+        const double2 c = lane < cpp ? chunk[lr * cpp + lane] : make_double2(0.0, 0.0);
+        const int mx = __reduce_max_sync(0xffffffffu, lane < cpp ? (int)c.y : INT_MIN);
+        double r = lane < cpp ? c.x * pow2i((int)c.y - mx) : 0.0;
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
         if (h == 1) {
-          rowk[buf * MR + lr] = mx;
-          rowr[buf * MR + lr] = r;
-        } else {
-          // (sum, shift) into every cluster CTA's slot [buf][lr][q] with st.async: the bytes complete the
-          // transaction count of the receiver's barrier (no fence, no remote arrival)
-          const unsigned la = smem_u32(&rx[((size_t)buf * MR + lr) * h + q]);
-          const unsigned lb = smem_u32(rbar);
-          for (int pr = 0; pr < h; ++pr) {
-            const unsigned ra = cluster_map(la, (unsigned)pr), rb = cluster_map(lb, (unsigned)pr);
-            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra),
-                         "l"((unsigned long long)__double_as_longlong(r)), "r"(rb)
-                         : "memory");
-            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra + 8u),
-                         "l"((unsigned long long)__double_as_longlong((double)mx)), "r"(rb)
-                         : "memory");
+          if (lane == 0) {
+            rowk[buf * MR + lr] = mx;
+            rowr[buf * MR + lr] = r;
+            rowf[buf * MR + lr] = alph[lr] * rcp_nomufu(r);
           }
+        } else if (lane < h) {
+          // (sum, shift) into cluster CTA `lane`'s slot [buf][lr][q] with st.async: the bytes complete the
+          // transaction count of the receiver's barrier (no fence, no remote arrival)
+          const unsigned ra = cluster_map(smem_u32(&rx[((size_t)buf * MR + lr) * h + q]), (unsigned)lane);
+          const unsigned rb = cluster_map(smem_u32(rbar), (unsigned)lane);
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra),
+                       "l"((unsigned long long)__double_as_longlong(r)), "r"(rb)
+                       : "memory");
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra + 8u),
+                       "l"((unsigned long long)__double_as_longlong((double)mx)), "r"(rb)
+                       : "memory");
         }
       }
       if (h > 1) {
         mbar_wait(rbar, (uint32_t)t & 1u);
-        for (int lr = et; lr < nrows; lr += kResET) {   // every CTA of the cluster combines the pieces in the same order
-          const double2* rv = rx + ((size_t)buf * MR + lr) * h;
-          int mx = INT_MIN;
-          for (int pr = 0; pr < h; ++pr) mx = max(mx, (int)rv[pr].y);
-          double r = 0.0;
-          for (int pr = 0; pr < h; ++pr) r += rv[pr].x * pow2i((int)rv[pr].y - mx);
-          rowk[buf * MR + lr] = mx;
-          rowr[buf * MR + lr] = r;
+        for (int lr = ew; lr < nrows; lr += kResNE) {   // every CTA of the cluster combines the pieces in the same order
+          const double2 c = lane < h ? rx[((size_t)buf * MR + lr) * h + lane] : make_double2(0.0, 0.0);
+          const int mx = __reduce_max_sync(0xffffffffu, lane < h ? (int)c.y : INT_MIN);
+          double r = lane < h ? c.x * pow2i((int)c.y - mx) : 0.0;
+#pragma unroll
+          for (int o = 2; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+          if (lane == 0) {
+            rowk[buf * MR + lr] = mx;
+            rowr[buf * MR + lr] = r;
+            rowf[buf * MR + lr] = alph[lr] * rcp_nomufu(r);
+          }
         }
       }
-      for (int lr = et; lr < nrows; lr += kResET) rowf[buf * MR + lr] = alph[lr] * rcp_nomufu(rowr[buf * MR + lr]);
       ebar();
       mark(2);
       // ---- column pass: P_j = sum_i (alpha_i / r_i) t_ij over the CTA's rows, fixed point, one reduction each
@@ -609,6 +651,7 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
       ebar();
       if (et == 0) {
         mbar_arrive(sgo);   // the k-sum warps compute the next iteration's s' while this one is reduced
+        mbar_arrive(&sempty[buf]);
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.lcnt + q) : "memory");
         if (!wait_count(p.lcnt + q, (unsigned)p.ncl * (unsigned)(T + 1ull))) ctl[RCTL_TIMEOUT] = 1u;
@@ -798,12 +841,29 @@ bool res_config(int64_t n, int64_t m, int64_t R, int64_t Rlo, int sms, int nrank
     const int MR = (MR0 + 1) & ~1;
     const int nq_max = MR0 * (W / 4);
     const int tq = (n % 4 == 0 && n <= 64) ? (int)(64 / n) : 0;   // 256 TMEM words per thread / 4n
-    const int nsq = std::max(0, nq_max - kResKT * tq);
+    int nsq = std::max(0, nq_max - kResKT * tq);
+    // shared memory left for quads; what does not fit is streamed from L2 every iteration -- allowed for up to a
+    // quarter of the quads of a shard that stays L2-resident (the 4-GPU C4 shard: 512 quads, 66 streamed)
+    const size_t fixed = res_layout((int)n, 0, nq_max, W, MR, h).total;
+    const int cap = fixed >= (size_t)kResMaxSmem ? 0 : (int)(((size_t)kResMaxSmem - fixed) / ((size_t)16 * n));
+    int nstream = 0;
+    if (nsq > cap) {
+      nstream = nsq - cap;
+      nsq = cap;
+    }
+    const bool stream_ok = nstream == 0 || (nstream * 4 <= nq_max && (double)n * R * m * 4.0 <= 96e6 &&
+                                            !(getenv("COT_RES_STREAM") && atoi(getenv("COT_RES_STREAM")) == 0));
     const ResLayout L = res_layout((int)n, nsq, nq_max, W, MR, h);
-    if (L.total > (size_t)kResMaxSmem) continue;
+    if (getenv("COT_RES_DEBUG"))
+      fprintf(stderr, "[res_config] n=%lld m=%lld R=%lld h=%d ncl=%d (active clusters %d) MR=%d quads=%d tq=%d nsq=%d "
+              "streamed=%d smem=%zu%s\n",
+              (long long)n, (long long)m, (long long)R, h, ncl, h > 1 ? max_active_clusters(h) : sms, MR0, nq_max, tq,
+              nsq, nstream, L.total, (L.total > (size_t)kResMaxSmem || !stream_ok) ? " (does not fit)" : "");
+    if (L.total > (size_t)kResMaxSmem || !stream_ok) continue;
     ResCfg c{h, W, ncl, MR, nq_max, tq, nsq, L.total};
-    // fewest quads per CTA (the k-sum bound); ties: the smaller cluster
-    if (!found || c.nq_max < best.nq_max) {
+    // fewest quads per CTA (the k-sum bound, a streamed quad counting double); ties: the smaller cluster
+    const int cost = nq_max + nstream, best_cost = best.nq_max + std::max(0, best.nq_max - kResKT * best.tq - best.nsq);
+    if (!found || cost < best_cost) {
       best = c;
       found = true;
     }
@@ -841,6 +901,9 @@ static void res_fill(const IterArgs& a, const Workspace& ws, const ResCfg& c, in
   p->nq_max = c.nq_max;
   p->tq = c.tq;
   p->nsq = c.nsq;
+  // throttle when the CTA's k-sums (one MUFU.EX2 per term, ~14 per clock) fit in the device-wide step (~6K clocks)
+  p->throttle = (double)c.nq_max * 4.0 * (double)a.n / 14.0 < 6000.0 ? 1 : 0;
+  if (const char* ev = getenv("COT_RES_THROTTLE")) p->throttle = atoi(ev) != 0;
   p->iters = iters;
   p->tol = a.tol;
   p->check_every = a.check_every > 0 ? a.check_every : 1;
