@@ -468,7 +468,7 @@ def run_ours(args, rank, world, local_rank):
     clocks = clk.summary()
     cluster = getattr(R, "path", None) in (2, 3, 4)
     if cluster:   # whole problems on chip: the bound is the SFU (one MUFU.EX2 per Gibbs evaluation), DESIGN.md §6
-        ex2_launch = float(B_local_evals(p, iters))
+        ex2_launch = float(B_local_evals(p, iters)) if mode != "row_sharded" else float(p.n) * R.R * p.m * iters
         achieved_sfu = ex2_launch / (per_launch_ms / 1e3)
         mhz = clocks.get("sm_mhz") or 1965.0
         peak_sfu = 148 * 16 * mhz * 1e6

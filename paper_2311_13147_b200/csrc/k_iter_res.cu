@@ -861,9 +861,12 @@ bool res_config(int64_t n, int64_t m, int64_t R, int64_t Rlo, int sms, int nrank
               nsq, nstream, L.total, (L.total > (size_t)kResMaxSmem || !stream_ok) ? " (does not fit)" : "");
     if (L.total > (size_t)kResMaxSmem || !stream_ok) continue;
     ResCfg c{h, W, ncl, MR, nq_max, tq, nsq, L.total};
-    // fewest quads per CTA (the k-sum bound, a streamed quad counting double); ties: the smaller cluster
+    // fewest quads per CTA (the k-sum bound, a streamed quad counting double); ties: the larger cluster while a CTA
+    // holds few row pieces (fewer CTAs per column group, fewer contributions per column sum: the 8-way C4 shard
+    // runs 6.38 / 5.78 / 5.66 us per iteration at h = 1 / 2 / 4), else the smaller one (C3: 7 rows per CTA at h = 1,
+    // 14 at h = 2, whose longer column pass outweighs the cheaper reduction: 12.8K vs 13.5K cycles per iteration)
     const int cost = nq_max + nstream, best_cost = best.nq_max + std::max(0, best.nq_max - kResKT * best.tq - best.nsq);
-    if (!found || cost < best_cost) {
+    if (!found || cost < best_cost || (cost == best_cost && MR0 <= 8 && h > best.h)) {
       best = c;
       found = true;
     }
