@@ -62,6 +62,9 @@ struct TmaParams {
   int pre;               // precomputed mode (NEXT-1): C is S [R][m] (n = 1) and s_ij = S_ij
   int kres;              // k-blocks [0, kres) of the CTA's rows are resident in shared memory (loaded once per
                          // launch); only [kres, n) is streamed through the ring every iteration
+  int ktm;               // k-blocks [kres, kres + ktm) of the CTA's rows are resident in TENSOR memory (each k-sum
+                         // thread's own columns of them, loaded once per launch; a multiple of 4): the ring
+                         // streams [kres + ktm, n)
   int rpw;               // row-per-warp epilogue (several rows per CTA, EPT == 1): no block reduction per row
   int det;               // deterministic mode: 128-bit fixed-point column partials (implies rpw); 2 lines per value
   unsigned long long* trace;   // diagnostics: [grid][8] cycle counters, or nullptr
@@ -379,7 +382,13 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
                                                     __float2int_rn(g4.z * c2), __float2int_rn(g4.w * c2));
     }
   }
+  if (warp == 0 && p.ktm > 0) {   // all 512 TMEM columns (one CTA per SM): the TMEM-resident k-blocks
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&ctl[12])));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
 
   // deterministic mode: the 128-bit fixed point (8 integer bits) holds every column partial only if
   // sum(alpha) < 2^7 (cerot_init flags larger masses); such a launch refuses to iterate (COT_E_ARG)
@@ -408,7 +417,7 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       for (int t = 0; t < p.iters; ++t) {
         for (int i = i0; i < i1; ++i) {
           const uint64_t pol = i < p.evict_last_rows ? pol_last : pol_first;
-          for (int k0 = p.kres; k0 < n; k0 += KS) {
+          for (int k0 = p.kres + p.ktm; k0 < n; k0 += KS) {
             if (lds_volatile(&ctl[2])) goto producer_done;
             const int kk = min(KS, n - k0);
             const long long tw0 = p.trace ? clock64() : 0;
@@ -470,6 +479,25 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       }
     };
     if (active0) load_g(i0);
+    // TMEM-resident k-blocks: thread kt's words ((r * ktm + kk) * CPT + q) * 4 + v of its lane (warp w reads
+    // lanes 32 (w mod 4) ..; two warps of a lane quarter split its 512 columns), loaded once per launch
+    const unsigned tcols = 512u / (unsigned)((nk + 3) / 4);
+    const unsigned tb = ctl[12] + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(warp >> 2) * tcols;
+    if (p.ktm > 0 && active0) {
+      for (int r = 0; r < nrows; ++r)
+        for (int kk = 0; kk < p.ktm; ++kk)
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            const int jv = q * nkt + kt;
+            const float4 v = jv < mv ? __ldg(reinterpret_cast<const VT*>(p.C + ((size_t)(p.kres + kk) * R + i0 + r) * m) + jv)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             tb + (unsigned)(((r * p.ktm + kk) * CPT + q) * 4)),
+                         "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
+                         "r"(__float_as_uint(v.w)));
+          }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
     const int total_rows = p.iters * nrows;
     for (int rr = 0; active0 && rr < total_rows; ++rr) {
       // CTA-uniform (k-sum warps) check of the halt flag
@@ -504,6 +532,36 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
           for (; k + 4 <= p.kres; k += 4) ksum4<CPT>(rb + (size_t)k * mv, mv, nkt, kt, c2, gc, s);
           for (; k < p.kres; ++k) ksum1<CPT>(rb + (size_t)k * mv, nkt, kt, c2, gc, s);
         }
+      }
+      if (p.ktm > 0) {   // the TMEM-resident k-blocks, four k-rows per load (the same grouping and order as ksum4)
+        const unsigned tr = tb + (unsigned)(r * p.ktm * CPT * 4);
+        if (!(p.diag & COT_DIAG_NO_COMPUTE))
+          for (int kk = 0; kk < p.ktm; kk += 4) {
+            unsigned x[16 * CPT];
+#pragma unroll
+            for (int h = 0; h < CPT; ++h)
+              asm volatile(
+                  "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                  : "=r"(x[16 * h]), "=r"(x[16 * h + 1]), "=r"(x[16 * h + 2]), "=r"(x[16 * h + 3]), "=r"(x[16 * h + 4]),
+                    "=r"(x[16 * h + 5]), "=r"(x[16 * h + 6]), "=r"(x[16 * h + 7]), "=r"(x[16 * h + 8]),
+                    "=r"(x[16 * h + 9]), "=r"(x[16 * h + 10]), "=r"(x[16 * h + 11]), "=r"(x[16 * h + 12]),
+                    "=r"(x[16 * h + 13]), "=r"(x[16 * h + 14]), "=r"(x[16 * h + 15])
+                  : "r"(tr + (unsigned)(kk * CPT * 4 + 16 * h)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            float e[4][CPT][4];
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4)
+#pragma unroll
+              for (int q = 0; q < CPT; ++q)
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                  e[k4][q][v] = ex2(fmaf(-__uint_as_float(x[(k4 * CPT + q) * 4 + v]), c2, gc[q][v]));
+#pragma unroll
+            for (int q = 0; q < CPT; ++q)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) s[q][v] += (e[0][q][v] + e[1][q][v]) + (e[2][q][v] + e[3][q][v]);
+          }
+        k0 = p.kres + p.ktm;
       }
       for (; k0 + KS <= n; k0 += KS) {
         mbar_wait(&full[slot], phase);
@@ -580,6 +638,11 @@ __device__ __forceinline__ void iter_tma_body(const TmaParams& p, const int bid,
       } else if (done) {
         if (consumed >= lds_volatile(&ctl[0])) break;
       }
+    }
+    if (p.ktm > 0) {   // every k-sum warp is past its last TMEM read
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      asm volatile("bar.sync 3, %0;" ::"r"(nkt) : "memory");
+      if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(ctl[12]));
     }
   } else {
     // ===================================================================== epilogue warps
@@ -1366,6 +1429,14 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
   // continues a resident launch bit for bit
   if (p.kres < (int)a.n) p.kres &= ~3;
   const size_t resid_bytes = (size_t)p.rpu * p.kres * row_bytes;
+  // TMEM-resident k-blocks (after the shared-memory ones): each k-sum thread holds 4 * CPT words per (row, k-block)
+  // of its 512 / ceil(nk / 4) TMEM columns; a multiple of 4 k-blocks (the k-sum grouping); COT_KTM overrides
+  p.ktm = 0;
+  if (!rows_only && iters > 1 && !(a.flags & COT_PRECOMPUTED) && p.kres < (int)a.n) {
+    const int words = 512 / ((p.nk + 3) / 4);
+    p.ktm = std::min((int)a.n - p.kres, words / (p.rpu * cpt * 4)) & ~3;
+    if (const char* ev = getenv("COT_KTM")) p.ktm = std::min(p.ktm, std::max(0, atoi(ev)) & ~3);
+  }
   p.nslot = (int)std::max<size_t>(2, std::min<size_t>(64, (budget - queue_bytes - 4096 - resid_bytes) / slot_bytes));
   // ring + 1 KiB pad (branch-free over-reads past the last column stay in-bounds) + resident k-blocks + row
   // queue + row statistics + barriers + control + reduction scratch
