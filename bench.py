@@ -518,6 +518,10 @@ def run_ours(args, rank, world, local_rank):
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src,
                      "traffic": None if trf is None else trf * (iters if R.persistent else 1),
+                     # the DRAM bytes ncu measured (profiles/ncu_summary.json) over the same launch time: below the
+                     # algorithmic bytes where k-blocks are resident on chip (shared memory, TMEM), so this is
+                     # the kernel's actual HBM utilisation, `frac` the algorithmic-bytes one
+                     "traffic_frac": None if trf is None else trf * (iters if R.persistent else 1) / (per_launch_ms / 1e3) / 1e9 / peak,
                      "algorithmic_bytes_per_launch": bytes_launch, "algorithmic_bytes_per_iter": bytes_iter,
                      "launch_ms_mean": per_launch_ms, "launch_samples": nsamp, "share_of_step": dom_share,
                      "us_per_iter": it_mean * 1e3 / iters}),
