@@ -184,6 +184,16 @@ __device__ __forceinline__ unsigned long long ld_poll(const unsigned long long* 
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// one column sum polled until its count is `want` (acquire: the sum's contributions are then all visible)
+__device__ __forceinline__ bool poll_sum1(const unsigned long long* p, unsigned want, unsigned long long& v) {
+  unsigned long long t0 = 0;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if ((unsigned)(v >> 56) == want) return true;
+    if (t0 == 0) t0 = res_timer();
+    else if (res_timer() - t0 > kResTimeoutNs) return false;
+  }
+}
 // the thread's columns j = et + k * kResET < W (k < 4), polled together until every count is `want`
 __device__ __forceinline__ bool poll_sums4(const unsigned long long* base, int et, int W, unsigned want,
                                            unsigned long long (&v)[4]) {
@@ -633,8 +643,12 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
           P3 = fma(f, ldexp_pos(s4.w, k4.w - a4.w - kM) * fb.y, P3);
         }
         ulonglong2* cb2 = reinterpret_cast<ulonglong2*>(colbuf + 4 * cq);
-        cb2[0] = make_ulonglong2(P0 > 0.0 ? __double2ull_rz(P0 * scale) : 0ull, P1 > 0.0 ? __double2ull_rz(P1 * scale) : 0ull);
-        cb2[1] = make_ulonglong2(P2 > 0.0 ? __double2ull_rz(P2 * scale) : 0ull, P3 > 0.0 ? __double2ull_rz(P3 * scale) : 0ull);
+        // multi-GPU: every partial carries 1 in the top byte (the rank-local sums count their contributions)
+        const unsigned long long one = fused ? kCntOne : 0ull;
+        cb2[0] = make_ulonglong2(one | (P0 > 0.0 ? __double2ull_rz(P0 * scale) : 0ull),
+                                 one | (P1 > 0.0 ? __double2ull_rz(P1 * scale) : 0ull));
+        cb2[1] = make_ulonglong2(one | (P2 > 0.0 ? __double2ull_rz(P2 * scale) : 0ull),
+                                 one | (P3 > 0.0 ? __double2ull_rz(P3 * scale) : 0ull));
       }
       ebar();
       mark(3);
@@ -648,15 +662,19 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
         const int j = et + k * kResET;
         if (j < W) red_add_gpu(dst + j, colbuf[j]);
       }
-      ebar();
+      if (!fused) ebar();
       if (et == 0) {
         mbar_arrive(sgo);   // the k-sum warps compute the next iteration's s' while this one is reduced
         mbar_arrive(&sempty[buf]);
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.lcnt + q) : "memory");
-        if (!wait_count(p.lcnt + q, (unsigned)p.ncl * (unsigned)(T + 1ull))) ctl[RCTL_TIMEOUT] = 1u;
+        if (fused) {   // (the counter is kept in step for a later unsharded launch on this workspace; no wait)
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.lcnt + q) : "memory");
+        } else {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.lcnt + q) : "memory");
+          if (!wait_count(p.lcnt + q, (unsigned)p.ncl * (unsigned)(T + 1ull))) ctl[RCTL_TIMEOUT] = 1u;
+        }
       }
-      ebar();
+      if (!fused) ebar();
       mark(4);
       // [multi-GPU] push this CTA's 1/ncl slice of the group's rank-local sums into every rank's exchange sums
       // with system-scope reductions; each pushed value carries 1 in its top byte, so a rank's exchange sum of a
@@ -669,16 +687,22 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
         }
         for (int jj = js0 + et; jj < js1; jj += kResET) {
           const int j = col0 + jj;
-          unsigned long long v;
-          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(lsum + (size_t)sT * m + j) : "memory");
+          unsigned long long v;   // the group's rank-local sum of the column, complete when its count is ncl
+          if (!poll_sum1(lsum + (size_t)sT * m + j, (unsigned)p.ncl, v)) {
+            timeout = true;
+            break;
+          }
           v = (v & kValMask) | kCntOne;
           for (int r = 0; r < nr; ++r) {   // the own rank's copy at GPU scope, the peers' at system scope
             if (r == p.rank) red_add_gpu(p.xsum[r] + (size_t)sX * m + j, v);
             else red_add_sys(p.xsum[r] + (size_t)sX * m + j, v);
           }
+          // the pusher is the only reader of this rank-local sum: zero it now (the slot is reused three iterations
+          // on, by CTAs that observed this thread's later pushes; the fence before those orders this store)
+          st_relaxed_sys(lsum + (size_t)sT * m + j, 0ull);
         }
       }
-      timeout = ctl[RCTL_TIMEOUT] != 0u;
+      if (ctl[RCTL_TIMEOUT]) timeout = true;
       const unsigned long long* src = fused ? xown + (size_t)sX * m : lsum + (size_t)sT * m;
       // ---- q-update of the own columns: z_j += log beta_j - log c_j (every CTA of the group, same bits)
       // in split form, multiplicatively: 2^{kz_j} Fz_j <- 2^{kz_j} Fz_j beta_j / c_j, renormalised by exponent bits
@@ -706,8 +730,8 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
       }
       // ---- zero this CTA's slice of the previous slot (read by every CTA before its reduction of this iteration)
       for (int j = js0 + et; j < js1; j += kResET) {
-        st_relaxed_sys(lsum + (size_t)sTp * m + col0 + j, 0ull);
-        if (fused) st_relaxed_sys(xown + (size_t)sXp * m + col0 + j, 0ull);
+        if (fused) st_relaxed_sys(xown + (size_t)sXp * m + col0 + j, 0ull);   // (rank-local slots: at the push)
+        else st_relaxed_sys(lsum + (size_t)sTp * m + col0 + j, 0ull);
       }
       timeout = bar_or(timeout);
       mark(5);
