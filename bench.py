@@ -255,66 +255,67 @@ class ShardedRunner:
         self.p, self.iters, self.stream = p, iters, stream
         self.B, self.n, self.m = 1, p.n, p.m
         self.row_begin, self.R = cdist.row_partition(p.m, world, rank)
-        # fused (default): the exchange inside the persistent kernel over peer-mapped buffers (cerot_iter_fused);
-        # COT_SHARD_IMPL=nccl: the baseline, one ncclAllReduce + 3 launches per iteration (cerot_iter_sharded)
-        self.fused = os.environ.get("COT_SHARD_IMPL", "fused") == "fused"
+        # fused (default): the exchange inside the persistent kernel over peer-mapped buffers (cerot_iter_fused),
+        # mapped with CUDA IPC, else (IPC refused, or its probe failed) as NCCL symmetric memory (the same kernel
+        # over ncclCommWindowRegister'ed buffers); COT_SHARD_IMPL=ncclwin: only the latter; COT_SHARD_IMPL=nccl:
+        # the baseline, one ncclAllReduce + 3 launches per iteration (cerot_iter_sharded)
+        impl = os.environ.get("COT_SHARD_IMPL", "fused")
+        kinds = {"fused": ["ipc", "ncclwin"], "ncclwin": ["ncclwin"]}.get(impl, [])
         self.flags = int(os.environ.get("COT_BENCH_FLAGS", "0"), 0)   # e.g. 0x10: COT_DETERMINISTIC
         self.fused_note = None
+        import torch.distributed as tdist
+
+        def agree(ok):   # every rank must take the same path
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+            if tdist.is_initialized():
+                tdist.all_reduce(flag, op=tdist.ReduceOp.MIN)
+            return int(flag.item()) == 1
         with stdout_to_stderr():
             self.comm = cdist.NcclComm()
-            self.xchg = None
-            if self.fused:
-                # the peer mappings need CUDA IPC between the ranks' GPUs; every rank must agree on the path
-                ok, err = 1, ""
-                try:
-                    self.xchg = cdist.PeerExchange(p.m)
-                except Exception as e:   # e.g. IPC not permitted in this container
-                    ok, err = 0, str(e)
-                flag = torch.tensor([ok], dtype=torch.int32, device=dev)
-                import torch.distributed as tdist
-                if tdist.is_initialized():
-                    tdist.all_reduce(flag, op=tdist.ReduceOp.MIN)
-                if int(flag.item()) == 0:
-                    if self.xchg is not None:
-                        self.xchg.close()
-                        self.xchg = None
-                    self.fused = False
-                    self.fused_note = f"fused exchange unavailable ({err or 'on another rank'}): NCCL baseline"
-                    print(f"[bench] {self.fused_note}", file=sys.stderr)
+        self.xchg = None
         Cl = np.ascontiguousarray(p.C[:, self.row_begin:self.row_begin + self.R, :])
         self.Cl_host = Cl
         self.sh = cdist.ShardedCerot(torch.as_tensor(Cl, device=dev), torch.as_tensor(p.alpha, device=dev),
                                      torch.as_tensor(p.beta, device=dev), float(p.eps[0]), self.row_begin, p.m,
                                      comm=self.comm, stream=stream)
-        if self.fused:
-            # probe: a few fused iterations must complete on every rank (peer stores visible, no COT_E_PEER)
-            # before the bench relies on the path; otherwise every rank falls back to the NCCL baseline
-            ok, err = 1, ""
+        self.xkind, notes = None, []
+        for kind in kinds:
+            ok, err = True, ""
             try:
                 with stdout_to_stderr():
-                    self.sh.init().iterate_fused(self.xchg, 3)
-                    if self.sh.state()[0] != 3:
-                        ok, err = 0, "probe iterations incomplete"
-            except Exception as e:
-                ok, err = 0, str(e)
-            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
-            import torch.distributed as tdist
-            if tdist.is_initialized():
-                tdist.all_reduce(flag, op=tdist.ReduceOp.MIN)
-            if int(flag.item()) == 0:
+                    self.xchg = cdist.PeerExchange(p.m) if kind == "ipc" else cdist.NcclWindowExchange(p.m, self.comm)
+            except Exception as e:   # e.g. IPC not permitted in this container, no NCCL symmetric memory
+                ok, err = False, str(e)
+            if agree(ok):
+                # probe: a few fused iterations must complete on every rank (peer stores visible, no COT_E_PEER)
+                try:
+                    with stdout_to_stderr():
+                        self.sh.init().iterate_fused(self.xchg, 3)
+                        if self.sh.state()[0] != 3:
+                            ok, err = False, "probe iterations incomplete"
+                except Exception as e:
+                    ok, err = False, str(e)
+                if agree(ok):
+                    self.xkind = kind
+                    break
+                err = "probe failed: " + (err or "on another rank")
+            if self.xchg is not None:
                 self.xchg.close()
                 self.xchg = None
-                self.fused = False
-                self.fused_note = f"fused exchange probe failed ({err or 'on another rank'}): NCCL baseline"
-                print(f"[bench] {self.fused_note}", file=sys.stderr)
+            notes.append(f"{kind}: {err or 'unavailable on another rank'}")
+            print(f"[bench] fused exchange over {kind} not used ({notes[-1]})", file=sys.stderr)
+        self.fused = self.xkind is not None
+        if not self.fused and kinds:
+            self.fused_note = "fused exchange unavailable (" + "; ".join(notes) + "): NCCL baseline"
         # flags actually run: the NCCL baseline has no fixed-point partials (COT_DETERMINISTIC is the fused path's)
         self.flags_requested = self.flags
         if not self.fused and self.flags & 0x10:
             self.flags &= ~0x10
             self.fused_note = (self.fused_note or "NCCL baseline") + "; COT_DETERMINISTIC dropped (fused path only)"
-        self.exchange = {"path": "fused" if self.fused else "nccl",
-                         "probe": ("ok (3 fused iterations on every rank)" if self.fused else
-                                   (self.fused_note or "not attempted (COT_SHARD_IMPL=nccl)"))}
+        self.exchange = {"path": ("fused" + ("" if self.xkind == "ipc" else " (NCCL symmetric memory)")) if self.fused
+                         else "nccl",
+                         "probe": ("ok (3 fused iterations on every rank" + (", " + "; ".join(notes) if notes else "")
+                                   + ")") if self.fused else (self.fused_note or "not attempted (COT_SHARD_IMPL=nccl)")}
         d = p.n * p.m
         self.Tl = torch.empty_like(self.sh.C)
         self.Trows = torch.empty((p.n, self.R, d), dtype=self.sh.C.dtype, device=dev)

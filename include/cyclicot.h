@@ -291,6 +291,17 @@ int cot_xchg_alloc(int64_t m, int nranks, void** xbuf, void* ipc_handle);
 int cot_xchg_open(const void* ipc_handle, void** peer_xbuf);
 int cot_xchg_close(void* peer_xbuf);
 int cot_xchg_free(void* xbuf);
+/* The same exchange buffers as NCCL symmetric memory (NCCL >= 2.27 device API; for processes where CUDA   */
+/* IPC handles cannot be shared): COLLECTIVE over `comm` (cot_comm_init) -- every rank allocates its       */
+/* cot_xchg_bytes(m, nranks) buffer with ncclMemAlloc (zeroed) and registers it with                       */
+/* ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC); *xbuf = this rank's buffer (DEVICE), *win = the window. */
+/* cot_xchg_nccl_peers writes (HOST array [nranks]) the device address of every rank's copy as mapped into */
+/* this process (the window's load/store-accessible peer pointers: ncclGetPeerPointer), i.e. the xbufs of  */
+/* cerot_iter_fused. cot_xchg_nccl_free deregisters (collective) and frees. COT_E_NCCL if the loaded NCCL  */
+/* has no symmetric-memory API or the registration fails.                                                  */
+int cot_xchg_nccl_alloc(void* comm, int64_t m, int nranks, void** xbuf, void** win);
+int cot_xchg_nccl_peers(void* win, int nranks, void** peers);
+int cot_xchg_nccl_free(void* comm, void* xbuf, void* win);
 /* `iters` fused iterations of this rank. xbufs: HOST array [nranks] of DEVICE pointers, rank q's         */
 /* exchange buffer as addressed by this process (xbufs[rank] = own buffer). Other arguments and the       */
 /* state / potentials as cerot_iter_sharded; cerot_init first (per rank). Asynchronous.                  */

@@ -97,6 +97,10 @@ _SIGS = {
     "cot_xchg_open": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_void_p)]),
     "cot_xchg_close": (ctypes.c_int, [_vp]),
     "cot_xchg_free": (ctypes.c_int, [_vp]),
+    "cot_xchg_nccl_alloc": (ctypes.c_int, [_vp, _i64, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
+                                           ctypes.POINTER(ctypes.c_void_p)]),
+    "cot_xchg_nccl_peers": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "cot_xchg_nccl_free": (ctypes.c_int, [_vp, _vp, _vp]),
     "cerot_iter_fused": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl,
                                         _i64, _u32, _vp, _vp, _vp, _sz, ctypes.c_int, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_void_p), _vp]),

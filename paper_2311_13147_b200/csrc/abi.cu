@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nccl_device.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -103,8 +104,13 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // NCCL >= 2.27 symmetric memory (optional): the fused exchange over NCCL-registered windows
+  ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void*) = nullptr;
+  ncclResult_t (*CommWindowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+  ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
 };
-static NcclApi& nccl() {
+static NcclApi& nccl_api() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -119,10 +125,21 @@ static NcclApi& nccl() {
     api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
     api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.MemAlloc = (decltype(api.MemAlloc))dlsym(h, "ncclMemAlloc");
+    api.MemFree = (decltype(api.MemFree))dlsym(h, "ncclMemFree");
+    api.CommWindowRegister = (decltype(api.CommWindowRegister))dlsym(h, "ncclCommWindowRegister");
+    api.CommWindowDeregister = (decltype(api.CommWindowDeregister))dlsym(h, "ncclCommWindowDeregister");
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString;
     if (!api.ok) api.err = "libnccl.so.2 lacks a required symbol";
   });
   return api;
+}
+
+// Device addresses of every rank's copy of an NCCL symmetric window (header-only device API: the window's LSA
+// flat base + rank stride), written to out[0 .. nranks)
+__global__ void k_window_peers(ncclWindow_t w, int nranks, void** out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    for (int r = 0; r < nranks; ++r) out[r] = ncclGetPeerPointer(w, 0, r);
 }
 
 size_t xchg_res_offset(int64_t m, int nranks) {
@@ -145,7 +162,7 @@ using namespace cot;
   do {                                                                            \
     ncclResult_t _r = (expr);                                                     \
     if (_r != ncclSuccess) {                                                      \
-      set_error(std::string(#expr) + ": " + nccl().GetErrorString(_r));          \
+      set_error(std::string(#expr) + ": " + nccl_api().GetErrorString(_r));          \
       return COT_E_NCCL;                                                          \
     }                                                                             \
   } while (0)
@@ -214,7 +231,7 @@ static int plan_and_report(const IterArgs& a, const Workspace& ws, void* T_block
   COT_CHECK_CUDA(launch_plan(a, ws, up, T_blocks, s));
   COT_CHECK_CUDA(launch_plan_reduce_local(a, ws, up, ws.plan_buf, s));
   if (comm) {
-    COT_CHECK_NCCL(nccl().AllReduce(ws.plan_buf, ws.plan_buf, (size_t)(a.B * (kPlanBufHead + a.m)), ncclFloat64,
+    COT_CHECK_NCCL(nccl_api().AllReduce(ws.plan_buf, ws.plan_buf, (size_t)(a.B * (kPlanBufHead + a.m)), ncclFloat64,
                                     ncclSum, (ncclComm_t)comm, s));
   }
   COT_CHECK_CUDA(launch_plan_finalize_buf(a, ws, ws.plan_buf, d_report ? d_report : ws.report, s));
@@ -726,12 +743,12 @@ int csrot_solve(const double* alpha, const double* beta, const void* C, int64_t 
 // ------------------------------------------------------------------------------------- row sharding
 int cot_nccl_unique_id(void* id128) {
   if (!id128) return arg_error("cot_nccl_unique_id: NULL output");
-  if (!nccl().ok) {
-    set_error(nccl().err);
+  if (!nccl_api().ok) {
+    set_error(nccl_api().err);
     return COT_E_NCCL;
   }
   ncclUniqueId id;
-  COT_CHECK_NCCL(nccl().GetUniqueId(&id));
+  COT_CHECK_NCCL(nccl_api().GetUniqueId(&id));
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
   memcpy(id128, &id, sizeof(id));
   return COT_OK;
@@ -739,25 +756,84 @@ int cot_nccl_unique_id(void* id128) {
 
 int cot_comm_init(const void* id128, int nranks, int rank, void** comm) {
   if (!id128 || !comm || nranks < 1 || rank < 0 || rank >= nranks) return arg_error("cot_comm_init: bad arguments");
-  if (!nccl().ok) {
-    set_error(nccl().err);
+  if (!nccl_api().ok) {
+    set_error(nccl_api().err);
     return COT_E_NCCL;
   }
   ncclUniqueId id;
   memcpy(&id, id128, sizeof(id));
   ncclComm_t c = nullptr;
-  COT_CHECK_NCCL(nccl().CommInitRank(&c, nranks, id, rank));
+  COT_CHECK_NCCL(nccl_api().CommInitRank(&c, nranks, id, rank));
   *comm = c;
+  return COT_OK;
+}
+
+int cot_xchg_nccl_alloc(void* comm, int64_t m, int nranks, void** xbuf, void** win) {
+  const size_t bytes = cot_xchg_bytes(m, nranks);
+  if (!comm || !bytes || !xbuf || !win) return arg_error("cot_xchg_nccl_alloc: need comm, m >= 1, 1 <= nranks <= 8, outputs");
+  if (!nccl_api().ok) {
+    set_error(nccl_api().err);
+    return COT_E_NCCL;
+  }
+  if (!nccl_api().MemAlloc || !nccl_api().CommWindowRegister) {
+    set_error("cot_xchg_nccl_alloc: the loaded NCCL has no symmetric-memory API (ncclMemAlloc / ncclCommWindowRegister)");
+    return COT_E_NCCL;
+  }
+  const size_t padded = (bytes + 4095) / 4096 * 4096;   // NCCL_WIN_REQUIRED_ALIGNMENT
+  void* p = nullptr;
+  COT_CHECK_NCCL(nccl_api().MemAlloc(&p, padded));
+  cudaError_t e = cudaMemset(p, 0, padded);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    nccl_api().MemFree(p);
+    set_error(std::string("cot_xchg_nccl_alloc: ") + cudaGetErrorString(e));
+    return COT_E_CUDA;
+  }
+  ncclWindow_t w = nullptr;
+  const ncclResult_t r = nccl_api().CommWindowRegister((ncclComm_t)comm, p, padded, &w, NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess) {
+    nccl_api().MemFree(p);
+    set_error(std::string("ncclCommWindowRegister: ") + nccl_api().GetErrorString(r));
+    return COT_E_NCCL;
+  }
+  *xbuf = p;
+  *win = (void*)w;
+  return COT_OK;
+}
+
+int cot_xchg_nccl_peers(void* win, int nranks, void** peers) {
+  if (!win || nranks < 1 || nranks > kMaxRanks || !peers) return arg_error("cot_xchg_nccl_peers: bad argument");
+  void** d = nullptr;
+  COT_CHECK_CUDA(cudaMalloc(&d, sizeof(void*) * kMaxRanks));
+  k_window_peers<<<1, 32>>>((ncclWindow_t)win, nranks, d);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(peers, d, sizeof(void*) * nranks, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) {
+    set_error(std::string("cot_xchg_nccl_peers: ") + cudaGetErrorString(e));
+    return COT_E_CUDA;
+  }
+  return COT_OK;
+}
+
+int cot_xchg_nccl_free(void* comm, void* xbuf, void* win) {
+  if (!nccl_api().ok) {
+    set_error(nccl_api().err);
+    return COT_E_NCCL;
+  }
+  if (comm && win && nccl_api().CommWindowDeregister)
+    COT_CHECK_NCCL(nccl_api().CommWindowDeregister((ncclComm_t)comm, (ncclWindow_t)win));
+  if (xbuf && nccl_api().MemFree) COT_CHECK_NCCL(nccl_api().MemFree(xbuf));
   return COT_OK;
 }
 
 int cot_comm_destroy(void* comm) {
   if (!comm) return COT_OK;
-  if (!nccl().ok) {
-    set_error(nccl().err);
+  if (!nccl_api().ok) {
+    set_error(nccl_api().err);
     return COT_E_NCCL;
   }
-  COT_CHECK_NCCL(nccl().CommDestroy((ncclComm_t)comm));
+  COT_CHECK_NCCL(nccl_api().CommDestroy((ncclComm_t)comm));
   return COT_OK;
 }
 
@@ -831,8 +907,8 @@ int cerot_iter_sharded(const double* alpha, const double* beta, const void* C_lo
   if (!alpha || !beta || !C_local || !G_local || !eps || !w_hat || !z_hat)
     return arg_error("cerot_iter_sharded: NULL argument");
   if (iters < 0 || tol < 0) return arg_error("cerot_iter_sharded: iters >= 0 and tol >= 0 required");
-  if (comm && !nccl().ok) {
-    set_error(nccl().err);
+  if (comm && !nccl_api().ok) {
+    set_error(nccl_api().err);
     return COT_E_NCCL;
   }
   Workspace ws;
@@ -847,7 +923,7 @@ int cerot_iter_sharded(const double* alpha, const double* beta, const void* C_lo
     COT_CHECK_CUDA(launch_colsum(ws, up, 1, m, (int)(t & 1), ws.c_local, s));
     const double* c = ws.c_local;
     if (comm) {   // the exchange step: one m-length fp64 allreduce over NVLink / NVSwitch per iteration
-      COT_CHECK_NCCL(nccl().AllReduce(ws.c_local, ws.c_global, (size_t)m, ncclFloat64, ncclSum, (ncclComm_t)comm, s));
+      COT_CHECK_NCCL(nccl_api().AllReduce(ws.c_local, ws.c_global, (size_t)m, ncclFloat64, ncclSum, (ncclComm_t)comm, s));
       c = ws.c_global;
     }
     COT_CHECK_CUDA(launch_zupdate(c, beta, 1, m, n, tol, check_every, z_hat, ws, s));
@@ -986,8 +1062,8 @@ int cerot_plan_sharded(const double* alpha, const double* beta, const void* C_lo
   if (R < 1 || row_begin < 0 || row_begin + R > m) return arg_error("cerot_plan_sharded: bad row range");
   if (!alpha || !beta || !C_local || !G_local || !eps || !w_hat || !z_hat)
     return arg_error("cerot_plan_sharded: NULL argument");
-  if (comm && !nccl().ok) {
-    set_error(nccl().err);
+  if (comm && !nccl_api().ok) {
+    set_error(nccl_api().err);
     return COT_E_NCCL;
   }
   Workspace ws;

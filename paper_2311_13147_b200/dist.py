@@ -106,6 +106,28 @@ class PeerExchange:
             self.local = ctypes.c_void_p()
 
 
+class NcclWindowExchange:
+    """The fused path's exchange buffers as NCCL symmetric memory (ncclMemAlloc + ncclCommWindowRegister) instead
+    of CUDA IPC handles: the same cerot_iter_fused kernels, the peer addresses taken from the NCCL window. For
+    processes that cannot share CUDA IPC handles. Collective: every rank constructs (and closes) it."""
+
+    def __init__(self, m: int, comm: "NcclComm"):
+        self.comm = comm
+        self.world = comm.world
+        self.rank = comm.rank
+        self.local = ctypes.c_void_p()
+        self.win = ctypes.c_void_p()
+        _check(lib().cot_xchg_nccl_alloc(comm.handle, m, self.world, ctypes.byref(self.local), ctypes.byref(self.win)),
+               "cot_xchg_nccl_alloc")
+        self.xbufs = (ctypes.c_void_p * self.world)()
+        _check(lib().cot_xchg_nccl_peers(self.win, self.world, self.xbufs), "cot_xchg_nccl_peers")
+
+    def close(self):
+        if self.local:
+            lib().cot_xchg_nccl_free(self.comm.handle, self.local, self.win)
+            self.local = ctypes.c_void_p()
+
+
 class NcclComm:
     """A libcyclicot-owned NCCL communicator over all ranks of the default torch.distributed group."""
 

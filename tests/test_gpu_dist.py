@@ -174,3 +174,39 @@ def test_solve_sharded_single_rank_matches_solve():
                 assert abs(r[k] - reps[0][k]) <= 1e-6 * abs(reps[0][k])
     finally:
         L.cot_comm_destroy(comm)
+
+
+def test_fused_over_nccl_symmetric_memory_single_rank():
+    """The fused path's exchange buffers as NCCL symmetric memory (ncclMemAlloc + ncclCommWindowRegister, peer
+    addresses from the window) instead of CUDA IPC: one rank, the same kernels; bitwise the same iterate as the
+    IPC-mapped buffer (the exchange arithmetic does not depend on how the buffer was mapped)."""
+    L = cot.lib()
+    uid = ctypes.create_string_buffer(128)
+    assert L.cot_nccl_unique_id(uid) == 0, L.cot_last_error()
+    comm = ctypes.c_void_p()
+    assert L.cot_comm_init(uid, 1, 0, ctypes.byref(comm)) == 0, L.cot_last_error()
+
+    class _C:
+        handle = comm
+        rank = 0
+        world = 1
+    try:
+        for maker in (lambda: synthetic.c4_large(m=512, n=16), lambda: synthetic.c4_large(m=1024, n=64)):
+            p = maker()
+            b0, R = cdist.row_partition(p.m, 8, 0) if p.n == 64 else (0, p.m)
+            outs = []
+            for kind in ("ipc", "ncclwin"):
+                x = cdist.PeerExchange(p.m) if kind == "ipc" else cdist.NcclWindowExchange(p.m, _C())
+                try:
+                    sh = cdist.ShardedCerot(_dev(p.C[:, b0:b0 + R, :]), _dev(p.alpha), _dev(p.beta), float(p.eps[0]),
+                                            b0, p.m).init()
+                    sh.iterate_fused(x, 12)
+                    sh.iterate_fused(x, 8)
+                    torch.cuda.synchronize()
+                    assert sh.state()[0] == 20
+                    outs.append((sh.z_hat.cpu().numpy(), sh.w_hat.cpu().numpy()[b0:b0 + R]))
+                finally:
+                    x.close()
+            assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    finally:
+        L.cot_comm_destroy(comm)
