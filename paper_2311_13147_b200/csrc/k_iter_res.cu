@@ -776,6 +776,23 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
     if (p.trace && et == 0)
       for (int k = 0; k < 7; ++k) p.trace[(size_t)blockIdx.x * 16 + 2 + k] = tr[k];
     if (halted && et == 0) *(volatile unsigned*)&ctl[RCTL_HALT] = 1u;
+    if (halted && timeout && h > 1) {
+      // A device-wide wait of this CTA gave up (a peer never arrived) while a cluster peer may have got past it
+      // and now waits, with no time-out, for this CTA's row pieces of the next iteration: send it empty pieces so
+      // that it reaches its own device-wide wait, times out there too and halts (no hang). Never on the fast path.
+      const int bn = done & 1;
+      for (int lr = ew; lr < nrows; lr += kResNE)
+        if (lane < h) {
+          const unsigned ra = cluster_map(smem_u32(&rx[((size_t)bn * MR + lr) * h + q]), (unsigned)lane);
+          const unsigned rb = cluster_map(smem_u32(rbar), (unsigned)lane);
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra), "l"(0ull),
+                       "r"(rb)
+                       : "memory");
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra + 8u),
+                       "l"(0ull), "r"(rb)
+                       : "memory");
+        }
+    }
     ebar();
     // ---- outputs: z of the own columns (cluster 0's CTAs), w_hat of the own rows (piece 0's CTAs), state
     if (active0 && done > 0) {
