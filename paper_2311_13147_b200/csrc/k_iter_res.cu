@@ -42,6 +42,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 namespace cot {
@@ -534,49 +535,57 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
       const float4* sb = sbuf + (size_t)buf * nqmax;
       // ---- row pass: a warp takes 32 quads of one piece; their terms are summed against the warp's exact maximum
       // exponent (one REDUX), then one warp sum per (warp, piece); RB rounds of pieces in flight per thread
-      constexpr int RB = 4;
-      for (int r0 = 0; r0 * ppr < nrows; r0 += RB) {
-        int e[RB][4];
-        float4 s4[RB];
-        int mxw[RB];
-        double v[RB];
-        const int cq = et % lpp;
+      // RB rounds of pieces in flight per thread: 1 when the CTA has one round (no idle REDUX / shuffles), else 4
+      auto row_pass = [&](auto rbc) {
+        constexpr int RB = decltype(rbc)::value;
+        for (int r0 = 0; r0 * ppr < nrows; r0 += RB) {
+          int e[RB][4];
+          float4 s4[RB];
+          int mxw[RB];
+          double v[RB];
+          const int cq = et % lpp;
 #pragma unroll
-        for (int u = 0; u < RB; ++u) {
-          const int lr = (r0 + u) * ppr + et / lpp;   // warp-uniform (lpp >= 32)
-          int emax = INT_MIN;
-          if (lr < nrows) {
-            const int Q = lr * W4 + cq;
-            s4[u] = sb[Q];
-            const int4 a4 = ash[Q];
-            const int4 k4 = reinterpret_cast<const int4*>(zk)[cq];
-            e[u][0] = k4.x - a4.x;
-            e[u][1] = k4.y - a4.y;
-            e[u][2] = k4.z - a4.z;
-            e[u][3] = k4.w - a4.w;
-            emax = max(max(e[u][0], e[u][1]), max(e[u][2], e[u][3]));
+          for (int u = 0; u < RB; ++u) {
+            const int lr = (r0 + u) * ppr + et / lpp;   // warp-uniform (lpp >= 32)
+            int emax = INT_MIN;
+            if (lr < nrows) {
+              const int Q = lr * W4 + cq;
+              s4[u] = sb[Q];
+              const int4 a4 = ash[Q];
+              const int4 k4 = reinterpret_cast<const int4*>(zk)[cq];
+              e[u][0] = k4.x - a4.x;
+              e[u][1] = k4.y - a4.y;
+              e[u][2] = k4.z - a4.z;
+              e[u][3] = k4.w - a4.w;
+              emax = max(max(e[u][0], e[u][1]), max(e[u][2], e[u][3]));
+            }
+            mxw[u] = __reduce_max_sync(0xffffffffu, emax);
           }
-          mxw[u] = __reduce_max_sync(0xffffffffu, emax);
-        }
-        const double2 fa = reinterpret_cast<const double2*>(zf)[2 * cq];
-        const double2 fb = reinterpret_cast<const double2*>(zf)[2 * cq + 1];
-#pragma unroll
-        for (int u = 0; u < RB; ++u) {
-          const int lr = (r0 + u) * ppr + et / lpp;
-          v[u] = lr < nrows ? (ldexp_pos(s4[u].x, e[u][0] - mxw[u]) * fa.x + ldexp_pos(s4[u].y, e[u][1] - mxw[u]) * fa.y) +
-                                  (ldexp_pos(s4[u].z, e[u][2] - mxw[u]) * fb.x + ldexp_pos(s4[u].w, e[u][3] - mxw[u]) * fb.y)
-                            : 0.0;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int u = 0; u < RB; ++u) v[u] += __shfl_xor_sync(0xffffffffu, v[u], o);
-        if (lane == 0)
+          const double2 fa = reinterpret_cast<const double2*>(zf)[2 * cq];
+          const double2 fb = reinterpret_cast<const double2*>(zf)[2 * cq + 1];
 #pragma unroll
           for (int u = 0; u < RB; ++u) {
             const int lr = (r0 + u) * ppr + et / lpp;
-            if (lr < nrows) chunk[lr * cpp + cq / 32] = make_double2(v[u], (double)mxw[u]);
+            v[u] = lr < nrows ? (ldexp_pos(s4[u].x, e[u][0] - mxw[u]) * fa.x + ldexp_pos(s4[u].y, e[u][1] - mxw[u]) * fa.y) +
+                                    (ldexp_pos(s4[u].z, e[u][2] - mxw[u]) * fb.x + ldexp_pos(s4[u].w, e[u][3] - mxw[u]) * fb.y)
+                              : 0.0;
           }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < RB; ++u) v[u] += __shfl_xor_sync(0xffffffffu, v[u], o);
+          if (lane == 0)
+#pragma unroll
+            for (int u = 0; u < RB; ++u) {
+              const int lr = (r0 + u) * ppr + et / lpp;
+              if (lr < nrows) chunk[lr * cpp + cq / 32] = make_double2(v[u], (double)mxw[u]);
+            }
+        }
+      };
+      {
+        const int rounds = (nrows + ppr - 1) / ppr;
+        if (rounds <= 1) row_pass(std::integral_constant<int, 1>{});
+        else row_pass(std::integral_constant<int, 4>{});
       }
       ebar();
       mark(1);
