@@ -13,26 +13,31 @@
 // consecutive columns, all n k-blocks) are its work items.
 //
 //   k-sum warps (8): s'_ij of every quad of the CTA for iteration t+1 while the epilogue still works on t
-//     (the k-sums do not depend on the potentials), double-buffered in shared memory (mbarriers). Quad Q of
-//     thread kt = Q % 256 sits in the thread's 1 KiB TMEM column range (tcgen05.ld) while it has room, else
-//     in shared memory.
-//   epilogue warps (4), per iteration:
-//     row pass: t'_ij = s'_ij 2^{kz_j - a_ij - kM} Fz_j with an exact per-32-quad shift kM (integer maximum,
-//       one REDUX), piece sums combined with exact power-of-two rescaling; with h > 1 the pieces' (sum, shift)
-//       pairs go to every CTA of the cluster through DSMEM (st.shared::cluster + remote mbarrier arrival), so
-//       all h CTAs hold the identical row sum r_i and shift kM_i;
+//     (the k-sums do not depend on the potentials), double-buffered in shared memory (mbarriers); throttled to
+//     start when iteration t's reduction is issued when they are short. Quad Q of thread kt = Q % 256 sits in
+//     the thread's TMEM column range (tcgen05.ld) while it has room, else in shared memory, else (a shard
+//     slightly over the capacity) it is streamed from L2 every iteration.
+//   epilogue warps (8), per iteration:
+//     row pass: t'_ij = s'_ij 2^{kz_j - a_ij - kM} Fz_j with an exact per-warp shift kM (integer maximum, one
+//       REDUX), piece sums combined with exact power-of-two rescaling (one warp per row); with h > 1 the
+//       pieces' (sum, shift) pairs go to every CTA of the cluster with st.async + the receiver's mbarrier
+//       transaction count, so all h CTAs hold the identical row sum r_i and shift kM_i;
 //     column pass: P_j = sum_i (alpha_i / r_i) t_ij over the CTA's rows, converted to 64-bit unsigned fixed
-//       point (scale 2^S with 2^(61-S) >= sum alpha: every column sum fits) and added with red.global.add.u64
-//       into the column sums of the iteration -- integer addition, so the sums do not depend on the order in
-//       which CTAs (or ranks) arrive: deterministic, and bitwise the same on every rank;
-//     device-wide step: one cumulative arrival counter per column group (the CTAs holding the same columns);
-//       [multi-GPU: after the local counter, each CTA pushes a 1/ncl slice of its group's rank-local sums into
-//       every rank's exchange buffer with system-scope reductions, then waits for the exchange counter];
-//       every CTA then reads the W column sums of its own columns and applies the q-update
-//       z_j += log beta_j - log c_j itself (no owner hop); the freeze-rule monitor n sum_j |c_j - beta_j| is
-//       formed by every CTA from all m sums in a fixed order on the iterations that need it.
-//   Sum buffers rotate over three slots by the absolute reduction index (workspace epoch), each CTA zeroing
-//   its 1/ncl slice of the previous slot after its wait: no per-iteration memset, no grid barrier.
+//       point (scale 2^S, 2^(53-S) >= sum alpha: every column sum fits below the count byte) and added with
+//       coalesced red.global.add.u64 into the iteration's column sums -- integer addition, so the sums do not
+//       depend on the order in which CTAs (or ranks) arrive: deterministic, and bitwise the same on every rank;
+//     device-wide step, one GPU: one cumulative arrival counter per column group (the CTAs holding the same
+//       columns), then every CTA reads its W column sums;
+//     device-wide step, sharded (cerot_iter_fused): every partial carries 1 in its top byte, so the rank-local
+//       sum of a column counts its contributions; the owner of each 1/ncl column slice polls its columns until
+//       the count is ncl, pushes the sums (again with 1 in the top byte) into every rank's exchange sums with
+//       system-scope reductions and zeroes its rank-local slot; every CTA polls its W exchange columns until
+//       their count is nranks. No fence, counter or CTA barrier after the reductions.
+//     q-update (every CTA of a group, same bits): 2^{kz_j} Fz_j <- 2^{kz_j} Fz_j beta_j / c_j, renormalised from
+//       the exponent bits (no log / exp per column); the freeze-rule monitor n sum_j |c_j - beta_j| is formed by
+//       every CTA from all m sums in a fixed order on the iterations that need it.
+//   Sum buffers rotate over three slots by the absolute reduction index (workspace / exchange epochs); slots
+//   are zeroed by their owners after the last read (no per-iteration memset, no grid barrier).
 #include "common.cuh"
 #include "internal.h"
 
