@@ -1391,7 +1391,9 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
   while (KS * 2 <= 16 && KS * 2 * row_bytes <= ks_bytes && KS * 2 <= (int)a.n) KS *= 2;
   p.KS = KS;
   const size_t slot_bytes = (size_t)p.KS * row_bytes;
-  p.qn = std::max(1, std::min(p.rpu, 8));
+  // row-queue depth: 6 (the smem it frees goes to the TMA ring: C4, 7 rows per CTA, 32.0 -> 31.0 us per
+  // iteration with the TMEM / L2-resident blocks; 4-6 measured flat)
+  p.qn = std::max(1, std::min(p.rpu, 6));
   if (const char* ev = getenv("COT_QN")) p.qn = std::max(1, atoi(ev));
   p.qn = std::max(p.qn, std::min(p.rpu, 4));   // the epilogue holds up to one batch (<= 4 rows) of queue slots
   const size_t gsh_bytes = (size_t)p.rpu * m * 4;   // the integer shifts a_ij
@@ -1403,6 +1405,9 @@ cudaError_t tma_config(const IterArgs& a, const Workspace& ws, int iters, bool r
   p.det = (a.flags & COT_DETERMINISTIC) ? 1 : 0;
   if (p.det && (p.rpu > 8 || rows_only)) return cudaErrorInvalidValue;   // the deterministic mode needs rpw
   p.rpw = ((ept == 1 && p.rpu <= 8 && !(rpwv && atoi(rpwv) == 0)) || p.det) ? 1 : 0;
+  // the row-per-warp epilogue waits for all rows of an iteration before it releases their slots: the queue must
+  // hold every row of the unit
+  if (p.rpw) p.qn = std::max(p.qn, p.rpu);
   const size_t rpw_bytes = p.rpw ? (size_t)m * 12 + (size_t)p.rpu * m * 8 : 0;
   const size_t queue_bytes = (size_t)p.qn * row_bytes + (p.gsh ? gsh_bytes : 0) + (size_t)p.rpu * 6 * 8 +
                              (size_t)kColScratch * 8 + rpw_bytes;
