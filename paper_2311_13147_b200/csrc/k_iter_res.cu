@@ -880,6 +880,7 @@ bool res_config(int64_t n, int64_t m, int64_t R, int64_t Rlo, int sms, int nrank
   if (const char* ev = getenv("COT_RES_H")) force_h = atoi(ev);
   bool found = false;
   ResCfg best{};
+  double best_cost = 0.0;
   for (int h : {1, 2, 4}) {
     if (force_h && h != force_h) continue;
     if (m > 1024 || m % h != 0 || (m / h) % 128 != 0) continue;
@@ -916,12 +917,14 @@ bool res_config(int64_t n, int64_t m, int64_t R, int64_t Rlo, int sms, int nrank
               nsq, nstream, L.total, (L.total > (size_t)kResMaxSmem || !stream_ok) ? " (does not fit)" : "");
     if (L.total > (size_t)kResMaxSmem || !stream_ok) continue;
     ResCfg c{h, W, ncl, MR, nq_max, tq, nsq, L.total};
-    // fewest quads per CTA (the k-sum bound, a streamed quad counting double); ties: the larger cluster while a CTA
-    // holds few row pieces (fewer CTAs per column group, fewer contributions per column sum: the 8-way C4 shard
-    // runs 6.38 / 5.78 / 5.66 us per iteration at h = 1 / 2 / 4), else the smaller one (C3: 7 rows per CTA at h = 1,
-    // 14 at h = 2, whose longer column pass outweighs the cheaper reduction: 12.8K vs 13.5K cycles per iteration)
-    const int cost = nq_max + nstream, best_cost = best.nq_max + std::max(0, best.nq_max - kResKT * best.tq - best.nsq);
-    if (!found || cost < best_cost || (cost == best_cost && MR0 <= 8 && h > best.h)) {
+    // fewest quads per CTA (the k-sum bound, a streamed quad counting double), scaled by the share of the SMs the
+    // grid leaves idle (4-CTA clusters co-reside 33 at a time: 132 of 148 SMs); ties: the larger cluster while a
+    // CTA holds few row pieces (fewer contributions per column sum), else the smaller one. Measured: the 8-way C4
+    // shard 5.17 / 4.69 / 4.79 us per iteration at h = 1 / 2 / 4, the 4-way 9.65 (h = 2) / 9.73 (h = 4); C3 7
+    // rows per CTA at h = 1 vs 14 at h = 2, whose longer column pass outweighs the cheaper reduction
+    const double cost = (double)(nq_max + nstream) * (double)sms / (double)(ncl * h);
+    if (!found || cost < best_cost * 0.999 || (cost <= best_cost * 1.001 && MR0 <= 8 && h > best.h)) {
+      best_cost = cost;
       best = c;
       found = true;
     }
