@@ -409,35 +409,54 @@ __device__ __forceinline__ void res_body(const ResParams& p, const int b) {
         }
         out[Q] = make_float4(s0, s1, s2, s3);
       }
-      // quads beyond the on-chip capacity (streamed from L2 every iteration, a shard that does not quite fit:
-      // the 4-GPU C4 shard): eight k-rows per step, the next eight loaded while these are summed
-      for (int Q = kt + kResKT * p.tq; Q < nq; Q += kResKT) {
-        if (Q - kResKT * p.tq < p.nsq) continue;
-        const int lr = Q / W4, cq = Q - lr * W4;
-        const float4* src = reinterpret_cast<const float4*>(p.C + ((size_t)lr0 + lr) * m + col0) + cq;
+      // quads beyond the on-chip capacity (streamed from L2 every iteration: a shard that does not quite fit, the
+      // 4-GPU C4 shard): the k-blocks of each such quad are split over 4 consecutive lanes (16 k-rows each at
+      // n = 64, eight loads in flight per lane) so the loads' latency is paid in parallel, and the four parts are
+      // combined by a fixed shuffle tree
+      {
+        const int qs0 = kResKT * p.tq + p.nsq;   // first streamed quad
+        const int items = max(0, nq - qs0) * 4;
+        const int kc = (n + 3) / 4;              // k-rows per part
         const size_t ks = (size_t)p.R * (m / 4);
-        const int4 a4 = ash[Q];
-        const float g0 = (float)a4.x, g1 = (float)a4.y, g2 = (float)a4.z, g3 = (float)a4.w;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        float4 A[8], Bn[8];
+        for (int base = 0; base < items; base += kResKT) {   // the same trip count in every k-sum warp
+          const int it = base + kt;
+          const int Q = qs0 + (it >> 2);
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+          if (it < items) {
+            const int kb = (it & 3) * kc, ke = min(n, kb + kc);
+            const int lr = Q / W4, cq = Q - lr * W4;
+            const float4* src = reinterpret_cast<const float4*>(p.C + ((size_t)lr0 + lr) * m + col0) + cq;
+            const int4 a4 = ash[Q];
+            const float g0 = (float)a4.x, g1 = (float)a4.y, g2 = (float)a4.z, g3 = (float)a4.w;
+            float4 A[8], Bn[8];
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) A[kk] = kk < n ? __ldcg(src + kk * ks) : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int k0 = 0; k0 < n; k0 += 8) {
+            for (int kk = 0; kk < 8; ++kk)
+              A[kk] = kb + kk < ke ? __ldcg(src + (size_t)(kb + kk) * ks) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k0 = kb; k0 < ke; k0 += 8) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            Bn[kk] = k0 + 8 + kk < n ? __ldcg(src + (size_t)(k0 + 8 + kk) * ks) : make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int kk = 0; kk < 8; ++kk)
+                Bn[kk] = k0 + 8 + kk < ke ? __ldcg(src + (size_t)(k0 + 8 + kk) * ks) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            if (k0 + kk < n) {
-              s0 += ex2(fmaf(-A[kk].x, c2, g0));
-              s1 += ex2(fmaf(-A[kk].y, c2, g1));
-              s2 += ex2(fmaf(-A[kk].z, c2, g2));
-              s3 += ex2(fmaf(-A[kk].w, c2, g3));
+              for (int kk = 0; kk < 8; ++kk)
+                if (k0 + kk < ke) {
+                  s0 += ex2(fmaf(-A[kk].x, c2, g0));
+                  s1 += ex2(fmaf(-A[kk].y, c2, g1));
+                  s2 += ex2(fmaf(-A[kk].z, c2, g2));
+                  s3 += ex2(fmaf(-A[kk].w, c2, g3));
+                }
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) A[kk] = Bn[kk];
             }
+          }
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) A[kk] = Bn[kk];
+          for (int o = 1; o <= 2; o <<= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+          }
+          if (it < items && (it & 3) == 0) out[Q] = make_float4(s0, s1, s2, s3);
         }
-        out[Q] = make_float4(s0, s1, s2, s3);
       }
       // shared-memory quads: four k-rows per step, loads first
       for (int Q = kt + kResKT * nt; Q < nq; Q += kResKT) {

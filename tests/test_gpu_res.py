@@ -152,13 +152,15 @@ def test_res_fused_emulated_ranks_match_oracle(world):
         cdist.free_xbufs(xb)
 
 
-def test_res_c4_shard_of_8_matches_streaming_kernel():
-    """C4 at full size (n = 64, m = 1024): rank 0's shard of the 8-way partition (128 rows) on the resident kernel
-    with the exchange with itself (cerot_iter_fused, one rank) -- the per-GPU work of the 8-GPU run -- gives the
-    streaming kernel's iterate on the same shard (COT_RES=0; that kernel is pinned to the oracle by
+@pytest.mark.parametrize("ways", [8, 4], ids=["8_way_on_chip", "4_way_streamed_quads"])
+def test_res_c4_shard_matches_streaming_kernel(ways):
+    """C4 at full size (n = 64, m = 1024): rank 0's shard of the 8-way (128 rows, on chip) and of the 4-way partition
+    (256 rows: ~13% of the quads streamed from L2 every iteration, k-split over four lanes) on the resident kernel
+    with the exchange with itself (cerot_iter_fused, one rank) -- the per-GPU work of the 8- / 4-GPU runs -- gives
+    the streaming kernel's iterate on the same shard (COT_RES=0; that kernel is pinned to the oracle by
     tests/test_gpu_fused.py) to fp32 k-sum rounding."""
     p = synthetic.c4_large()
-    b0, R = cdist.row_partition(p.m, 8, 0)
+    b0, R = cdist.row_partition(p.m, ways, 0)
     assert cot.lib().cot_fused_path(p.n, p.m, R, 1, 0, 0) == 4
     sh = cdist.ShardedCerot(_dev(p.C[:, b0:b0 + R, :]), _dev(p.alpha), _dev(p.beta), float(p.eps[0]), b0, p.m)
     x = cdist.PeerExchange(p.m)
