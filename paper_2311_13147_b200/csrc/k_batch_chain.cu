@@ -185,7 +185,27 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
   const uint32_t peer = (uint32_t)((crank + 1 + gsend) % NCH);
   const uint32_t xh_peer = NCH > 1 ? mapa_u32(smem_u32(xh), peer) : 0u;
   const uint32_t xbar_peer = NCH > 1 ? mapa_u32(smem_u32(&bars[5]), peer) : 0u;
+  // a_ij of the thread's rows also in tensor memory (128 columns: four warps per 32-lane quarter, 32 columns each,
+  // words 4k + v = a of row warp + 16k, column 4 jc + v): the r-pass reads them with LDTM (~12 cycles, a separate
+  // datapath) instead of LDS.128 on this SM's busy shared-memory port
+  unsigned* tslot = reinterpret_cast<unsigned*>(smem + 96);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const unsigned ta = *tslot + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * 32);
+#pragma unroll
+  for (int k = 0; k < RPW; ++k) {
+    const int i = warp + k * kChainWarps;
+    const int ic = FULL || i < m ? i : 0;
+    const int4 a4 = reinterpret_cast<const int4*>(As + (size_t)ic * m)[jc];
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ta + 4u * k), "r"(a4.x),
+                 "r"(a4.y), "r"(a4.z), "r"(a4.w));
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   SolverState st = st0;
   bool underflow = false;
   int t = 0;
@@ -231,7 +251,12 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
       const bool ok = FULL || (i < m && lane < mv);
       const int ic = FULL || i < m ? i : 0;
       const float4 s4 = reinterpret_cast<const float4*>(sq + (size_t)ic * m)[jc];
-      const int4 a4 = reinterpret_cast<const int4*>(As + (size_t)ic * m)[jc];
+      int4 a4;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(a4.x), "=r"(a4.y), "=r"(a4.z), "=r"(a4.w)
+                   : "r"(ta + 4u * k));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      (void)ic;
       const int ex[4] = {k4.x - a4.x, k4.y - a4.y, k4.z - a4.z, k4.w - a4.w};   // kz_j + 896 - a_ij
       const int em = max(max(ex[0], ex[1]), max(ex[2], ex[3]));
       // exact row shift kM_i = max_j (kz_j - a_ij): the largest term is >= 1/2
@@ -399,6 +424,9 @@ __device__ __forceinline__ void chain_role(const ChainParams& p, const int64_t b
     out.converged = st.converged;
     p.state[b] = out;
   }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(*tslot));
 }
 
 __global__ void __launch_bounds__(kChainThreads, 1) k_batch_chain(const __grid_constant__ ChainParams p) {
