@@ -247,6 +247,9 @@ int cerot_rows_shard(const double* alpha, const void* C_local, const void* G_loc
 int cerot_zupdate(const double* beta, const double* c, int64_t n, int64_t m, double tol, int64_t check_every,
                   double* z_hat, void* workspace, size_t ws_bytes, void* stream);
 /* `iters` iterations: cerot_rows_shard -> ncclAllReduce(c) (if comm) -> cerot_zupdate, all on `stream`.  */
+/* Groups of 8 iterations are captured once as a CUDA graph (on a private stream) and replayed on      */
+/* `stream`; bitwise the same as per-iteration launches (COT_SHARDED_NO_GRAPH=1 forces those). The       */
+/* caller's comm must not be used by another thread while this call enqueues.                           */
 int cerot_iter_sharded(const double* alpha, const double* beta, const void* C_local, const void* G_local,
                        int64_t n, int64_t m, int64_t row_begin, int64_t R, int dtype, const double* eps,
                        int64_t iters, double tol, int64_t check_every, uint32_t flags, double* w_hat,

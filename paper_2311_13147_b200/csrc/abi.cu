@@ -918,15 +918,50 @@ int cerot_iter_sharded(const double* alpha, const double* beta, const void* C_lo
                                z_hat, row_begin, R);
   const UnitPlan up = unit_plan(1, R, device_sm_count());
   cudaStream_t s = (cudaStream_t)stream;
-  for (int64_t t = 0; t < iters; ++t) {
-    COT_CHECK_CUDA(rows_pass(a, ws, (int)(t & 1), s));
-    COT_CHECK_CUDA(launch_colsum(ws, up, 1, m, (int)(t & 1), ws.c_local, s));
+  // one iteration t: row pass, rank-local column sums, the exchange, q-update
+  auto enqueue = [&](int64_t t, cudaStream_t q) -> int {
+    COT_CHECK_CUDA(rows_pass(a, ws, (int)(t & 1), q));
+    COT_CHECK_CUDA(launch_colsum(ws, up, 1, m, (int)(t & 1), ws.c_local, q));
     const double* c = ws.c_local;
     if (comm) {   // the exchange step: one m-length fp64 allreduce over NVLink / NVSwitch per iteration
-      COT_CHECK_NCCL(nccl_api().AllReduce(ws.c_local, ws.c_global, (size_t)m, ncclFloat64, ncclSum, (ncclComm_t)comm, s));
+      COT_CHECK_NCCL(nccl_api().AllReduce(ws.c_local, ws.c_global, (size_t)m, ncclFloat64, ncclSum, (ncclComm_t)comm, q));
       c = ws.c_global;
     }
-    COT_CHECK_CUDA(launch_zupdate(c, beta, 1, m, n, tol, check_every, z_hat, ws, s));
+    COT_CHECK_CUDA(launch_zupdate(c, beta, 1, m, n, tol, check_every, z_hat, ws, q));
+    return COT_OK;
+  };
+  // The iteration has no host-side dependence (the freeze rule is applied on the device), so kUnroll iterations
+  // (an even count: the row pass alternates its two buffers) are captured ONCE as a CUDA graph, allreduce
+  // included, and replayed: one graph launch per kUnroll iterations instead of 3 kernel launches + 1 NCCL call
+  // each. Capture is on a private stream (the caller's may be the legacy stream); if it fails (e.g. an NCCL
+  // build without capture support) the plain per-iteration enqueue below runs everything.
+  constexpr int64_t kUnroll = 8;
+  int64_t t0 = 0;
+  if (iters >= 2 * kUnroll && !getenv("COT_SHARDED_NO_GRAPH")) {
+    cudaStream_t cs = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess;
+    if (ok) ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      bool body_ok = true;
+      for (int64_t t = 0; t < kUnroll && body_ok; ++t) body_ok = enqueue(t, cs) == COT_OK;
+      ok = cudaStreamEndCapture(cs, &g) == cudaSuccess && body_ok;
+    }
+    if (ok) ok = cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+    if (ok) {
+      for (; t0 + kUnroll <= iters; t0 += kUnroll) COT_CHECK_CUDA(cudaGraphLaunch(ge, s));
+    } else {
+      cudaGetLastError();   // a failed capture leaves nothing enqueued; fall back to the plain loop
+      t0 = 0;
+    }
+    if (ge) cudaGraphExecDestroy(ge);   // freed once the in-flight launches complete
+    if (g) cudaGraphDestroy(g);
+    if (cs) cudaStreamDestroy(cs);
+  }
+  for (int64_t t = t0; t < iters; ++t) {
+    st = enqueue(t, s);
+    if (st) return st;
   }
   return COT_OK;
 }

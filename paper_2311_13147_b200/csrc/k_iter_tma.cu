@@ -1539,11 +1539,13 @@ cudaError_t launch_iter_tma(const IterArgs& a, const Workspace& ws, int iters, b
   // A stream larger than L2: the first rows of every block (~56 MB of it) are streamed with an L2 evict_last hint
   // and stay resident across iterations, the rest evict_first (C4: rows [0, 244) of the 56 streamed k-blocks;
   // 33.8 -> 32.0 us per iteration; 192-288 rows measured flat, 320 and more thrash). COT_EVICT_LAST_ROWS overrides.
-  if (!rows_only && iters > 1 && !getenv("COT_EVICT_LAST_ROWS")) {
+  // Rows-only launches (cerot_iter_sharded's row pass, replayed once per iteration) use the same split: L2
+  // keeps its contents across launches, so the evict_last rows are re-read from L2 by the next launch.
+  if ((rows_only || iters > 1) && !getenv("COT_EVICT_LAST_ROWS")) {
     const double row_bytes = (double)(a.n - p.kres - p.ktm) * (double)a.m * 4.0;   // one row's streamed k-blocks
     if (row_bytes > 0.0 && row_bytes * (double)a.R > 96e6)
-      p.evict_last_rows = (int)std::min<double>((double)a.R, 56e6 / row_bytes);
-  }
+      p.evict_last_rows = (int)std::min<double>((double)a.R, (rows_only ? 40e6 : 56e6) / row_bytes);
+  }   // rows-only C4 (whole rows streamed): 0 / 150 / 213 / 300 rows measured 52.5 / 50.8 / 52.5 / 52.4 us/iter
   p.trace = trace_begin(s);
   e = check_occupancy(cfg.fn, cfg.threads, cfg.smem, cfg.grid, sms);
   if (e != cudaSuccess) return e;

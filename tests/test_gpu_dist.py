@@ -129,6 +129,42 @@ def test_nccl_single_rank_communicator():
         L.cot_comm_destroy(comm)
 
 
+@pytest.mark.parametrize("with_comm", [True, False], ids=["nccl1", "no_comm"])
+def test_sharded_graph_replay_is_bitwise(with_comm, monkeypatch):
+    """cerot_iter_sharded captures 8 iterations (row pass, column sums, allreduce, q-update) once as a CUDA
+    graph and replays it; the tail runs as plain launches. Replay is the same work in the same order, so 37
+    iterations (4 graph replays + 5 plain) and the freeze rule (tol > 0) are bit-identical to the per-iteration
+    enqueue (COT_SHARDED_NO_GRAPH=1)."""
+    L = cot.lib()
+    comm = ctypes.c_void_p()
+    if with_comm:
+        uid = ctypes.create_string_buffer(128)
+        assert L.cot_nccl_unique_id(uid) == 0, L.cot_last_error()
+        assert L.cot_comm_init(uid, 1, 0, ctypes.byref(comm)) == 0, L.cot_last_error()
+
+    class _C:
+        handle = comm
+    try:
+        p = synthetic.c4_large(m=256, n=16)
+        runs = []
+        for no_graph in (False, True):
+            if no_graph:
+                monkeypatch.setenv("COT_SHARDED_NO_GRAPH", "1")
+            else:
+                monkeypatch.delenv("COT_SHARDED_NO_GRAPH", raising=False)
+            a = cdist.ShardedCerot(_dev(p.C), _dev(p.alpha), _dev(p.beta), float(p.eps[0]), 0, p.m,
+                                   comm=_C() if with_comm else None).init()
+            a.iterate(37, tol=1e-6, check_every=4)
+            torch.cuda.synchronize()
+            runs.append((a.z_hat.cpu().numpy(), a.w_hat.cpu().numpy(), a.state()))
+        (z0, w0, s0), (z1, w1, s1) = runs
+        assert np.array_equal(z0, z1) and np.array_equal(w0, w1)
+        assert s0 == s1
+    finally:
+        if with_comm:
+            L.cot_comm_destroy(comm)
+
+
 def test_batched_problem_sharding_is_exact():
     """C5 problem sharding: when every rank holds at least one problem per SM (the C5 regime: 4096 problems),
     a unit of rows is a whole problem, so solving a contiguous slice of the batch is bit-identical to the same
