@@ -1598,6 +1598,16 @@ cudaError_t launch_iter_tma_fused(const FusedRank* r, int nv, int nranks, bool e
     p.xepoch = r[v].xepoch;
     // a shard whose cost rows fit comfortably in L2 is kept there across iterations
     if (!emulate && (double)(r[v].a.n + 1) * r[v].a.R * r[v].a.m * 4.0 <= 80e6) p.evict_last_rows = (int)r[v].a.R;
+    // emulated ranks share one GPU's L2: the unsharded launch's ~56 MB evict_last budget split over them (C4, 8
+    // virtual ranks: 16 / 27 / 40 rows each measured 39.9 / 39.9 / 44.2 us per iteration against 41.3 with none)
+    // (1/2/4 virtual ranks then match the unsharded launch: 31.8 / 31.9 / 32.3 vs 32.0; 8: 40.0). A real rank
+    // whose shard does not fit L2 takes the unsharded launch's rule (the first ~56 MB of rows evict_last).
+    if (!getenv("COT_EVICT_LAST_ROWS") && p.evict_last_rows < (int)r[v].a.R) {
+      const double row_bytes = (double)(r[v].a.n - p.kres - p.ktm) * (double)r[v].a.m * 4.0;
+      const double budget = emulate ? 40e6 / nranks : 56e6;
+      if (row_bytes > 0.0 && row_bytes * (double)r[v].a.R * (emulate ? nranks : 1) > 96e6)
+        p.evict_last_rows = (int)std::min<double>((double)r[v].a.R, budget / row_bytes);
+    }
   }
   for (int v = 0; v < nv; ++v) pm.rp[v].ncs = ncs;
   const int grid = pm.base[nv];
