@@ -342,6 +342,21 @@ int cerot_two_stage(const double* a, const double* b, const void* C, int64_t n, 
                     const double* eps, int64_t iters1, double tol1, int64_t iters2, double tol2,
                     int64_t check_every, double* f_hat, double* g_hat, double* w_hat, double* z_hat,
                     void* workspace, size_t ws_bytes, cot_report* report, int64_t* iters_done, void* stream);
+/* The same algorithm with App. F's stage-2 stopping rule: stage 2 runs until the difference     */
+/* between its objective function value and `obj_ref` -- the value obtained by directly solving the       */
+/* problem with the original Sinkhorn algorithm, supplied by the caller (HOST double) -- is below         */
+/* `tol_obj` (> 0; the paper uses 1e-4), checked every check_every iterations on the plan                 */
+/* T = diag(p) K diag(q) after the iteration's q-update, or for iters2 iterations. The objective is the   */
+/* regularised primal <C,T> + eps sum T (log T - 1) (report->reg_primal, FULL-problem value; DESIGN       */
+/* reading Q19). Each check costs the two report passes of one extra iteration and one host sync.         */
+/* report->residual receives the last measured |objective - obj_ref| (0 if never checked). Returns        */
+/* COT_NOT_CONVERGED if the gap was not reached, COT_E_ARG if tol_obj <= 0 or obj_ref is not finite.      */
+/* Other arguments, workspace and outputs as cerot_two_stage.                                             */
+int cerot_two_stage_gap(const double* a, const double* b, const void* C, int64_t n, int64_t m, int dtype,
+                        const double* eps, int64_t iters1, double tol1, int64_t iters2, double obj_ref,
+                        double tol_obj, int64_t check_every, double* f_hat, double* g_hat, double* w_hat,
+                        double* z_hat, void* workspace, size_t ws_bytes, cot_report* report, int64_t* iters_done,
+                        void* stream);
 
 /* ---------------------------------------------------------------------------------------------- */
 /* NEXT-4: the small LOT of Theorem 1 (eq. small_problem_CLOT; Alg. 1 line 2), the paper's     */

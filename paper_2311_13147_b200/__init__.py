@@ -84,6 +84,9 @@ _SIGS = {
     "cerot_two_stage": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl, _i64, _dbl, _i64,
                                        _vp, _vp, _vp, _vp, _vp, _sz, ctypes.POINTER(cot_report),
                                        ctypes.POINTER(_i64), _vp]),
+    "cerot_two_stage_gap": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _dbl, _i64, _dbl,
+                                           _dbl, _i64, _vp, _vp, _vp, _vp, _vp, _sz, ctypes.POINTER(cot_report),
+                                           ctypes.POINTER(_i64), _vp]),
     # NEXT-4: host network simplex for the small LOT (host pointers)
     "clot_small_lot": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp, ctypes.POINTER(_dbl), _vp, _vp,
                                       ctypes.POINTER(_i64)]),
@@ -358,10 +361,12 @@ def csrot_solve(C, alpha, beta, gamma, tol=0.0, max_sweeps=1000, check_every=1, 
     return w, z, T, out
 
 
-def two_stage_sinkhorn(a, b, C, eps, iters1, iters2, tol1=0.0, tol2=0.0, check_every=1, stream=None):
+def two_stage_sinkhorn(a, b, C, eps, iters1, iters2, tol1=0.0, tol2=0.0, check_every=1, stream=None,
+                       obj_ref=None, tol_obj=0.0):
     """NEXT-2: Algorithm 3 on the device (cerot_two_stage). a, b: device [d] fp64 (approximately
     n-periodic), C: device [n][m][m]. Returns (f_hat, g_hat [d], w_hat, z_hat [m], report dict) with
-    eps-scaled potentials; report values are full-problem (no factor n)."""
+    eps-scaled potentials; report values are full-problem (no factor n). With obj_ref and tol_obj > 0 stage 2
+    stops on App. F's objective gap instead of tol2 (cerot_two_stage_gap)."""
     import torch
     n, m = C.shape[0], C.shape[1]
     dt = _dtype_code(C)
@@ -376,9 +381,14 @@ def two_stage_sinkhorn(a, b, C, eps, iters1, iters2, tol1=0.0, tol2=0.0, check_e
     ws = torch.empty(int(lib().cot_two_stage_workspace_bytes(n, m, dt)), dtype=torch.uint8, device=dev)
     rep = cot_report()
     its = (ctypes.c_int64 * 2)()
-    code = lib().cerot_two_stage(_ptr(a), _ptr(b), _ptr(C), n, m, dt, _ptr(eps_t), iters1, tol1, iters2, tol2,
-                                 check_every, _ptr(f), _ptr(g), _ptr(w), _ptr(z), _ptr(ws), ws.numel(),
-                                 ctypes.byref(rep), its, _stream(stream))
+    if obj_ref is not None:
+        code = lib().cerot_two_stage_gap(_ptr(a), _ptr(b), _ptr(C), n, m, dt, _ptr(eps_t), iters1, tol1, iters2,
+                                         float(obj_ref), float(tol_obj), check_every, _ptr(f), _ptr(g), _ptr(w),
+                                         _ptr(z), _ptr(ws), ws.numel(), ctypes.byref(rep), its, _stream(stream))
+    else:
+        code = lib().cerot_two_stage(_ptr(a), _ptr(b), _ptr(C), n, m, dt, _ptr(eps_t), iters1, tol1, iters2, tol2,
+                                     check_every, _ptr(f), _ptr(g), _ptr(w), _ptr(z), _ptr(ws), ws.numel(),
+                                     ctypes.byref(rep), its, _stream(stream))
     _check(code, "cerot_two_stage", ok=(0, 1))
     d = {k: getattr(rep, k) for k in REPORT_FIELDS}
     d.update(iters1=int(its[0]), iters2=int(its[1]), converged=bool(rep.converged), status=STATUS[rep.status])

@@ -591,10 +591,13 @@ size_t cot_two_stage_workspace_bytes(int64_t n, int64_t m, int dtype) {
   return two_stage_layout(n, m, dtype, nullptr, &o, &al, &be, &bt, &dv, &mo, &rr, &rc, &rp);
 }
 
-int cerot_two_stage(const double* a, const double* b, const void* C, int64_t n, int64_t m, int dtype, const double* eps,
-                    int64_t iters1, double tol1, int64_t iters2, double tol2, int64_t check_every, double* f_hat,
-                    double* g_hat, double* w_hat, double* z_hat, void* workspace, size_t ws_bytes,
-                    cot_report* report, int64_t* iters_done, void* stream) {
+// Both stage-2 stopping rules: the marginal monitor (tol2) and App. F's objective gap (tol_obj > 0: |regularised
+// primal of the current plan - obj_ref| < tol_obj), each checked every check_every iterations.
+static int two_stage_impl(const double* a, const double* b, const void* C, int64_t n, int64_t m, int dtype,
+                          const double* eps, int64_t iters1, double tol1, int64_t iters2, double tol2, double obj_ref,
+                          double tol_obj, int64_t check_every, double* f_hat, double* g_hat, double* w_hat,
+                          double* z_hat, void* workspace, size_t ws_bytes, cot_report* report, int64_t* iters_done,
+                          void* stream) {
   int st = check_shape(1, n, m, dtype);
   if (st) return st;
   if (!a || !b || !C || !eps || !f_hat || !g_hat || !w_hat || !z_hat)
@@ -637,7 +640,8 @@ int cerot_two_stage(const double* a, const double* b, const void* C, int64_t n, 
   COT_CHECK_CUDA(launch_transpose_blocks(C, n, m, dtype, Bt, s));
   int64_t it2 = 0;
   double residual = 0.0;
-  bool have_res = false;
+  bool have_res = false, gap_ok = false;
+  double gap = 0.0;
   for (int64_t t = 0; t < iters2; ++t) {
     COT_CHECK_CUDA(launch_full_pass(C, n, m, dtype, eps, a, g_hat, f_hat, nullptr, nullptr, 0, s));   // p-update
     COT_CHECK_CUDA(launch_full_pass(Bt, n, m, dtype, eps, b, f_hat, g_hat, dev, nullptr, 1, s));     // q-update
@@ -650,6 +654,19 @@ int cerot_two_stage(const double* a, const double* b, const void* C, int64_t n, 
       have_res = true;
       if (tol2 > 0.0 && it2 % check_every == 0 && residual <= tol2) break;
     }
+    if (tol_obj > 0.0 && it2 % check_every == 0) {   // App. F: the objective of the plan after this iteration
+      COT_CHECK_CUDA(launch_full_pass(C, n, m, dtype, eps, a, g_hat, f_hat, nullptr, rep_rows, 2, s));
+      COT_CHECK_CUDA(launch_full_pass(Bt, n, m, dtype, eps, b, f_hat, g_hat, nullptr, rep_cols, 2, s));
+      COT_CHECK_CUDA(launch_full_finalize(rep_rows, rep_cols, a, b, f_hat, g_hat, d, eps, 0.0, rep, s));
+      double hv[kReportDoubles];
+      COT_CHECK_CUDA(cudaMemcpyAsync(hv, rep, sizeof(hv), cudaMemcpyDeviceToHost, s));
+      COT_CHECK_CUDA(cudaStreamSynchronize(s));
+      gap = std::fabs(hv[1] - obj_ref);
+      if (gap < tol_obj) {
+        gap_ok = true;
+        break;
+      }
+    }
   }
   // ---- report of the returned plan T = diag(p) K diag(q) (line 17)
   COT_CHECK_CUDA(launch_full_pass(C, n, m, dtype, eps, a, g_hat, f_hat, nullptr, rep_rows, 2, s));
@@ -659,6 +676,8 @@ int cerot_two_stage(const double* a, const double* b, const void* C, int64_t n, 
   double h[kReportDoubles];
   COT_CHECK_CUDA(cudaMemcpyAsync(h, rep, sizeof(h), cudaMemcpyDeviceToHost, s));
   COT_CHECK_CUDA(cudaStreamSynchronize(s));
+  const bool wanted = tol2 > 0.0 || tol_obj > 0.0;
+  const bool conv = (tol2 > 0.0 && have_res && residual <= tol2) || gap_ok;
   if (report) {
     report->objective = h[0];
     report->reg_primal = h[1];
@@ -667,16 +686,34 @@ int cerot_two_stage(const double* a, const double* b, const void* C, int64_t n, 
     report->col_l1 = h[4];
     report->col_l2 = h[5];
     report->mass = h[6];
-    report->residual = h[7];
+    report->residual = tol_obj > 0.0 ? gap : h[7];
     report->iters = it2;
-    report->converged = tol2 > 0.0 && have_res && residual <= tol2;
-    report->status = (tol2 > 0.0 && !report->converged) ? COT_NOT_CONVERGED : COT_OK;
+    report->converged = conv;
+    report->status = (wanted && !conv) ? COT_NOT_CONVERGED : COT_OK;
   }
   if (iters_done) {
     iters_done[0] = it1;
     iters_done[1] = it2;
   }
-  return (tol2 > 0.0 && !(have_res && residual <= tol2)) ? COT_NOT_CONVERGED : COT_OK;
+  return (wanted && !conv) ? COT_NOT_CONVERGED : COT_OK;
+}
+
+int cerot_two_stage(const double* a, const double* b, const void* C, int64_t n, int64_t m, int dtype, const double* eps,
+                    int64_t iters1, double tol1, int64_t iters2, double tol2, int64_t check_every, double* f_hat,
+                    double* g_hat, double* w_hat, double* z_hat, void* workspace, size_t ws_bytes,
+                    cot_report* report, int64_t* iters_done, void* stream) {
+  return two_stage_impl(a, b, C, n, m, dtype, eps, iters1, tol1, iters2, tol2, 0.0, 0.0, check_every, f_hat, g_hat,
+                        w_hat, z_hat, workspace, ws_bytes, report, iters_done, stream);
+}
+
+int cerot_two_stage_gap(const double* a, const double* b, const void* C, int64_t n, int64_t m, int dtype,
+                        const double* eps, int64_t iters1, double tol1, int64_t iters2, double obj_ref, double tol_obj,
+                        int64_t check_every, double* f_hat, double* g_hat, double* w_hat, double* z_hat,
+                        void* workspace, size_t ws_bytes, cot_report* report, int64_t* iters_done, void* stream) {
+  if (!(tol_obj > 0.0) || !std::isfinite(obj_ref))
+    return arg_error("cerot_two_stage_gap: tol_obj > 0 and a finite obj_ref required");
+  return two_stage_impl(a, b, C, n, m, dtype, eps, iters1, tol1, iters2, 0.0, obj_ref, tol_obj, check_every, f_hat,
+                        g_hat, w_hat, z_hat, workspace, ws_bytes, report, iters_done, stream);
 }
 
 // ------------------------------------------------------------------------------------- NEXT-3: C-SROT

@@ -85,3 +85,51 @@ def test_two_stage_converges_with_the_oracle():
     assert rep["converged"] and t2 < 2000
     assert abs(rep["iters2"] - t2) <= 1
     assert rep["residual"] <= 1e-9
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
+@pytest.mark.parametrize("check_every", [1, 2])
+def test_two_stage_gap_rule_matches_oracle(dtype, check_every):
+    """App. F's stage-2 stopping rule through cerot_two_stage_gap against oracle.two_stage_sinkhorn_gap:
+    the reference value is the oracle's directly solved objective; both stop at the same stage-2 iteration
+    (tol_obj sits a factor >= 1.5 away from the gaps of the neighbouring checks, asserted on the oracle side, so
+    fp32 cost rounding cannot move the decision) and return the same plan."""
+    p = synthetic.c3_image(H=8)
+    a, b = synthetic.approx_symmetric(p, noise=0.9)
+    C = p.C.astype(dtype)
+    C64 = C.astype(np.float64)
+    eps = float(p.eps[0]) * 5
+    Cf = oracle.expand_cost(C64)
+    f0, g0, _, _ = oracle.sinkhorn_full(a, b, Cf, eps, 20000, tol=1e-13)
+    ref = oracle.entropic_objective_full(oracle.plan_full(f0, g0, Cf, eps), Cf, eps)
+    tol_obj = 5e-5
+    fo, go, t1, t2, gap_o = oracle.two_stage_sinkhorn_gap(a, b, C64, eps, 2, 400, ref, tol_obj, check_every=check_every)
+    assert 1 < t2 < 400 and gap_o < tol_obj / 1.5
+    _, _, _, tprev, gap_prev = oracle.two_stage_sinkhorn_gap(a, b, C64, eps, 2, t2 - check_every, ref, 0.0,
+                                                             check_every=check_every)
+    assert tprev == t2 - check_every and gap_prev > tol_obj * 1.5
+    f, g, w, z, rep = cot.two_stage_sinkhorn(_dev(a), _dev(b), _dev(C), eps, 2, 400, check_every=check_every,
+                                             obj_ref=ref, tol_obj=tol_obj)
+    assert rep["converged"] and rep["status"] == "COT_OK"
+    assert (rep["iters1"], rep["iters2"]) == (t1, t2)
+    bar = 1e-5 if dtype == np.float32 else 1e-10           # DESIGN §4 bars
+    assert abs(rep["residual"] - gap_o) <= bar            # the measured |objective - obj_ref|
+    assert abs(rep["reg_primal"] - (oracle.entropic_objective_full(oracle.plan_full(fo, go, Cf, eps), Cf, eps))) <= bar
+    Tg = oracle.plan_full(f.cpu().numpy() * eps, g.cpu().numpy() * eps, Cf, eps)
+    assert np.abs(Tg - oracle.plan_full(fo, go, Cf, eps)).sum() < bar
+
+
+def test_two_stage_gap_rule_not_reached_and_argument_errors():
+    p = synthetic.c3_image(H=8)
+    a, b = synthetic.approx_symmetric(p, noise=0.5)
+    eps = float(p.eps[0]) * 5
+    C = p.C.astype(np.float64)
+    f, g, w, z, rep = cot.two_stage_sinkhorn(_dev(a), _dev(b), _dev(C), eps, 5, 7, obj_ref=1e3, tol_obj=1e-4)
+    assert not rep["converged"] and rep["status"] == "COT_NOT_CONVERGED" and rep["iters2"] == 7
+    # the iterates are those of the plain two-stage run (the rule only decides when to stop)
+    f2, g2, _, _, _ = cot.two_stage_sinkhorn(_dev(a), _dev(b), _dev(C), eps, 5, 7)
+    assert torch.equal(f, f2) and torch.equal(g, g2)
+    with pytest.raises(Exception):
+        cot.two_stage_sinkhorn(_dev(a), _dev(b), _dev(C), eps, 5, 7, obj_ref=0.0, tol_obj=0.0)
+    with pytest.raises(Exception):
+        cot.two_stage_sinkhorn(_dev(a), _dev(b), _dev(C), eps, 5, 7, obj_ref=float("nan"), tol_obj=1e-4)

@@ -65,3 +65,52 @@ def test_stage2_warm_start_is_alg3_line11():
     f_bf = np.array([eps * (np.log(a[I]) - np.log(sum(np.exp((zt[J] - C[I, J]) / eps) for J in range(15))))
                      for I in range(15)])
     assert np.abs(f - f_bf).max() < 1e-12
+
+
+def test_entropic_objective_closed_form_and_duality():
+    """Pins of entropic_objective_full (eq. problem_CROT + eq. reg_for_entropy_ROT): (i) closed form for the
+    independent coupling with zero cost, eps (sum a log a + sum b log b - 1); (ii) strong duality at the
+    Sinkhorn optimum (eq. dual_problem_cyclic_ROT with n = 1): primal = <f,a> + <g,b> - eps sum T, a value
+    computed without the entropy term, so a wrong sign or a dropped '-1' fails."""
+    rng = np.random.default_rng(3)
+    a = rng.random(6); a /= a.sum()
+    b = rng.random(7); b /= b.sum()
+    T = np.outer(a, b)
+    want = 0.3 * ((a * np.log(a)).sum() + (b * np.log(b)).sum() - 1.0)
+    assert abs(oracle.entropic_objective_full(T, np.zeros((6, 7)), 0.3) - want) < 1e-14
+    C = rng.random((6, 7))
+    f, g, _, _ = oracle.sinkhorn_full(a, b, C, 0.2, 5000, tol=1e-14)
+    Topt = oracle.plan_full(f, g, C, 0.2)
+    dual = f @ a + g @ b - 0.2 * Topt.sum()
+    assert abs(oracle.entropic_objective_full(Topt, C, 0.2) - dual) < 1e-11
+    # suboptimal feasible plan: primal above the optimum (the objective is minimised, P:17)
+    assert oracle.entropic_objective_full(T, C, 0.2) > dual + 1e-6
+
+
+def test_gap_rule_stops_at_the_first_iteration_within_tol():
+    """App. F: stage 2 stops at the first checked iteration whose objective is within tol_obj of the
+    directly solved value. Checked against the recorded iterates of the plain original Sinkhorn from the same
+    start (sinkhorn_full(record=True)): the stop index is the first one below tol, the one before is not, and
+    the returned potentials are that iterate; a tol never reached runs all iters2; a huge tol stops at once."""
+    p = synthetic.c3_image(H=8)
+    a, b = synthetic.approx_symmetric(p, noise=0.5)
+    eps = float(p.eps[0]) * 5
+    C = oracle.expand_cost(p.C)
+    f0, g0, _, _ = oracle.sinkhorn_full(a, b, C, eps, 20000, tol=1e-13)          # "directly solving"
+    ref = oracle.entropic_objective_full(oracle.plan_full(f0, g0, C, eps), C, eps)
+    f, g, t1, t2, gap = oracle.two_stage_sinkhorn_gap(a, b, p.C, eps, 5, 400, ref, 1e-8)
+    assert t1 == 5 and 1 < t2 < 400 and gap < 1e-8
+    w, z, _, _ = oracle.cyclic_sinkhorn(oracle.fold_average(a, p.n), oracle.fold_average(b, p.n), p.C, eps, 5,
+                                        form="kernel")
+    _, _, _, hist = oracle.sinkhorn_full(a, b, C, eps, t2, record=True, g0=oracle.expand_vector(z, p.n))
+    gaps = [abs(oracle.entropic_objective_full(oracle.plan_full(fh, gh, C, eps), C, eps) - ref)
+            for fh, gh, _ in hist]
+    assert all(x >= 1e-8 for x in gaps[:-1]) and gaps[-1] < 1e-8
+    assert np.array_equal(f, hist[-1][0]) and np.array_equal(g, hist[-1][1])
+    # check_every = 3: stops at the first multiple of 3 at or after t2
+    _, _, _, t3, _ = oracle.two_stage_sinkhorn_gap(a, b, p.C, eps, 5, 400, ref, 1e-8, check_every=3)
+    assert t3 % 3 == 0 and t2 <= t3 < t2 + 3
+    _, _, _, tn, _ = oracle.two_stage_sinkhorn_gap(a, b, p.C, eps, 5, 20, ref, 1e-300)
+    assert tn == 20
+    _, _, _, th, _ = oracle.two_stage_sinkhorn_gap(a, b, p.C, eps, 5, 20, ref, 1e300)
+    assert th == 1
