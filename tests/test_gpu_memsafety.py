@@ -180,6 +180,25 @@ def run_two_stage(A):
     return [f, g, w, z]
 
 
+def run_two_stage_gap(A):
+    """App. F's stage-2 rule (cerot_two_stage_gap): the report passes run inside the loop, every 2nd iteration;
+    the reference value is never reached (obj_ref = 1e3), so all 6 iterations and 3 checks run."""
+    L = cot.lib()
+    p = synthetic.random_cyclic(seed=6, n=4, m=32, dtype=np.float32, eps=0.1)
+    a, b = synthetic.approx_symmetric(p)
+    n, m = p.n, p.m
+    ad, bd, Cd, ed = A.inp(a), A.inp(b), A.inp(p.C), A.inp(np.array([0.1]))
+    f, g = A.out((n * m,), torch.float64), A.out((n * m,), torch.float64)
+    w, z = A.out((m,), torch.float64), A.out((m,), torch.float64)
+    ws = A.workspace(L.cot_two_stage_workspace_bytes(n, m, F32))
+    rep = cot.cot_report()
+    its = (ctypes.c_int64 * 2)()
+    code = L.cerot_two_stage_gap(P(ad), P(bd), P(Cd), n, m, F32, P(ed), 5, 0.0, 6, 1e3, 1e-4, 2, P(f), P(g), P(w),
+                                 P(z), P(ws), ws.numel(), ctypes.byref(rep), its, S())
+    assert code == 1 and its[1] == 6, (code, its[1])        # COT_NOT_CONVERGED
+    return [f, g, w, z]
+
+
 def run_srot(A):
     L = cot.lib()
     p = synthetic.random_cyclic(seed=7, n=4, m=32, dtype=np.float32, eps=0.1)
@@ -236,6 +255,7 @@ CASES = {
     "fused_emulated_2": lambda A: run_fused(A, 2),
     "fused_emulated_2_tma": lambda A: _env({"COT_RES": "0"}, lambda: run_fused(A, 2)),
     "two_stage": run_two_stage,
+    "two_stage_gap": run_two_stage_gap,
     "srot": run_srot,
 }
 
