@@ -76,15 +76,27 @@ def test_two_stage_exact_symmetry_continues_the_cyclic_iteration():
 
 
 def test_two_stage_converges_with_the_oracle():
+    """Stage 2 to the marginal tolerance: tol2 is placed at the geometric mean of the oracle's residuals of two
+    consecutive iterations (a factor >= 1.02 from each, asserted), so both sides must stop at exactly the same
+    iteration, and the plans are compared there (no +-1 allowance)."""
     p = synthetic.c3_image(H=16)
     a, b = synthetic.approx_symmetric(p, noise=0.1)
     C = p.C.astype(np.float64)
     eps = 0.05
-    f, g, w, z, rep = cot.two_stage_sinkhorn(_dev(a), _dev(b), _dev(C), eps, 30, 2000, tol2=1e-9)
-    fo, go, t1, t2 = oracle.two_stage_sinkhorn(a, b, C, eps, 30, 2000, tol2=1e-9)
-    assert rep["converged"] and t2 < 2000
-    assert abs(rep["iters2"] - t2) <= 1
-    assert rep["residual"] <= 1e-9
+    Cf = oracle.expand_cost(C)
+    _, zo, _, _ = oracle.cyclic_sinkhorn(oracle.fold_average(a, p.n), oracle.fold_average(b, p.n), C, eps, 30,
+                                         form="kernel")
+    _, _, _, hist = oracle.sinkhorn_full(a, b, Cf, eps, 40, record=True, g0=oracle.expand_vector(zo, p.n))
+    res = [h[2] for h in hist]
+    k = next(i for i in range(20, 39) if res[i] > 1.04 * res[i + 1] and all(r > res[i] for r in res[:i]))
+    tol2 = float(np.sqrt(res[k] * res[k + 1]))
+    fo, go, t1, t2 = oracle.two_stage_sinkhorn(a, b, C, eps, 30, 2000, tol2=tol2)
+    assert t2 == k + 2
+    f, g, w, z, rep = cot.two_stage_sinkhorn(_dev(a), _dev(b), _dev(C), eps, 30, 2000, tol2=tol2)
+    assert rep["converged"] and (rep["iters1"], rep["iters2"]) == (t1, t2)
+    assert rep["residual"] <= tol2 and abs(rep["residual"] - res[k + 1]) <= 1e-10
+    Tg = oracle.plan_full(f.cpu().numpy() * eps, g.cpu().numpy() * eps, Cf, eps)
+    assert np.abs(Tg - oracle.plan_full(fo, go, Cf, eps)).sum() < 1e-10
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
